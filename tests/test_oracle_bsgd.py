@@ -1,0 +1,288 @@
+"""Pins of the oracle's BSGD layer (§IV fixed point 539-639)
+against closed forms, special cases, independent re-implementations and
+printed values — never against the oracle itself."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import bsgd as ob
+from oracle.projector import BlockGrid, Projector
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------------------- sampler
+def test_splitmix64_kat():
+    want = [int(l, 16) for l in open(os.path.join(GOLDEN, "splitmix64.txt")) if not l.startswith("#")]
+    got = [ob.rnd(0, 0, 0, k) for k in range(4)]
+    assert got == want
+
+
+def test_select_properties_and_uniformity():
+    n, m = 6, 2
+    counts = {}
+    for e in range(6000):
+        s = ob.select(12345, 2, e, n, m)
+        assert s == sorted(s) and len(set(s)) == m and all(0 <= v < n for v in s)
+        counts[tuple(s)] = counts.get(tuple(s), 0) + 1
+    assert len(counts) == math.comb(n, m)
+    exp = 6000 / math.comb(n, m)
+    chi2 = sum((c - exp) ** 2 / exp for c in counts.values())
+    assert chi2 < 45.0                      # 14 dof, p ~ 1e-4
+    assert ob.select(1, 1, 0, 5, 5) == [0, 1, 2, 3, 4]
+    assert sorted(ob.permutation(7, 0, 0, 50)) == list(range(50))
+
+
+def test_view_partition():
+    for kind in ["random", "contiguous", "interleaved"]:
+        rows = ob.view_partition(360, 5, kind, seed=3)
+        flat = sorted(v for r in rows for v in r)
+        assert flat == list(range(360)) and all(len(r) == 72 for r in rows)
+        assert all(r == sorted(r) for r in rows)
+    rows = ob.view_partition(90, 4, "random", seed=1)
+    assert [len(r) for r in rows] == [23, 23, 22, 22]      # first V mod M get +1
+    with pytest.raises(ValueError):
+        ob.view_partition(3, 4)
+
+
+def test_eq8_printed_examples():
+    for line in open(os.path.join(GOLDEN, "eq8.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        t = line.split()
+        node, M, N, alpha, gamma = int(t[0]), int(t[1]), int(t[2]), float(t[3]), float(t[4])
+        aM, gN, a, g = ob.eq8_counts(node, M, N)
+        assert abs(a - alpha) < 1e-12 and abs(g - gamma) < 1e-12
+        assert aM == round(alpha * M) and gN == round(gamma * N)
+    # NodeNum = M N -> alpha = gamma = 1
+    assert ob.eq8_counts(32, 4, 8)[:2] == (4, 8)
+
+
+# --------------------------------------------------------------------------- small systems
+def sec3a_system(M=4, N=2, noise=True):
+    """The paper's §III-A system: 2D fan, K = 16, OP = OD = 50, 30 detectors,
+    10° steps -> A in R^{1080 x 256}; 17.5 dB noise."""
+    vecs = synth.circular("fan", 36, 360.0, 50.0, 50.0, 30, 1, 1.0, 1.0)
+    g = synth.Geometry(synth.FAN, vecs, 30, 1, (16, 16, 1))
+    blocks = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1)}[N]
+    grid = BlockGrid(g.dims, blocks)
+    P = Projector(g, grid)
+    A = P.dense()
+    x_true = synth.rasterise(synth.ellipsoids_world("shepp2d", g.dims), g.dims).ravel()
+    y = A @ x_true
+    if noise:
+        y = synth.gaussian_noise_snr(y, 17.5, seed=5)
+    return g, grid, A, x_true, y
+
+
+def global_of(grid, xb):
+    return grid.from_blocks(xb).ravel()
+
+
+@pytest.mark.parametrize("M,N", [(4, 2), (1, 1)])
+def test_alpha_gamma_one_is_gd_closed_form(M, N):
+    """alpha = gamma = 1 refreshes every z and g_hat, so Algo 1 is GD
+    x_{k+1} = x_k + 2 mu A^T (y - A x_k); closed form via the
+    SVD of A: x_k = sum_i (1 - (1 - 2 mu s_i^2)^k)/s_i (u_i.y) v_i."""
+    g, grid, A, x_true, y = sec3a_system(M, N)
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    mu = 0.5 / s[0] ** 2
+    prm = ob.Params(seed=9, mu=mu, rows_per_epoch=M, cols_per_epoch=N)
+    o = ob.OracleBSGD(g, grid.blocks, M, y, prm, row_kind="random")
+    keep = s > 1e-10 * s[0]
+    uy = U.T @ y
+    f_prev = 0.5 * y @ y
+    for k in range(1, 21):
+        o.epoch()
+        xk = (Vt[keep].T * ((1 - (1 - 2 * mu * s[keep] ** 2) ** k) / s[keep])) @ uy[keep]
+        xg = global_of(grid, o.x)
+        assert np.max(np.abs(xg - xk)) <= 1e-10 * np.max(np.abs(xk))
+        f = 0.5 * np.sum((y - A @ xg) ** 2)
+        assert f <= f_prev * (1 + 1e-12)                   # monotone (mu < 1/s_max^2)
+        # the maintained r of epoch k is y - A x_{k-1} (formed before the step)
+        assert abs(o.log[-1]["obj"] - f_prev) <= 1e-9 * f_prev
+        f_prev = f
+
+
+def test_gamma_one_is_sag():
+    """gamma = 1 makes BSGD SAG ("When gamma = 1, the method becomes
+    SAG"): an independent SAG over the M row blocks with stored gradients."""
+    M, N = 4, 2
+    g, grid, A, x_true, y = sec3a_system(M, N)
+    s0 = np.linalg.norm(A, 2)
+    mu = 0.3 / s0 ** 2
+    prm = ob.Params(seed=4, mu=mu, rows_per_epoch=1, cols_per_epoch=N)
+    o = ob.OracleBSGD(g, grid.blocks, M, y, prm)
+    rows = [o.P.rows_of(r) for r in o.rows]
+    # independent SAG on the dense A (global column order)
+    x = np.zeros(A.shape[1])
+    d = [np.zeros(A.shape[1]) for _ in range(M)]
+    for k in range(60):
+        (i,) = ob.select(4, 1, k, M, 1)
+        Ai = A[rows[i]]
+        d[i] = 2 * Ai.T @ (y[rows[i]] - Ai @ x)
+        x = x + mu * sum(d)
+        o.epoch()
+        assert np.max(np.abs(global_of(grid, o.x) - x)) <= 1e-11 * max(1.0, np.max(np.abs(x)))
+
+
+def test_fixed_point_is_least_squares():
+    """§IV: the state (x_lsq, z^j = A^{J_j} x_lsq,
+    g_hat^i_{J_j} = 2 (A_{I_i}^{J_j})^T (y - A x_lsq)_{I_i}) is a fixed point of
+    every epoch; a perturbed x is not."""
+    M, N = 4, 4
+    g, grid, A, x_true, y = sec3a_system(M, N)
+    x_lsq = np.linalg.lstsq(A, y, rcond=None)[0]
+    s0 = np.linalg.norm(A, 2)
+    prm = ob.Params(seed=2, mu=0.5 / s0 ** 2, rows_per_epoch=2, cols_per_epoch=2)
+
+    def make(xg):
+        o = ob.OracleBSGD(g, grid.blocks, M, y, prm, row_kind="interleaved")
+        o.x = grid.to_blocks(xg.reshape(1, 16, 16))
+        views_all = np.arange(g.n_views)
+        for j in range(N):
+            o.z[j] = o.P.fp(views_all, j, o.x[j])
+        o.r = y - o.z.sum(0)
+        for i in range(M):
+            for j in range(N):
+                o.ghat[i, j] = 2 * o.P.bp(o.rows[i], j, o.r)
+        o.g = o.ghat.sum(0)
+        return o
+
+    o = make(x_lsq)
+    x0 = o.x.copy()
+    assert np.max(np.abs(o.g)) < 1e-9 * np.max(np.abs(o.ghat))      # A^T r = 0 at x_lsq
+    for _ in range(30):
+        o.epoch()
+    assert np.max(np.abs(o.x - x0)) <= 1e-10 * np.max(np.abs(x0))
+    o2 = make(x_lsq + 1e-3 * np.random.default_rng(0).standard_normal(x_lsq.shape))
+    xp = o2.x.copy()
+    for _ in range(30):
+        o2.epoch()
+    assert np.max(np.abs(o2.x - xp)) > 1e-6
+
+
+def test_tiles_one_im_equals_bsgd():
+    """A single sub-detector tile makes Algo 2 identical to Algo 1."""
+    g, grid, A, x_true, y = sec3a_system(4, 4, noise=False)
+    s0 = np.linalg.norm(A, 2)
+    base = dict(seed=8, mu=0.5 / s0 ** 2, rows_per_epoch=1, cols_per_epoch=2)
+    o1 = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(**base))
+    o2 = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(im=True, **base), tiles=(1, 1))
+    for _ in range(10):
+        o1.epoch()
+        o2.epoch()
+    assert np.array_equal(o1.x, o2.x)
+
+
+def test_im_table_and_containment():
+    """IM weights: each row sums to 2^16 up to the floor (<= T); a block whose
+    shadow lies inside one tile gets all the weight."""
+    vecs = synth.circular("parallel", 8, 180.0, 0, 0, 64, 1, 1.0, 1.0)
+    g = synth.Geometry(synth.PARALLEL, vecs, 64, 1, (64, 64, 1))
+    P = Projector(g, BlockGrid(g.dims, (1, 2, 1)))       # halves along y
+    q = ob.im_table(P, (2, 1))
+    assert np.all(q.sum(axis=2) <= ob.IM_SCALE) and np.all(q.sum(axis=2) >= ob.IM_SCALE - 2)
+    # view 0: rays along -x at y = iu - 31.5; detector half 0 sees exactly block 0
+    assert list(q[0, 0]) == [ob.IM_SCALE, 0] and list(q[1, 0]) == [0, ob.IM_SCALE]
+
+
+def test_im_epoch_touches_only_tile_rows():
+    g, grid, A, x_true, y = sec3a_system(4, 4, noise=False)
+    prm = ob.Params(seed=3, mu=1e-4, rows_per_epoch=1, cols_per_epoch=2, im=True)
+    o = ob.OracleBSGD(g, grid.blocks, 4, y, prm, tiles=(2, 1))
+    o.x[:] = 1.0
+    rec = o.epoch()
+    rows_hit = set()
+    for (j, v), t in rec["tiles"].items():
+        u0, u1, _, _ = o.rects[t]
+        nz = np.nonzero(o.z[j].reshape(g.n_views, 30)[v])[0]
+        assert np.all((nz >= u0) & (nz < u1))
+        rows_hit.add(j)
+    assert rows_hit == set(rec["cols"])
+
+
+# --------------------------------------------------------------------------- TV
+def test_tv_grad_adjoint():
+    rng = np.random.default_rng(1)
+    for shape in [(1, 7, 9), (4, 5, 6)]:
+        u = rng.standard_normal(shape)
+        p = rng.standard_normal((3,) + shape)
+        assert abs(np.sum(ob.tv_grad(u) * p) - np.sum(u * ob.tv_grad_T(p))) < 1e-10
+
+
+def test_tv_prox_closed_forms():
+    """w = 0 -> identity; constant image unchanged; image constant along y with a
+    step between x-runs of lengths L1, L2 -> exact 1D ROF: levels move by w/L1 and
+    w/L2 toward each other until they meet (TV of Eq. 6 with a zero boundary
+    difference)."""
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal((1, 8, 8))
+    assert np.array_equal(ob.tv_prox(b, 0.0), b)
+    c = np.full((1, 8, 8), 3.25)
+    assert np.max(np.abs(ob.tv_prox(c, 0.7) - c)) < 1e-12
+    step = np.zeros((1, 8, 8))
+    step[..., 4:] = 1.0
+    for w, lo, hi in [(0.5, 0.125, 0.875), (3.0, 0.5, 0.5)]:
+        t = ob.tv_prox(step, w, iters=20000)
+        assert np.max(np.abs(t[..., :4] - lo)) < 1e-9 and np.max(np.abs(t[..., 4:] - hi)) < 1e-9
+    # unequal runs L1 = 2, L2 = 6 (3D volume, step along x, constant in y and z)
+    s3 = np.zeros((3, 4, 8))
+    s3[..., 2:] = 1.0
+    t = ob.tv_prox(s3, 0.2, iters=20000)
+    assert np.max(np.abs(t[..., :2] - 0.1)) < 1e-8 and np.max(np.abs(t[..., 2:] - (1 - 0.2 / 6))) < 1e-8
+
+
+def test_tv_prox_20_iterations_improves_objective():
+    rng = np.random.default_rng(2)
+    img = synth.rasterise(synth.ellipsoids_world("shepp2d", (32, 32, 1)), (32, 32, 1))
+    b = img + 0.1 * rng.standard_normal(img.shape)
+    w = 0.05
+    obj = lambda t: 0.5 * np.sum((t - b) ** 2) + w * ob.tv_value(t)
+    t = ob.tv_prox(b, w, 20)
+    assert obj(t) < obj(b)
+    # non-expansive (prox of a convex function)
+    b2 = b + 0.05 * rng.standard_normal(b.shape)
+    t_many = ob.tv_prox(b, w, 3000)
+    t2_many = ob.tv_prox(b2, w, 3000)
+    assert np.linalg.norm(t_many - t2_many) <= np.linalg.norm(b - b2) * (1 + 1e-6)
+
+
+# --------------------------------------------------------------------------- Algo 3
+def test_auto_mu_decisions():
+    """Algo 3 lines 5-12 on scripted |r| and theta."""
+    kw = dict(eps=0.05, delta=0.4, t1=0.5, t2=0.0)
+    # |r| decreasing twice -> increase
+    assert ob.auto_mu_decision(1.0, 1.0, 2.0, 3.0, 0.9, 0.9, **kw) == pytest.approx(1.05)
+    # |r| increasing twice and theta < t2 -> decrease
+    assert ob.auto_mu_decision(1.0, 3.0, 2.0, 1.0, -0.1, 0.9, **kw) == pytest.approx(0.6)
+    # increasing twice and |theta - theta_prev| > t1 -> decrease
+    assert ob.auto_mu_decision(1.0, 3.0, 2.0, 1.0, 0.2, 0.9, **kw) == pytest.approx(0.6)
+    # increasing twice but theta stable and positive -> unchanged (criterion 2 fails)
+    assert ob.auto_mu_decision(1.0, 3.0, 2.0, 1.0, 0.8, 0.9, **kw) == 1.0
+    # mixed -> unchanged; equalities are not strict monotonicity
+    assert ob.auto_mu_decision(1.0, 2.0, 3.0, 2.5, -1.0, 0.9, **kw) == 1.0
+    assert ob.auto_mu_decision(1.0, 2.0, 2.0, 2.0, -1.0, 0.9, **kw) == 1.0
+    # undefined theta: only theta < t2 could fire, and it is undefined -> unchanged
+    assert ob.auto_mu_decision(1.0, 3.0, 2.0, 1.0, None, None, **kw) == 1.0
+    assert ob.auto_mu_decision(1.0, 3.0, 2.0, 1.0, -0.5, None, **kw) == pytest.approx(0.6)
+
+
+def test_auto_mu_recovers_from_large_step():
+    """Survey-time behaviour: from mu0 = 4/s_max^2 fixed-step BSGD
+    diverges while auto-mu brings the objective down."""
+    g, grid, A, x_true, y = sec3a_system(4, 2, noise=False)
+    s0 = np.linalg.norm(A, 2)
+    base = dict(seed=1, mu=4.0 / s0 ** 2, rows_per_epoch=1, cols_per_epoch=1)
+    fixed = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(**base))
+    auto = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(auto_mu=True, **base))
+    for _ in range(300):
+        fixed.epoch()
+        auto.epoch()
+    f0 = 0.5 * y @ y
+    assert fixed.log[-1]["obj"] > f0
+    assert auto.log[-1]["obj"] < 0.05 * f0
+    assert auto.log[-1]["mu"] < base["mu"]
