@@ -1,0 +1,227 @@
+/*
+ * bsgd.h — C ABI of the B200-native BSGD hot path (Gao, Biguri, Blumensath,
+ * arXiv 1903.11874, "Block stochastic gradient descent for large-scale
+ * tomographic reconstruction in a parallel network").
+ *
+ * Problem (§I, Eq. 1-2):  min_x 1/2 ||y - A x||^2, where A is the
+ * non-negative Siddon system matrix, never stored: A x (forward projection, FP)
+ * and A^T r (back projection, BP) are computed on the fly by CUDA kernels.
+ * Partition (§II, Eq. 3): M row blocks I_i (sets of whole views,
+ * PAPER.md:449) x N column blocks J_j (equal boxes of a bx x by x bz grid).
+ *
+ * Conventions shared by every call
+ *  - Units: voxel edge = 1; volume centred at the rotation centre; voxel
+ *    (ix,iy,iz) covers [ix - nx/2, ix+1 - nx/2) x ... (half-open).
+ *  - Projections: float32, layout [view][v][u] (u fastest), ray id
+ *    (view*det_v + iv)*det_u + iu, full length n_views*det_v*det_u.
+ *  - Images: float32, BLOCK-MAJOR: block j = (jz*by + jy)*bx + jx, then
+ *    [z][y][x] inside the block.  For z-slab grids (1,1,N) this is the plain
+ *    [z][y][x] volume.  A rank owns the contiguous blocks
+ *    [rank*N/world, (rank+1)*N/world); "x_owned" is those blocks back to back.
+ *  - Pointers: "device" = CUDA device memory of the ctx's device; "host" = CPU
+ *    memory.  bsgd_run accepts y / x_owned / x_true in either (detected with
+ *    cudaPointerGetAttributes; host buffers are copied in and x copied back).
+ *  - Streams: every enqueueing call takes a cudaStream_t as void* (NULL = the
+ *    legacy default stream).  Calls are asynchronous unless stated otherwise.
+ *  - Ownership: the caller owns every buffer it passes; the ctx owns its
+ *    internal state (z^j, g_hat^i, g, r, transposed image copy, scratch),
+ *    allocated at create through `bsgd_alloc` (NULL = cudaMalloc).
+ *  - Errors: every call returns bsgd_status; nothing throws across the ABI.
+ *    Invalid arguments are rejected before any device work (state unchanged).
+ *    A CUDA or NCCL failure poisons the ctx (BSGD_E_POISONED afterwards).
+ *    bsgd_last_error() gives a message.
+ *  - Concurrency: one ctx per process per GPU; not thread-safe.  Collective
+ *    calls (bsgd_create with world > 1, bsgd_step, bsgd_run) must be issued in
+ *    the same order on every rank.
+ */
+#ifndef BSGD_H
+#define BSGD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSGD_ABI_VERSION 1
+
+typedef struct bsgd_ctx_s* bsgd_ctx;
+
+typedef enum {
+    BSGD_OK = 0,
+    BSGD_E_GEOMETRY = 1,   /* n_views < 1, zero detector elements, non-finite vectors, zero ray direction */
+    BSGD_E_PARTITION = 2,  /* M < 1 or M > n_views, dims not divisible by the block grid, N % world != 0   */
+    BSGD_E_DIMENSION = 3,  /* block / row block / view id out of range, rect outside the detector          */
+    BSGD_E_CONTRACT = 4,   /* invalid selection (duplicate / unsorted), mu not finite, bad flags            */
+    BSGD_E_CUDA = 5,
+    BSGD_E_NCCL = 6,
+    BSGD_E_OOM = 7,
+    BSGD_E_POISONED = 8
+} bsgd_status;
+
+typedef enum { BSGD_PARALLEL = 0, BSGD_FAN = 1, BSGD_CONE = 2 } bsgd_beam;
+
+/* Scan geometry (Fig. 3; §III-E).  vecs: host
+ * fp64 [n_views][12] = {src (fan/cone) or unit ray direction (parallel),
+ * detector centre, detector u step, detector v step}, copied at create.
+ * Ray (view, iv, iu) passes through det + (iu-(nu-1)/2) u + (iv-(nv-1)/2) v;
+ * fan/cone rays start at src; 2D = det_v 1 and nz 1.                          */
+typedef struct { int32_t beam, n_views, det_u, det_v; const double* vecs; } bsgd_geometry;
+typedef struct { int32_t nx, ny, nz; } bsgd_dims;
+typedef struct { int32_t bx, by, bz; } bsgd_block_grid;
+/* Row blocks ("randomly partitioned the 360 projections into 5
+ * groups"): kind 0 = seeded random partition, 1 = contiguous, 2 = interleaved.
+ * tiles_u x tiles_v = sub-detector tiles of BSGD-IM (Fig. 2). */
+typedef struct { int32_t M, kind; uint64_t seed; int32_t tiles_u, tiles_v; } bsgd_row_grid;
+/* Multi-GPU: one process per GPU; nccl_id = 128 bytes from bsgd_nccl_unique_id
+ * on rank 0, broadcast by the caller (NULL when world == 1).                 */
+typedef struct { int32_t rank, world; const uint8_t* nccl_id; } bsgd_dist;
+/* Device allocator used for ALL ctx state (Python points it at the torch
+ * caching allocator).  NULL = cudaMalloc/cudaFree.                           */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* stream, void* user);
+    void (*free)(void* ptr, size_t bytes, void* stream, void* user);
+    void* user;
+} bsgd_alloc;
+
+/* ---- pure host functions (no ctx, no device) ---------------------------- */
+int32_t bsgd_abi_version(void);
+/* Number of CUDA kernels this library has launched in this process (all
+ * contexts); the bench reports the count inside its timed region.           */
+uint64_t bsgd_kernel_launches(void);
+const char* bsgd_last_error(bsgd_ctx ctx /* NULL = thread-local last error */);
+/* Circular orbit per-view vectors: theta_v = v*arc/n_views
+ * degrees with exact-quadrant trig; src = OP(cos,sin,0), det = -OD(cos,sin,0),
+ * u = pitch_u(-sin,cos,0), v = pitch_v(0,0,1); parallel: dir = -(cos,sin,0),
+ * det = 0.  vecs_out: host [n_views][12].                                     */
+bsgd_status bsgd_geometry_circular(int32_t beam, int32_t n_views, double arc_deg, double OP, double OD,
+                                   int32_t det_u, int32_t det_v, double pitch_u, double pitch_v,
+                                   double* vecs_out);
+/* SplitMix64 counter RNG (reading A3): m of n without replacement, sorted.
+ * stream 0 = view partition, 1 = row blocks, 2 = column blocks, 3 = IM tiles. */
+bsgd_status bsgd_sample(uint64_t seed, int32_t stream, int32_t epoch, int32_t n, int32_t m, int32_t* out);
+/* Row-block partition: views_out [n_views] (blocks back to back, each sorted),
+ * offsets_out [M+1].                                                          */
+bsgd_status bsgd_view_partition(int32_t n_views, int32_t M, int32_t kind, uint64_t seed,
+                                int32_t* views_out, int32_t* offsets_out);
+/* Eq. 8: gamma = min{1, nodes/N}, alpha = nodes/(M N gamma);
+ * counts alpha*M and gamma*N rounded half up, at least 1 (reading A4).        */
+bsgd_status bsgd_eq8(int32_t nodes, int32_t M, int32_t N, int32_t* rows_per_epoch, int32_t* cols_per_epoch);
+/* Blocks owned by a rank: [*first, *first + *count).                          */
+bsgd_status bsgd_owned_blocks(int32_t N, int32_t world, int32_t rank, int32_t* first, int32_t* count);
+/* 128-byte NCCL unique id (call on rank 0 only, then broadcast).             */
+bsgd_status bsgd_nccl_unique_id(uint8_t* out128);
+
+/* ---- context ------------------------------------------------------------- */
+bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks,
+                        bsgd_row_grid rows, const bsgd_dist* dist /* NULL = single GPU */,
+                        const bsgd_alloc* alloc /* NULL = cudaMalloc */, bsgd_ctx* out);
+void bsgd_destroy(bsgd_ctx ctx);
+
+typedef struct {
+    int32_t N, M, n_views, det_u, det_v, owned_first, owned_count, tiles;
+    int64_t block_voxels, n_rays, owned_voxels;
+    int32_t block_dims[3];
+    uint64_t device_bytes;   /* bytes of ctx-owned device state */
+} bsgd_info;
+bsgd_status bsgd_get_info(bsgd_ctx ctx, bsgd_info* out);
+/* Views of row block i: out [n] (n = size of I_i, sorted); *n returns the size. */
+bsgd_status bsgd_row_block_views(bsgd_ctx ctx, int32_t i, int32_t* out, int32_t* n);
+
+/* ---- single operators (no collective; device pointers; caller's stream) ---
+ * views: host [n_views] view ids; rects: host [n_views][4] detector rect
+ * (u0,u1,v0,v1) half-open per view, or NULL = whole detector.
+ * bsgd_forward: proj[rays] (=|+=) A_{views,rects}^{J_j} x_block      (Algo 1 l.5)
+ *   x_block: device block j (block layout); proj: device, full length; rays
+ *   outside the views/rects are not touched.
+ * bsgd_back:    g_block (=|+=) scale * (A_{views,rects}^{J_j})^T proj (Algo 1 l.9, PAPER.md:143;
+ *   the algorithm uses scale = 2).                                            */
+bsgd_status bsgd_forward(bsgd_ctx ctx, int32_t n_views, const int32_t* views, const int32_t* rects,
+                         int32_t col_block, const float* x_block, float* proj, int32_t accumulate,
+                         void* stream);
+bsgd_status bsgd_back(bsgd_ctx ctx, int32_t n_views, const int32_t* views, const int32_t* rects,
+                      int32_t col_block, const float* proj, float* g_block, float scale,
+                      int32_t accumulate, void* stream);
+/* Exact per-(owned block, view, tile) ones-pass masses w = sum over the tile's
+ * rays of the chord through the block box (the L1 norm of A_tile^J; reading A9),
+ * and the integer importance table q = floor(2^16 w / sum_t w) used by the
+ * sampler.  host out: [owned_count][n_views][tiles].                        */
+bsgd_status bsgd_im_weights(bsgd_ctx ctx, double* w_out, uint32_t* q_out);
+
+/* ---- algorithm state ------------------------------------------------------ */
+/* Algo 1 line 1: z^j = 0, g_hat^i = 0, g = 0, r = y, epoch = 0.
+ * y: device, full length, replicated on every rank.                          */
+bsgd_status bsgd_reset(bsgd_ctx ctx, const float* y, void* stream);
+
+enum {
+    BSGD_IS = 1,            /* BSGD-IM, Algo 2                     */
+    BSGD_IS_UNIFORM = 2,    /* BSGD-RAN: uniform tile draws            */
+    BSGD_TV = 4,            /* BSGD-TV, Algo 4                     */
+    BSGD_AUTO_MU = 8,       /* Algo 3                             */
+    BSGD_SGD = 16,          /* Eq. 4 mini-batch SGD baseline       */
+    BSGD_RESUME = 32,       /* bsgd_run: continue from the current state (no reset)   */
+    BSGD_TIMING = 64        /* bsgd_run: per-phase CUDA-event times into the log      */
+};
+
+/* One epoch of Algo 1 / Algo 2 with an explicit selection (identical on all
+ * ranks).  rows: sorted row-block ids; cols: sorted column-block ids;
+ * im_tiles: NULL (Algo 1) or host [n_cols][V_sel] tile ids, V_sel = number of
+ * views of the selected row blocks in ascending row-block order (Algo 2 l.5).
+ * flags: BSGD_SGD only.  Contains the residual allreduce when world > 1.     */
+typedef struct {
+    int32_t n_rows; const int32_t* rows;
+    int32_t n_cols; const int32_t* cols;
+    const int32_t* im_tiles;
+} bsgd_selection;
+bsgd_status bsgd_step(bsgd_ctx ctx, const float* y, float* x_owned, const bsgd_selection* sel,
+                      float mu, uint32_t flags, void* stream);
+
+typedef struct {
+    uint64_t seed;
+    int32_t epochs;
+    int32_t rows_per_epoch, cols_per_epoch;   /* alpha*M, gamma*N; 0 = Eq. 8 with NodeNum = world */
+    double mu0;
+    uint32_t flags;
+    double lambda;                            /* TV weight lambda of Eq. 5          */
+    int32_t tv_iters, tv_period;              /* FGP iterations (20); period 0 = round(1/(alpha gamma)) */
+    double eps, delta, t1, t2;                /* Algo 3 constants (reading A12: .05, .4, .5, 0)   */
+    int32_t is_off_last_epochs;               /* final epochs without IS           */
+} bsgd_run_params;
+
+/* Per-epoch log; every pointer is host memory and nullable.                  */
+typedef struct {
+    double* obj;        /* [epochs] 1/2 ||r||^2 of the maintained r (reading A30)       */
+    double* rmse;       /* [epochs] RMSE(x, x_true) over all voxels (needs x_true)       */
+    double* mu;         /* [epochs] step used in the epoch                              */
+    int32_t* sel_rows;  /* [epochs][rows_per_epoch]                                     */
+    int32_t* sel_cols;  /* [epochs][cols_per_epoch]                                     */
+    uint64_t* visits;   /* [epochs] FP ray-voxel intersections (BP visits are equal)     */
+    double* t_ms;       /* [epochs][6] fp, residual(+allreduce), bp, step, tv, total     */
+} bsgd_run_log;
+
+/* Run params->epochs epochs of BSGD (Algo 1) or its variants selected by
+ * flags, sampling with the counter RNG from params->seed.  y, x_owned, x_true
+ * may be host or device pointers (host: copied in / x copied back).
+ * Synchronises `stream` before returning (the log is host memory).           */
+bsgd_status bsgd_run(bsgd_ctx ctx, const float* y, float* x_owned, const float* x_true,
+                     const bsgd_run_params* params, bsgd_run_log* log, void* stream);
+
+/* Inspection (tests): copy internal state to / from host memory.
+ * what: 0 = z^j of owned block slot `index` (n_rays floats);
+ *       1 = g_hat^i of (i = index / owned_count, owned slot = index % owned_count);
+ *       2 = g of owned slot `index`;  3 = r (n_rays floats);
+ *       4 = per-row-block ||r_I||^2 (M doubles);  5 = current mu (1 double).
+ * bytes must match the item's size exactly.  Synchronous.                    */
+bsgd_status bsgd_get_state(bsgd_ctx ctx, int32_t what, int32_t index, void* host_dst, size_t bytes);
+bsgd_status bsgd_set_state(bsgd_ctx ctx, int32_t what, int32_t index, const void* host_src, size_t bytes);
+
+/* sigma_max(A)^2 by `iters` power iterations on A^T A (all views, all blocks;
+ * collective when world > 1).  Synchronous.                                   */
+bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, double* sigma_max_sq,
+                                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSGD_H */

@@ -1,0 +1,398 @@
+"""B200-native BSGD hot path (Gao, Biguri, Blumensath, arXiv 1903.11874).
+
+Thin ctypes binding over ``libbsgd.so`` (the C ABI declared in
+``include/bsgd.h``).  Argument marshalling only: every step of the path runs in
+the library's CUDA kernels.  PyTorch supplies device memory (the library's
+state is allocated through the torch caching allocator), streams and the
+process group used to broadcast the NCCL id.
+
+There is deliberately no CPU fallback: importing this package without the
+built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbsgd.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc, sm_100a). There is no CPU fallback.")
+
+_lib = C.CDLL(LIB_PATH)
+
+PARALLEL, FAN, CONE = 0, 1, 2
+IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING = 1, 2, 4, 8, 16, 32, 64
+STATUS = {0: "OK", 1: "E_GEOMETRY", 2: "E_PARTITION", 3: "E_DIMENSION", 4: "E_CONTRACT", 5: "E_CUDA",
+          6: "E_NCCL", 7: "E_OOM", 8: "E_POISONED"}
+
+
+class BsgdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"bsgd {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+# ---------------------------------------------------------------- C structs
+class Geometry(C.Structure):
+    _fields_ = [("beam", C.c_int32), ("n_views", C.c_int32), ("det_u", C.c_int32), ("det_v", C.c_int32),
+                ("vecs", C.POINTER(C.c_double))]
+
+
+class Dims(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32)]
+
+
+class BlockGrid(C.Structure):
+    _fields_ = [("bx", C.c_int32), ("by", C.c_int32), ("bz", C.c_int32)]
+
+
+class RowGrid(C.Structure):
+    _fields_ = [("M", C.c_int32), ("kind", C.c_int32), ("seed", C.c_uint64), ("tiles_u", C.c_int32),
+                ("tiles_v", C.c_int32)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8))]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class Alloc(C.Structure):
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", C.c_void_p)]
+
+
+class Info(C.Structure):
+    _fields_ = [("N", C.c_int32), ("M", C.c_int32), ("n_views", C.c_int32), ("det_u", C.c_int32),
+                ("det_v", C.c_int32), ("owned_first", C.c_int32), ("owned_count", C.c_int32),
+                ("tiles", C.c_int32), ("block_voxels", C.c_int64), ("n_rays", C.c_int64),
+                ("owned_voxels", C.c_int64), ("block_dims", C.c_int32 * 3), ("device_bytes", C.c_uint64)]
+
+
+class Selection(C.Structure):
+    _fields_ = [("n_rows", C.c_int32), ("rows", C.POINTER(C.c_int32)), ("n_cols", C.c_int32),
+                ("cols", C.POINTER(C.c_int32)), ("im_tiles", C.POINTER(C.c_int32))]
+
+
+class RunParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("epochs", C.c_int32), ("rows_per_epoch", C.c_int32),
+                ("cols_per_epoch", C.c_int32), ("mu0", C.c_double), ("flags", C.c_uint32),
+                ("lambda_", C.c_double), ("tv_iters", C.c_int32), ("tv_period", C.c_int32),
+                ("eps", C.c_double), ("delta", C.c_double), ("t1", C.c_double), ("t2", C.c_double),
+                ("is_off_last_epochs", C.c_int32)]
+
+
+class RunLog(C.Structure):
+    _fields_ = [("obj", C.POINTER(C.c_double)), ("rmse", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
+                ("sel_rows", C.POINTER(C.c_int32)), ("sel_cols", C.POINTER(C.c_int32)),
+                ("visits", C.POINTER(C.c_uint64)), ("t_ms", C.POINTER(C.c_double))]
+
+
+P = C.POINTER
+_ctx = C.c_void_p
+SIGS = {
+    "bsgd_abi_version": ([], C.c_int32),
+    "bsgd_kernel_launches": ([], C.c_uint64),
+    "bsgd_last_error": ([_ctx], C.c_char_p),
+    "bsgd_geometry_circular": ([C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_int32,
+                                C.c_double, C.c_double, P(C.c_double)], C.c_int),
+    "bsgd_sample": ([C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32)], C.c_int),
+    "bsgd_view_partition": ([C.c_int32, C.c_int32, C.c_int32, C.c_uint64, P(C.c_int32), P(C.c_int32)], C.c_int),
+    "bsgd_eq8": ([C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+    "bsgd_owned_blocks": ([C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+    "bsgd_nccl_unique_id": ([P(C.c_uint8)], C.c_int),
+    "bsgd_create": ([P(Geometry), Dims, BlockGrid, RowGrid, P(Dist), P(Alloc), P(_ctx)], C.c_int),
+    "bsgd_destroy": ([_ctx], None),
+    "bsgd_get_info": ([_ctx, P(Info)], C.c_int),
+    "bsgd_row_block_views": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+    "bsgd_forward": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                      C.c_void_p], C.c_int),
+    "bsgd_back": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p, C.c_float,
+                   C.c_int32, C.c_void_p], C.c_int),
+    "bsgd_im_weights": ([_ctx, P(C.c_double), P(C.c_uint32)], C.c_int),
+    "bsgd_reset": ([_ctx, C.c_void_p, C.c_void_p], C.c_int),
+    "bsgd_step": ([_ctx, C.c_void_p, C.c_void_p, P(Selection), C.c_float, C.c_uint32, C.c_void_p], C.c_int),
+    "bsgd_run": ([_ctx, C.c_void_p, C.c_void_p, C.c_void_p, P(RunParams), P(RunLog), C.c_void_p], C.c_int),
+    "bsgd_get_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
+    "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
+    "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
+}
+for _name, (_args, _res) in SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def _check(code, ctx=None):
+    if code != 0:
+        msg = _lib.bsgd_last_error(ctx)
+        raise BsgdError(code, msg.decode() if msg else "")
+
+
+def _i32(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    return a, a.ctypes.data_as(P(C.c_int32))
+
+
+def _ptr(t):
+    """Device or host address of a torch tensor / numpy array / int."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------- pure host functions
+def abi_version() -> int:
+    return _lib.bsgd_abi_version()
+
+
+def kernel_launches() -> int:
+    """Kernels this library launched so far in this process."""
+    return int(_lib.bsgd_kernel_launches())
+
+
+def geometry_circular(beam, n_views, arc_deg, OP, OD, det_u, det_v, pitch_u, pitch_v) -> np.ndarray:
+    out = np.zeros((n_views, 12), dtype=np.float64)
+    b = {"parallel": PARALLEL, "fan": FAN, "cone": CONE}.get(beam, beam)
+    _check(_lib.bsgd_geometry_circular(int(b), n_views, arc_deg, OP, OD, det_u, det_v, pitch_u, pitch_v,
+                                       out.ctypes.data_as(P(C.c_double))))
+    return out
+
+
+def sample(seed, stream, epoch, n, m) -> list[int]:
+    out = np.zeros(max(m, 1), dtype=np.int32)
+    _check(_lib.bsgd_sample(seed, stream, epoch, n, m, out.ctypes.data_as(P(C.c_int32))))
+    return out[:m].tolist()
+
+
+def view_partition(n_views, M, kind=0, seed=0) -> list[list[int]]:
+    v = np.zeros(n_views, dtype=np.int32)
+    o = np.zeros(M + 1, dtype=np.int32)
+    kind = {"random": 0, "contiguous": 1, "interleaved": 2}.get(kind, kind)
+    _check(_lib.bsgd_view_partition(n_views, M, int(kind), seed, v.ctypes.data_as(P(C.c_int32)),
+                                    o.ctypes.data_as(P(C.c_int32))))
+    return [v[o[i]:o[i + 1]].tolist() for i in range(M)]
+
+
+def eq8(nodes, M, N) -> tuple[int, int]:
+    a, g = C.c_int32(), C.c_int32()
+    _check(_lib.bsgd_eq8(nodes, M, N, C.byref(a), C.byref(g)))
+    return a.value, g.value
+
+
+def owned_blocks(N, world, rank) -> tuple[int, int]:
+    f, c = C.c_int32(), C.c_int32()
+    _check(_lib.bsgd_owned_blocks(N, world, rank, C.byref(f), C.byref(c)))
+    return f.value, c.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.bsgd_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def dist_from_process_group():
+    """(rank, world, nccl_id) with the id made on rank 0 and broadcast through
+    the current torch.distributed process group."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if world == 1:
+        return 0, 1, None
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0)
+    return rank, world, bytes(t.cpu().numpy().tobytes())
+
+
+# ---------------------------------------------------------------- torch allocator bridge
+class _TorchAllocator:
+    def __init__(self, device):
+        import torch
+        self.device = device
+        self.torch = torch
+
+        def _alloc(nbytes, stream, user):
+            try:
+                return self.torch.cuda.caching_allocator_alloc(int(nbytes), self.device)
+            except Exception:
+                return None
+
+        def _free(ptr, nbytes, stream, user):
+            try:
+                self.torch.cuda.caching_allocator_delete(int(ptr))
+            except Exception:
+                pass
+
+        self._a = ALLOC_FN(_alloc)
+        self._f = FREE_FN(_free)
+        self.struct = Alloc(self._a, self._f, None)
+
+
+# ---------------------------------------------------------------- context
+@dataclass
+class RunResult:
+    obj: np.ndarray
+    rmse: np.ndarray
+    mu: np.ndarray
+    sel_rows: np.ndarray
+    sel_cols: np.ndarray
+    visits: np.ndarray
+    t_ms: Optional[np.ndarray]
+
+
+class Context:
+    """One BSGD problem on this process's GPU (bsgd_create ... bsgd_destroy)."""
+
+    def __init__(self, beam, vecs, det, dims, blocks, M, kind=0, row_seed=0, tiles=(1, 1),
+                 rank=0, world=1, nccl_id=None, torch_alloc=True, device=None):
+        import torch
+        self.device = torch.cuda.current_device() if device is None else device
+        self.vecs = np.ascontiguousarray(vecs, dtype=np.float64)
+        b = {"parallel": PARALLEL, "fan": FAN, "cone": CONE}.get(beam, beam)
+        kind = {"random": 0, "contiguous": 1, "interleaved": 2}.get(kind, kind)
+        g = Geometry(int(b), self.vecs.shape[0], int(det[0]), int(det[1]), self.vecs.ctypes.data_as(P(C.c_double)))
+        self._idbuf = None
+        dist = None
+        if world > 1:
+            self._idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            dist = Dist(rank, world, C.cast(self._idbuf, P(C.c_uint8)))
+        self._alloc = _TorchAllocator(self.device) if torch_alloc else None
+        h = _ctx()
+        with torch.cuda.device(self.device):
+            _check(_lib.bsgd_create(C.byref(g), Dims(*dims), BlockGrid(*blocks),
+                                    RowGrid(M, int(kind), row_seed, int(tiles[0]), int(tiles[1])),
+                                    C.byref(dist) if dist else None,
+                                    C.byref(self._alloc.struct) if self._alloc else None, C.byref(h)))
+        self.h = h
+        inf = Info()
+        _check(_lib.bsgd_get_info(self.h, C.byref(inf)), self.h)
+        self.info = inf
+        self.N, self.M = inf.N, inf.M
+        self.block_voxels = inf.block_voxels
+        self.n_rays = inf.n_rays
+        self.owned_first, self.owned_count = inf.owned_first, inf.owned_count
+        self.block_dims = tuple(inf.block_dims)
+        self.det = (int(det[0]), int(det[1]))
+
+    @classmethod
+    def from_geometry(cls, geom, blocks, M, **kw):
+        """geom: synth.Geometry-like (beam, vecs, det_u, det_v, dims)."""
+        return cls(geom.beam, geom.vecs, (geom.det_u, geom.det_v), geom.dims, blocks, M, **kw)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.bsgd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, code):
+        _check(code, self.h)
+
+    def row_block_views(self, i) -> list[int]:
+        n = C.c_int32()
+        self._c(_lib.bsgd_row_block_views(self.h, i, None, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int32)
+        self._c(_lib.bsgd_row_block_views(self.h, i, out.ctypes.data_as(P(C.c_int32)), C.byref(n)))
+        return out.tolist()
+
+    def forward(self, views, col_block, x_block, proj, rects=None, accumulate=False, stream=None):
+        v, vp = _i32(views)
+        r, rp = _i32(rects) if rects is not None else (None, None)
+        self._c(_lib.bsgd_forward(self.h, len(v), vp, rp, col_block, _ptr(x_block), _ptr(proj), int(accumulate),
+                                  _stream(stream)))
+
+    def back(self, views, col_block, proj, g_block, rects=None, scale=1.0, accumulate=False, stream=None):
+        v, vp = _i32(views)
+        r, rp = _i32(rects) if rects is not None else (None, None)
+        self._c(_lib.bsgd_back(self.h, len(v), vp, rp, col_block, _ptr(proj), _ptr(g_block), float(scale),
+                               int(accumulate), _stream(stream)))
+
+    def im_weights(self):
+        T = self.info.tiles
+        n = self.owned_count * self.info.n_views * T
+        w = np.zeros(n, dtype=np.float64)
+        q = np.zeros(n, dtype=np.uint32)
+        self._c(_lib.bsgd_im_weights(self.h, w.ctypes.data_as(P(C.c_double)), q.ctypes.data_as(P(C.c_uint32))))
+        shape = (self.owned_count, self.info.n_views, T)
+        return w.reshape(shape), q.reshape(shape)
+
+    def reset(self, y, stream=None):
+        self._c(_lib.bsgd_reset(self.h, _ptr(y), _stream(stream)))
+
+    def step(self, y, x, rows, cols, mu, tiles=None, sgd=False, stream=None):
+        r, rp = _i32(rows)
+        c, cp = _i32(cols if cols is not None else [])
+        t, tp = _i32(tiles) if tiles is not None else (None, None)
+        sel = Selection(len(r), rp, len(c), cp, tp)
+        self._c(_lib.bsgd_step(self.h, _ptr(y), _ptr(x), C.byref(sel), float(mu), SGD if sgd else 0,
+                               _stream(stream)))
+
+    def run(self, y, x, epochs, mu0, seed=1, x_true=None, rows_per_epoch=0, cols_per_epoch=0, flags=0,
+            lam=0.1, tv_iters=20, tv_period=0, eps=0.05, delta=0.4, t1=0.5, t2=0.0, is_off_last=0,
+            stream=None) -> RunResult:
+        prm = RunParams(seed, epochs, rows_per_epoch, cols_per_epoch, mu0, flags, lam, tv_iters, tv_period,
+                        eps, delta, t1, t2, is_off_last)
+        aM = rows_per_epoch or eq8(self.info.N // self.owned_count, self.M, self.N)[0]
+        gN = cols_per_epoch or eq8(self.info.N // self.owned_count, self.M, self.N)[1]
+        E = max(epochs, 1)
+        obj, rmse, mu = np.zeros(E), np.zeros(E), np.zeros(E)
+        sr = np.zeros(E * aM, dtype=np.int32)
+        sc = np.zeros(E * gN, dtype=np.int32)
+        vis = np.zeros(E, dtype=np.uint64)
+        tms = np.zeros(E * 6) if flags & TIMING else None
+        log = RunLog(obj.ctypes.data_as(P(C.c_double)), rmse.ctypes.data_as(P(C.c_double)),
+                     mu.ctypes.data_as(P(C.c_double)), sr.ctypes.data_as(P(C.c_int32)),
+                     sc.ctypes.data_as(P(C.c_int32)), vis.ctypes.data_as(P(C.c_uint64)),
+                     tms.ctypes.data_as(P(C.c_double)) if tms is not None else None)
+        self._c(_lib.bsgd_run(self.h, _ptr(y), _ptr(x), _ptr(x_true), C.byref(prm), C.byref(log), _stream(stream)))
+        return RunResult(obj[:epochs], rmse[:epochs], mu[:epochs], sr.reshape(E, aM)[:epochs],
+                         sc.reshape(E, gN)[:epochs], vis[:epochs],
+                         tms.reshape(E, 6)[:epochs] if tms is not None else None)
+
+    def get_state(self, what, index=0):
+        sizes = {0: (self.n_rays, np.float32), 1: (self.block_voxels, np.float32), 2: (self.block_voxels, np.float32),
+                 3: (self.n_rays, np.float32), 4: (self.M, np.float64), 5: (1, np.float64)}
+        n, dt = sizes[what]
+        out = np.zeros(n, dtype=dt)
+        self._c(_lib.bsgd_get_state(self.h, what, index, out.ctypes.data, out.nbytes))
+        return out
+
+    def set_state(self, what, index, arr):
+        dt = np.float64 if what in (4, 5) else np.float32
+        a = np.ascontiguousarray(arr, dtype=dt)
+        self._c(_lib.bsgd_set_state(self.h, what, index, a.ctypes.data, a.nbytes))
+
+    def power_iteration(self, iters=30, seed=0, stream=None) -> float:
+        out = C.c_double()
+        self._c(_lib.bsgd_power_iteration(self.h, iters, seed, C.byref(out), _stream(stream)))
+        return out.value

@@ -1,0 +1,1113 @@
+// BSGD epoch engine and the extern "C" boundary (include/bsgd.h).
+//
+// One process per GPU.  A rank owns the contiguous column blocks
+// [rank*N/G, (rank+1)*N/G) ("each parallel node calculates a
+// forward projection A_I^{J_j} x_{J_j}.  The summation over j is then
+// calculated ... using an ALLREDUCE procedure").  Every epoch: host selection
+// (Algo 1 line 3) -> FP of the owned selected blocks (line 5) -> partial sum of
+// the owned z^j over the selected rows -> ncclAllReduce (the only per-epoch
+// exchange) -> r_I = y_I - sum_j z^j_I (line 7) -> BP (line 9) -> g / x update
+// (lines 11-14).  Algo 3 (auto mu) and Algo 4 (TV prox) hook in after the step.
+#include <math.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace bsgd {
+
+static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void fail(bsgd_status code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        char buf[512];
+        snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+        fail(e == cudaErrorMemoryAllocation ? BSGD_E_OOM : BSGD_E_CUDA, buf);
+    }
+}
+
+#define BSGD_NCCL(x)                                                                          \
+    do {                                                                                      \
+        ncclResult_t r_ = (x);                                                                \
+        if (r_ != ncclSuccess) ::bsgd::fail(BSGD_E_NCCL, std::string(#x " failed: ") +        \
+                                                         ncclGetErrorString(r_));             \
+    } while (0)
+
+}  // namespace bsgd
+
+using namespace bsgd;
+
+struct bsgd_ctx_s {
+    // ---- configuration
+    int beam = 0, n_views = 0, nu = 0, nv = 0;
+    std::vector<double> vecs;
+    int dims[3] = {0, 0, 0}, bgrid[3] = {1, 1, 1}, bd[3] = {0, 0, 0};
+    int N = 1, M = 1, kind = 0, tiles_u = 1, tiles_v = 1, T = 1;
+    uint64_t row_seed = 0;
+    int rank = 0, world = 1, first = 0, s = 1;
+    long long bsize = 0, n_rays = 0, per = 0;
+    double R = 0.0;
+    std::vector<std::vector<int>> rows;   // views of each row block (sorted)
+    std::vector<int> view_row;             // row block of each view
+    // ---- memory
+    bsgd_alloc alloc{nullptr, nullptr, nullptr};
+    struct Buf { void* p; size_t bytes; };
+    std::vector<Buf> bufs;
+    uint64_t bytes = 0;
+    // ---- device state
+    double* d_vecs = nullptr;
+    float *xT = nullptr, *g = nullptr, *ghat = nullptr, *z = nullptr, *r = nullptr;
+    float *accN = nullptr, *accT = nullptr, *pc = nullptr;
+    float *eud_cur = nullptr, *eud_prev = nullptr;
+    float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
+          *tv_b = nullptr;
+    float *fp_scratchT = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr;
+    float *y_dev = nullptr, *x_dev = nullptr, *xt_dev = nullptr;
+    double* d_normsq = nullptr;
+    double* d_red = nullptr;           // 8 doubles scratch
+    double* d_log = nullptr;           // per-epoch [obj, rmse] scratch
+    long long d_log_cap = 0;
+    unsigned long long* d_visits = nullptr;
+    unsigned long long* d_vislog = nullptr;
+    // launch tables
+    char* d_tab = nullptr;
+    size_t tab_bytes = 0;
+    // ---- host state
+    std::vector<double> h_normsq;
+    double mu = 0.0;
+    int epoch = 0;
+    std::vector<uint32_t> q;            // IM table [s][n_views][T]
+    std::vector<double> w;
+    bool q_ready = false;
+    // Algo 3 state
+    bool have_prev_eud = false, have_theta_prev = false;
+    double theta_prev = 0.0;
+    std::vector<double> rnorm_hist;     // ||r||^{k} at k = 0, M, 2M, ...
+    ncclComm_t comm = nullptr;
+    bool poisoned = false;
+    std::string err;
+
+    // ------------------------------------------------------------ memory
+    void* dalloc(size_t n) {
+        if (n == 0) n = 16;
+        n = (n + 255) & ~(size_t)255;
+        void* p = nullptr;
+        if (alloc.alloc) {
+            p = alloc.alloc(n, nullptr, alloc.user);
+            if (!p) fail(BSGD_E_OOM, "allocator callback returned NULL");
+        } else {
+            cudaError_t e = cudaMalloc(&p, n);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                fail(BSGD_E_OOM, "cudaMalloc of " + std::to_string(n) + " bytes failed");
+            }
+        }
+        bufs.push_back({p, n});
+        bytes += n;
+        return p;
+    }
+    template <class T> T* dnew(long long count, bool zero = true) {
+        T* p = (T*)dalloc(sizeof(T) * (size_t)count);
+        if (zero) BSGD_CUDA(cudaMemset(p, 0, sizeof(T) * (size_t)count));
+        return p;
+    }
+    void release() {
+        for (auto& b : bufs) {
+            if (alloc.free) alloc.free(b.p, b.bytes, nullptr, alloc.user);
+            else cudaFree(b.p);
+        }
+        bufs.clear();
+    }
+
+    KGeom kgeom() const {
+        KGeom k;
+        k.vecs = d_vecs;
+        k.beam = beam;
+        k.nu = nu;
+        k.nv = nv;
+        k.n_views = n_views;
+        for (int c = 0; c < 3; ++c) k.dims[c] = dims[c];
+        k.R = R;
+        return k;
+    }
+    void box(int j, int lo[3], int hi[3]) const {
+        int jx = j % bgrid[0], jy = (j / bgrid[0]) % bgrid[1], jz = j / (bgrid[0] * bgrid[1]);
+        lo[0] = jx * bd[0]; lo[1] = jy * bd[1]; lo[2] = jz * bd[2];
+        for (int c = 0; c < 3; ++c) hi[c] = lo[c] + bd[c];
+    }
+    bool owned(int j) const { return j >= first && j < first + s; }
+
+    // pack host tables into the device arena; returns device pointers
+    template <class T> T* tab_put(size_t& off, const std::vector<T>& v, std::vector<char>& staging) {
+        off = (off + 15) & ~(size_t)15;
+        size_t nb = sizeof(T) * v.size();
+        if (off + nb > staging.size()) staging.resize(off + nb);
+        if (nb) memcpy(staging.data() + off, v.data(), nb);
+        T* dp = (T*)(d_tab + off);
+        off += nb;
+        return dp;
+    }
+    void tab_upload(const std::vector<char>& staging, size_t used, cudaStream_t st) {
+        if (used > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
+        BSGD_CUDA(cudaMemcpyAsync(d_tab, staging.data(), used, cudaMemcpyHostToDevice, st));
+    }
+
+    // ------------------------------------------------------------ operators
+    // FP for `blocks` (owned slots) over `views`; rects[b][slot] (empty = full detector).
+    void fp(const std::vector<int>& views, const std::vector<int>& slots, const std::vector<int4>& rects,
+            std::vector<const float*> xN, std::vector<const float*> xTs, std::vector<float*> zout,
+            int accumulate, cudaStream_t st, size_t tab_off = 0) {
+        project(PROJ_FP, views, slots, rects, xN, xTs, {}, {}, zout, nullptr, 0.f, accumulate, st, tab_off);
+    }
+
+    void project(int mode, const std::vector<int>& views, const std::vector<int>& slots,
+                 const std::vector<int4>& rects, const std::vector<const float*>& xN,
+                 const std::vector<const float*>& xTs, const std::vector<float*>& oN,
+                 const std::vector<float*>& oT, const std::vector<float*>& zout, const float* rproj,
+                 float scale, int accumulate, cudaStream_t st, size_t tab_off = 0) {
+        const int nb = (int)slots.size(), ns = (int)views.size();
+        if (nb == 0 || ns == 0) return;
+        std::vector<BlockDesc> bl(nb);
+        for (int b = 0; b < nb; ++b) {
+            BlockDesc& d = bl[b];
+            box(first + slots[b], d.lo, d.hi);
+            d.xN = xN.empty() ? nullptr : xN[b];
+            d.xT = xTs.empty() ? nullptr : xTs[b];
+            d.outN = oN.empty() ? nullptr : oN[b];
+            d.outT = oT.empty() ? nullptr : oT[b];
+            d.z = zout.empty() ? nullptr : zout[b];
+        }
+        std::vector<int4> rc = rects;
+        int maxr = 0;
+        if (rc.empty()) rc.assign((size_t)nb * ns, make_int4(0, nu, 0, nv));
+        for (auto& q : rc) maxr = std::max(maxr, (q.y - q.x) * (q.w - q.z));
+        std::vector<char> staging;
+        size_t off = tab_off;
+        staging.resize(off);
+        ProjLaunch L;
+        L.g = kgeom();
+        L.n_slots = ns;
+        L.views = tab_put(off, views, staging);
+        L.rects = tab_put(off, rc, staging);
+        L.n_blocks = nb;
+        L.blocks = tab_put(off, bl, staging);
+        L.max_rect_rays = maxr;
+        L.rproj = rproj;
+        L.scale = scale;
+        L.accumulate = accumulate;
+        L.visits = (mode == PROJ_FP) ? d_visits : nullptr;
+        if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
+        BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_off, staging.data() + tab_off, off - tab_off,
+                                  cudaMemcpyHostToDevice, st));
+        launch_project(mode, L, st);
+    }
+
+    float* ghat_of(int i, int b) { return ghat + ((long long)i * s + b) * bsize; }
+
+    void update(int mode, int b, float* x, float mu_, int final_, float* out, int accumulate,
+                cudaStream_t st, float* accN_ = nullptr, float* accT_ = nullptr, float* xT_ = nullptr,
+                int ghat_i = 0) {
+        UpdLaunch U;
+        U.bd[0] = bd[0]; U.bd[1] = bd[1]; U.bd[2] = bd[2];
+        U.accN = accN_ ? accN_ : accN + b * bsize;
+        U.accT = accT_ ? accT_ : accT + b * bsize;
+        U.ghat = ghat ? ghat_of(ghat_i, b) : nullptr;
+        U.g = g + b * bsize;
+        U.x = x;
+        U.xT = xT_ ? xT_ : xT + b * bsize;
+        U.out = out;
+        U.mu = mu_;
+        U.final_ = final_;
+        U.accumulate = accumulate;
+        launch_block_update(mode, U, st);
+    }
+
+    void refresh_xT(float* x_owned, const std::vector<int>& slots, cudaStream_t st) {
+        for (int b : slots) update(UPD_XT, b, x_owned + b * bsize, 0.f, 1, nullptr, 0, st);
+    }
+
+    void allreduce_f(float* p, size_t n, cudaStream_t st) {
+        if (world > 1) BSGD_NCCL(ncclAllReduce(p, p, n, ncclFloat, ncclSum, comm, st));
+    }
+    void allreduce_d(double* p, size_t n, cudaStream_t st) {
+        if (world > 1) BSGD_NCCL(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, st));
+    }
+
+    // ------------------------------------------------------------ one epoch
+    // Algo 1 / Algo 2 / Eq. 4 with an explicit selection.  tiles: [n_cols][V_sel] or empty.
+    void epoch_step(const float* y, float* x_owned, const std::vector<int>& sel_rows,
+                    const std::vector<int>& sel_cols, const std::vector<int>& tiles, float mu_,
+                    bool sgd, cudaStream_t st, cudaEvent_t* ev, bool refresh = true) {
+        std::vector<int> vsel, slot_row;
+        for (int i : sel_rows)
+            for (int v : rows[i]) {
+                vsel.push_back(v);
+                slot_row.push_back(i);
+            }
+        const int V = (int)vsel.size();
+        std::vector<int> cols = sgd ? std::vector<int>() : sel_cols;
+        if (sgd) for (int j = 0; j < N; ++j) cols.push_back(j);
+        // owned selected blocks and their global column slot
+        std::vector<int> oslots, ocs;
+        for (int cs = 0; cs < (int)cols.size(); ++cs)
+            if (owned(cols[cs])) {
+                oslots.push_back(cols[cs] - first);
+                ocs.push_back(cs);
+            }
+        const int nb = (int)oslots.size();
+        // x^T of the selected blocks must match x (the caller may have changed x);
+        // bsgd_run keeps it in sync itself (refresh = false)
+        if (refresh) refresh_xT(x_owned, oslots, st);
+        auto rect_for = [&](int b, int vs) -> int4 {
+            if (tiles.empty()) return make_int4(0, nu, 0, nv);
+            int t = tiles[(size_t)ocs[b] * V + vs];
+            int tu = t % tiles_u, tv = t / tiles_u;
+            return make_int4((int)((long long)tu * nu / tiles_u), (int)((long long)(tu + 1) * nu / tiles_u),
+                             (int)((long long)tv * nv / tiles_v), (int)((long long)(tv + 1) * nv / tiles_v));
+        };
+        if (ev) BSGD_CUDA(cudaEventRecord(ev[0], st));
+        // ---- lines 4-6: z^j_{I_i} = A_{I_i}^{J_j} x_{J_j}  (IM: tile rows only)
+        {
+            std::vector<int4> rc((size_t)nb * V);
+            std::vector<const float*> xs, xts;
+            std::vector<float*> zs;
+            for (int b = 0; b < nb; ++b) {
+                for (int vs = 0; vs < V; ++vs) rc[(size_t)b * V + vs] = rect_for(b, vs);
+                xs.push_back(x_owned + oslots[b] * bsize);
+                xts.push_back(xT + oslots[b] * bsize);
+                zs.push_back(z + oslots[b] * n_rays);
+            }
+            project(PROJ_FP, vsel, oslots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
+        }
+        if (ev) BSGD_CUDA(cudaEventRecord(ev[1], st));
+        // ---- line 7: r = y - sum_j z^j on the selected rows (+ allreduce of the partials)
+        {
+            std::vector<char> staging(tab_bytes / 2);
+            size_t off = tab_bytes / 2;
+            staging.resize(off);
+            ResLaunch Rl;
+            Rl.n_slots = V;
+            Rl.views = tab_put(off, vsel, staging);
+            Rl.slot_row = tab_put(off, slot_row, staging);
+            int* drows = tab_put(off, sel_rows, staging);
+            BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_bytes / 2, staging.data() + tab_bytes / 2,
+                                      off - tab_bytes / 2, cudaMemcpyHostToDevice, st));
+            Rl.per = (int)per;
+            Rl.z = z;
+            Rl.n_rays = n_rays;
+            Rl.s = s;
+            Rl.y = y;
+            Rl.r = r;
+            Rl.pc = pc;
+            Rl.normsq = d_normsq;
+            launch_zero_rows(d_normsq, drows, (int)sel_rows.size(), st);
+            if (world == 1) {
+                Rl.mode = 0;
+                launch_residual(Rl, st);
+            } else {
+                Rl.mode = 1;
+                launch_residual(Rl, st);
+                allreduce_f(pc, (size_t)V * per, st);
+                Rl.mode = 2;
+                launch_residual(Rl, st);
+            }
+        }
+        if (ev) BSGD_CUDA(cudaEventRecord(ev[2], st));
+        // ---- lines 8-10: g_hat^i_{J_j} = 2 (A_{I_i}^{J_j})^T r_{I_i}, then lines 11-14
+        std::vector<float*> oN, oT;
+        std::vector<const float*> none;
+        for (int b = 0; b < nb; ++b) {
+            oN.push_back(accN + oslots[b] * bsize);
+            oT.push_back(accT + oslots[b] * bsize);
+        }
+        if (sgd) {   // Eq. 4: g = 2 A_I^T r_I over all selected rows, no memory
+            std::vector<int4> rc((size_t)nb * V, make_int4(0, nu, 0, nv));
+            project(PROJ_BP, vsel, oslots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
+            if (ev) BSGD_CUDA(cudaEventRecord(ev[3], st));
+            for (int b = 0; b < nb; ++b)
+                update(UPD_SGD, oslots[b], x_owned + oslots[b] * bsize, mu_, 1, nullptr, 0, st);
+        } else {
+            int vs0 = 0;
+            for (size_t ii = 0; ii < sel_rows.size(); ++ii) {
+                const int i = sel_rows[ii];
+                const int Vi = (int)rows[i].size();
+                std::vector<int> vi(vsel.begin() + vs0, vsel.begin() + vs0 + Vi);
+                std::vector<int4> rc((size_t)nb * Vi);
+                for (int b = 0; b < nb; ++b)
+                    for (int k = 0; k < Vi; ++k) rc[(size_t)b * Vi + k] = rect_for(b, vs0 + k);
+                project(PROJ_BP, vi, oslots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
+                if (ev && ii + 1 == sel_rows.size()) BSGD_CUDA(cudaEventRecord(ev[3], st));
+                const int fin = (ii + 1 == sel_rows.size());
+                for (int b = 0; b < nb; ++b)
+                    update(UPD_BSGD, oslots[b], x_owned + oslots[b] * bsize, mu_, fin, nullptr, 0, st,
+                           nullptr, nullptr, nullptr, i);
+                vs0 += Vi;
+            }
+        }
+        if (ev) BSGD_CUDA(cudaEventRecord(ev[4], st));
+    }
+
+    void reset(const float* y, cudaStream_t st) {
+        BSGD_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)s * n_rays, st));
+        BSGD_CUDA(cudaMemsetAsync(ghat, 0, sizeof(float) * (size_t)M * s * bsize, st));
+        BSGD_CUDA(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)s * bsize, st));
+        BSGD_CUDA(cudaMemsetAsync(d_normsq, 0, sizeof(double) * M, st));
+        // r = y - sum z = y on every row block, with ||r_I||^2 (Algo 1 line 1)
+        std::vector<int> all(n_views), srow(n_views);
+        int pos = 0;
+        for (int i = 0; i < M; ++i)
+            for (int v : rows[i]) {
+                all[pos] = v;
+                srow[pos++] = i;
+            }
+        std::vector<char> staging;
+        size_t off = 0;
+        ResLaunch Rl;
+        Rl.n_slots = n_views;
+        Rl.views = tab_put(off, all, staging);
+        Rl.slot_row = tab_put(off, srow, staging);
+        tab_upload(staging, off, st);
+        Rl.per = (int)per;
+        Rl.z = z;
+        Rl.n_rays = n_rays;
+        Rl.s = s;
+        Rl.y = y;
+        Rl.r = r;
+        Rl.pc = pc;
+        Rl.normsq = d_normsq;
+        Rl.mode = 0;
+        launch_residual(Rl, st);   // z = 0 here, so r = y (no allreduce needed)
+        if (eud_cur) BSGD_CUDA(cudaMemsetAsync(eud_cur, 0, sizeof(float) * (size_t)s * bsize, st));
+        epoch = 0;
+        have_prev_eud = false;
+        have_theta_prev = false;
+        rnorm_hist.clear();
+    }
+
+    void ensure_im_table(cudaStream_t st) {
+        if (q_ready) return;
+        double* dw = dnew<double>((long long)s * n_views * T);
+        std::vector<BlockDesc> bl(s);
+        for (int b = 0; b < s; ++b) box(first + b, bl[b].lo, bl[b].hi);
+        std::vector<char> staging;
+        size_t off = 0;
+        ImLaunch I;
+        I.g = kgeom();
+        I.n_blocks = s;
+        I.blocks = tab_put(off, bl, staging);
+        I.tiles_u = tiles_u;
+        I.tiles_v = tiles_v;
+        I.w = dw;
+        tab_upload(staging, off, st);
+        launch_im_weights(I, st);
+        w.assign((size_t)s * n_views * T, 0.0);
+        BSGD_CUDA(cudaMemcpyAsync(w.data(), dw, sizeof(double) * w.size(), cudaMemcpyDeviceToHost, st));
+        BSGD_CUDA(cudaStreamSynchronize(st));
+        q.assign(w.size(), 0u);
+        for (size_t e = 0; e < w.size(); e += T) {
+            double S = 0.0;
+            for (int t = 0; t < T; ++t) S += w[e + t];
+            for (int t = 0; t < T; ++t) q[e + t] = S > 0 ? (uint32_t)floor(65536.0 * w[e + t] / S) : 0u;
+        }
+        q_ready = true;
+    }
+
+    // FGP TV prox (Algo 4 line 16) on the owned volume: x <- argmin 1/2|t-x|^2 + w TV(t)
+    void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st) {
+        const long long n = (long long)s * bsize;
+        if (!tv_u) {
+            tv_u = dnew<float>(n, false);
+            tv_p = dnew<float>(3 * n, false);
+            tv_q = dnew<float>(3 * n, false);
+            tv_b = dnew<float>(n, false);
+            long long plane = (long long)dims[0] * dims[1];
+            tv_hq = dnew<float>(plane);
+            tv_hu = dnew<float>(plane);
+        }
+        if (wgt == 0.0 || iters <= 0) return;
+        BSGD_CUDA(cudaMemcpyAsync(tv_b, x_owned, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+        BSGD_CUDA(cudaMemsetAsync(tv_p, 0, sizeof(float) * 3 * n, st));
+        BSGD_CUDA(cudaMemsetAsync(tv_q, 0, sizeof(float) * 3 * n, st));
+        TvLaunch Tl;
+        for (int c = 0; c < 3; ++c) {
+            Tl.dims[c] = dims[c];
+            Tl.bdims[c] = bd[c];
+            Tl.bgrid[c] = bgrid[c];
+        }
+        Tl.block0 = first;
+        Tl.b = tv_b;
+        Tl.u = tv_u;
+        Tl.p = tv_p;
+        Tl.q = tv_q;
+        Tl.out = x_owned;
+        Tl.halo_q_next = tv_hq;
+        Tl.halo_u_prev = tv_hu;
+        Tl.w = wgt;
+        int axes = (dims[0] > 1) + (dims[1] > 1) + (dims[2] > 1);
+        Tl.L = 4.0 * axes;
+        Tl.n = n;
+        Tl.z0 = first * bd[2];
+        Tl.z1 = (first + s) * bd[2];
+        const long long plane = (long long)dims[0] * dims[1];
+        double sk = 1.0;
+        for (int it = 0; it < iters; ++it) {
+            const double sk1 = (1.0 + sqrt(1.0 + 4.0 * sk * sk)) / 2.0;
+            Tl.beta = (sk - 1.0) / sk1;
+            // u = b - w grad^T q   (needs q_z of plane z1 from the next rank)
+            halo_exchange(tv_q + 2 * n, tv_hq, plane, /*send first plane down*/ true, st);
+            launch_tv_u(Tl, tv_q, tv_u, st);
+            // p, q update (needs u of plane z0-1 from the previous rank)
+            halo_exchange(tv_u + n - plane, tv_hu, plane, false, st);
+            launch_tv_pq(Tl, st);
+            sk = sk1;
+        }
+        halo_exchange(tv_p + 2 * n, tv_hq, plane, true, st);
+        launch_tv_u(Tl, tv_p, x_owned, st);
+    }
+
+    // z-slab halo: `down` = send my first plane (src) to rank-1 and receive rank+1's first
+    // plane into dst; otherwise send my last plane (src) to rank+1, receive from rank-1.
+    void halo_exchange(const float* src, float* dst, long long plane, bool down, cudaStream_t st) {
+        if (world == 1) return;
+        BSGD_NCCL(ncclGroupStart());
+        if (down) {
+            if (rank > 0) BSGD_NCCL(ncclSend(src, plane, ncclFloat, rank - 1, comm, st));
+            if (rank < world - 1) BSGD_NCCL(ncclRecv(dst, plane, ncclFloat, rank + 1, comm, st));
+        } else {
+            if (rank < world - 1) BSGD_NCCL(ncclSend(src, plane, ncclFloat, rank + 1, comm, st));
+            if (rank > 0) BSGD_NCCL(ncclRecv(dst, plane, ncclFloat, rank - 1, comm, st));
+        }
+        BSGD_NCCL(ncclGroupEnd());
+    }
+};
+
+// ============================================================================
+// C ABI
+// ============================================================================
+namespace {
+
+template <class F> bsgd_status guard(bsgd_ctx ctx, F&& f) {
+    if (ctx && ctx->poisoned) {
+        g_last_error = "context poisoned by an earlier CUDA/NCCL error: " + ctx->err;
+        return BSGD_E_POISONED;
+    }
+    try {
+        f();
+        return BSGD_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        if (ctx) {
+            ctx->err = e.msg;
+            if (e.code == BSGD_E_CUDA || e.code == BSGD_E_NCCL) ctx->poisoned = true;
+        }
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return BSGD_E_OOM;
+    } catch (...) {
+        g_last_error = "unknown exception";
+        return BSGD_E_CUDA;
+    }
+}
+
+cudaStream_t S(void* p) { return (cudaStream_t)p; }
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void check_views(bsgd_ctx c, int n, const int32_t* views, const int32_t* rects) {
+    if (n < 0 || (n > 0 && !views)) fail(BSGD_E_CONTRACT, "views pointer is NULL");
+    for (int k = 0; k < n; ++k) {
+        if (views[k] < 0 || views[k] >= c->n_views) fail(BSGD_E_DIMENSION, "view id out of range");
+        if (rects) {
+            const int32_t* q = rects + 4 * k;
+            if (q[0] < 0 || q[1] > c->nu || q[0] > q[1] || q[2] < 0 || q[3] > c->nv || q[2] > q[3])
+                fail(BSGD_E_DIMENSION, "detector rect outside the detector");
+        }
+    }
+}
+
+void check_sorted_unique(const int32_t* v, int n, int hi, const char* what) {
+    for (int k = 0; k < n; ++k) {
+        if (v[k] < 0 || v[k] >= hi) fail(BSGD_E_CONTRACT, std::string(what) + " id out of range");
+        if (k && v[k] <= v[k - 1]) fail(BSGD_E_CONTRACT, std::string(what) + " must be sorted and unique");
+    }
+}
+
+}  // namespace
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+int32_t bsgd_abi_version(void) { return BSGD_ABI_VERSION; }
+
+uint64_t bsgd_kernel_launches(void) { return g_launches.load(); }
+
+const char* bsgd_last_error(bsgd_ctx ctx) {
+    if (ctx && !ctx->err.empty()) return ctx->err.c_str();
+    return g_last_error.c_str();
+}
+
+bsgd_status bsgd_geometry_circular(int32_t beam, int32_t n_views, double arc_deg, double OP, double OD,
+                                   int32_t det_u, int32_t det_v, double pitch_u, double pitch_v,
+                                   double* vecs_out) {
+    return guard(nullptr, [&] {
+        if (n_views < 1 || det_u < 1 || det_v < 1 || !vecs_out) fail(BSGD_E_GEOMETRY, "bad counts");
+        if (beam != BSGD_PARALLEL && (!(OP > 0) || !(OD > 0)))
+            fail(BSGD_E_GEOMETRY, "non-positive source/detector distance");
+        if (beam < 0 || beam > 2) fail(BSGD_E_GEOMETRY, "unknown beam");
+        host::circular(beam, n_views, arc_deg, OP, OD, det_u, det_v, pitch_u, pitch_v, vecs_out);
+    });
+}
+
+bsgd_status bsgd_sample(uint64_t seed, int32_t stream, int32_t epoch, int32_t n, int32_t m, int32_t* out) {
+    return guard(nullptr, [&] {
+        if (n < 1 || m < 0 || m > n || !out || stream < 0 || epoch < 0 || epoch >= (1 << 24))
+            fail(BSGD_E_CONTRACT, "bad sample arguments");
+        host::select(seed, stream, epoch, n, m, out);
+    });
+}
+
+bsgd_status bsgd_view_partition(int32_t n_views, int32_t M, int32_t kind, uint64_t seed, int32_t* views_out,
+                                int32_t* offsets_out) {
+    return guard(nullptr, [&] {
+        if (M < 1 || M > n_views) fail(BSGD_E_PARTITION, "M must be in [1, n_views]");
+        if (kind < 0 || kind > 2) fail(BSGD_E_CONTRACT, "unknown partition kind");
+        host::view_partition(n_views, M, kind, seed, views_out, offsets_out);
+    });
+}
+
+bsgd_status bsgd_eq8(int32_t nodes, int32_t M, int32_t N, int32_t* aM, int32_t* gN) {
+    return guard(nullptr, [&] {
+        if (nodes < 1 || M < 1 || N < 1) fail(BSGD_E_CONTRACT, "counts must be >= 1");
+        host::eq8(nodes, M, N, aM, gN);
+    });
+}
+
+bsgd_status bsgd_owned_blocks(int32_t N, int32_t world, int32_t rank, int32_t* first, int32_t* count) {
+    return guard(nullptr, [&] {
+        if (world < 1 || rank < 0 || rank >= world || N < 1) fail(BSGD_E_CONTRACT, "bad rank/world");
+        if (N % world) fail(BSGD_E_PARTITION, "N must be divisible by the number of ranks");
+        *count = N / world;
+        *first = rank * (N / world);
+    });
+}
+
+bsgd_status bsgd_nccl_unique_id(uint8_t* out128) {
+    return guard(nullptr, [&] {
+        ncclUniqueId id;
+        BSGD_NCCL(ncclGetUniqueId(&id));
+        memcpy(out128, &id, sizeof id);
+    });
+}
+
+bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks, bsgd_row_grid rowg,
+                        const bsgd_dist* dist, const bsgd_alloc* alloc, bsgd_ctx* out) {
+    std::unique_ptr<bsgd_ctx_s> c(new bsgd_ctx_s());
+    bsgd_status st = guard(nullptr, [&] {
+        if (!geom || !out || !geom->vecs) fail(BSGD_E_GEOMETRY, "NULL geometry");
+        if (geom->n_views < 1 || geom->det_u < 1 || geom->det_v < 1) fail(BSGD_E_GEOMETRY, "bad counts");
+        if (geom->beam < 0 || geom->beam > 2) fail(BSGD_E_GEOMETRY, "unknown beam");
+        for (long long k = 0; k < 12LL * geom->n_views; ++k)
+            if (!isfinite(geom->vecs[k])) fail(BSGD_E_GEOMETRY, "non-finite geometry vector");
+        if (dims.nx < 1 || dims.ny < 1 || dims.nz < 1) fail(BSGD_E_PARTITION, "bad volume dims");
+        if (blocks.bx < 1 || blocks.by < 1 || blocks.bz < 1 || dims.nx % blocks.bx || dims.ny % blocks.by ||
+            dims.nz % blocks.bz)
+            fail(BSGD_E_PARTITION, "volume dims must be divisible by the block grid");
+        if (rowg.M < 1 || rowg.M > geom->n_views) fail(BSGD_E_PARTITION, "M must be in [1, n_views]");
+        if (rowg.kind < 0 || rowg.kind > 2) fail(BSGD_E_PARTITION, "unknown row partition kind");
+        if (rowg.tiles_u < 1 || rowg.tiles_v < 1 || rowg.tiles_u > geom->det_u || rowg.tiles_v > geom->det_v)
+            fail(BSGD_E_PARTITION, "bad tile grid");
+        c->beam = geom->beam;
+        c->n_views = geom->n_views;
+        c->nu = geom->det_u;
+        c->nv = geom->det_v;
+        c->vecs.assign(geom->vecs, geom->vecs + 12LL * geom->n_views);
+        c->dims[0] = dims.nx; c->dims[1] = dims.ny; c->dims[2] = dims.nz;
+        c->bgrid[0] = blocks.bx; c->bgrid[1] = blocks.by; c->bgrid[2] = blocks.bz;
+        for (int k = 0; k < 3; ++k) c->bd[k] = c->dims[k] / c->bgrid[k];
+        c->N = blocks.bx * blocks.by * blocks.bz;
+        c->M = rowg.M;
+        c->kind = rowg.kind;
+        c->row_seed = rowg.seed;
+        c->tiles_u = rowg.tiles_u;
+        c->tiles_v = rowg.tiles_v;
+        c->T = rowg.tiles_u * rowg.tiles_v;
+        c->bsize = (long long)c->bd[0] * c->bd[1] * c->bd[2];
+        c->per = (long long)c->nu * c->nv;
+        c->n_rays = c->per * c->n_views;
+        c->R = 0.5 * sqrt((double)dims.nx * dims.nx + (double)dims.ny * dims.ny + (double)dims.nz * dims.nz) + 1.0;
+        for (int v = 0; v < c->n_views; ++v) {     // zero-length rays are invalid geometry
+            const double* q = &c->vecs[12 * v];
+            if (c->beam == BSGD_PARALLEL && q[0] == 0 && q[1] == 0 && q[2] == 0)
+                fail(BSGD_E_GEOMETRY, "zero parallel ray direction");
+        }
+        if (dist && dist->world > 1) {
+            c->rank = dist->rank;
+            c->world = dist->world;
+            if (c->rank < 0 || c->rank >= c->world) fail(BSGD_E_CONTRACT, "bad rank");
+            if (c->N % c->world) fail(BSGD_E_PARTITION, "N must be divisible by the number of ranks");
+            if (!dist->nccl_id) fail(BSGD_E_CONTRACT, "nccl_id required when world > 1");
+        }
+        c->s = c->N / c->world;
+        c->first = c->rank * c->s;
+        // row blocks
+        std::vector<int32_t> vv(c->n_views), off(c->M + 1);
+        host::view_partition(c->n_views, c->M, c->kind, c->row_seed, vv.data(), off.data());
+        c->rows.resize(c->M);
+        c->view_row.resize(c->n_views);
+        for (int i = 0; i < c->M; ++i)
+            for (int k = off[i]; k < off[i + 1]; ++k) {
+                c->rows[i].push_back(vv[k]);
+                c->view_row[vv[k]] = i;
+            }
+        if (alloc) c->alloc = *alloc;
+        // device state
+        const long long sb = (long long)c->s * c->bsize;
+        c->d_vecs = c->dnew<double>(12LL * c->n_views, false);
+        BSGD_CUDA(cudaMemcpy(c->d_vecs, c->vecs.data(), sizeof(double) * c->vecs.size(), cudaMemcpyHostToDevice));
+        c->xT = c->dnew<float>(sb);
+        c->g = c->dnew<float>(sb);
+        c->ghat = c->dnew<float>((long long)c->M * sb);
+        c->z = c->dnew<float>((long long)c->s * c->n_rays);
+        c->r = c->dnew<float>(c->n_rays);
+        c->accN = c->dnew<float>(sb);
+        c->accT = c->dnew<float>(sb);
+        c->pc = c->world > 1 ? c->dnew<float>(c->n_rays) : nullptr;
+        c->d_normsq = c->dnew<double>(c->M);
+        c->d_red = c->dnew<double>(16);
+        c->d_visits = c->dnew<unsigned long long>(1);
+        c->tab_bytes = 2 * (size_t)(64 + 16 * ((size_t)c->n_views * (2 + 4LL * c->s + 1) + 64LL * c->s + c->M) + 4096);
+        c->d_tab = (char*)c->dalloc(c->tab_bytes);
+        c->h_normsq.assign(c->M, 0.0);
+        if (c->world > 1) {
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_id, sizeof id);
+            BSGD_NCCL(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+        }
+        BSGD_CUDA(cudaDeviceSynchronize());
+    });
+    if (st != BSGD_OK) {
+        if (c->comm) ncclCommDestroy(c->comm);
+        c->release();
+        return st;
+    }
+    *out = c.release();
+    return BSGD_OK;
+}
+
+void bsgd_destroy(bsgd_ctx ctx) {
+    if (!ctx) return;
+    cudaDeviceSynchronize();
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    ctx->release();
+    delete ctx;
+}
+
+bsgd_status bsgd_get_info(bsgd_ctx c, bsgd_info* o) {
+    return guard(c, [&] {
+        if (!c || !o) fail(BSGD_E_CONTRACT, "NULL");
+        o->N = c->N; o->M = c->M; o->n_views = c->n_views; o->det_u = c->nu; o->det_v = c->nv;
+        o->owned_first = c->first; o->owned_count = c->s; o->tiles = c->T;
+        o->block_voxels = c->bsize; o->n_rays = c->n_rays; o->owned_voxels = c->bsize * c->s;
+        for (int k = 0; k < 3; ++k) o->block_dims[k] = c->bd[k];
+        o->device_bytes = c->bytes;
+    });
+}
+
+bsgd_status bsgd_row_block_views(bsgd_ctx c, int32_t i, int32_t* out, int32_t* n) {
+    return guard(c, [&] {
+        if (!c || !n) fail(BSGD_E_CONTRACT, "NULL");
+        if (i < 0 || i >= c->M) fail(BSGD_E_DIMENSION, "row block out of range");
+        *n = (int32_t)c->rows[i].size();
+        if (out) memcpy(out, c->rows[i].data(), sizeof(int32_t) * c->rows[i].size());
+    });
+}
+
+bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int32_t* rects, int32_t col_block,
+                         const float* x_block, float* proj, int32_t accumulate, void* stream) {
+    return guard(c, [&] {
+        if (!c || !x_block || !proj) fail(BSGD_E_CONTRACT, "NULL");
+        check_views(c, n, views, rects);
+        if (!c->owned(col_block)) fail(BSGD_E_DIMENSION, "column block not owned by this rank");
+        if (n == 0) return;
+        if (!c->fp_scratchT) c->fp_scratchT = c->dnew<float>(c->bsize, false);
+        const int b = col_block - c->first;
+        cudaStream_t st = S(stream);
+        c->update(UPD_XT, b, const_cast<float*>(x_block), 0.f, 1, nullptr, 0, st, nullptr, nullptr,
+                  c->fp_scratchT);
+        std::vector<int> vv(views, views + n);
+        std::vector<int4> rc;
+        if (rects)
+            for (int k = 0; k < n; ++k) rc.push_back(make_int4(rects[4 * k], rects[4 * k + 1], rects[4 * k + 2], rects[4 * k + 3]));
+        c->project(PROJ_FP, vv, {b}, rc, {x_block}, {c->fp_scratchT}, {}, {}, {proj}, nullptr, 0.f, accumulate,
+                   st, 0);
+    });
+}
+
+bsgd_status bsgd_back(bsgd_ctx c, int32_t n, const int32_t* views, const int32_t* rects, int32_t col_block,
+                      const float* proj, float* g_block, float scale, int32_t accumulate, void* stream) {
+    return guard(c, [&] {
+        if (!c || !proj || !g_block) fail(BSGD_E_CONTRACT, "NULL");
+        check_views(c, n, views, rects);
+        if (!c->owned(col_block)) fail(BSGD_E_DIMENSION, "column block not owned by this rank");
+        if (!isfinite(scale)) fail(BSGD_E_CONTRACT, "scale not finite");
+        const int b = col_block - c->first;
+        cudaStream_t st = S(stream);
+        std::vector<int> vv(views, views + n);
+        std::vector<int4> rc;
+        if (rects)
+            for (int k = 0; k < n; ++k) rc.push_back(make_int4(rects[4 * k], rects[4 * k + 1], rects[4 * k + 2], rects[4 * k + 3]));
+        float* aN = c->accN + b * c->bsize;
+        float* aT = c->accT + b * c->bsize;
+        if (n > 0) c->project(PROJ_BP, vv, {b}, rc, {}, {}, {aN}, {aT}, {}, proj, scale, 0, st, 0);
+        c->update(UPD_OUT, b, nullptr, 0.f, 0, g_block, accumulate, st);
+    });
+}
+
+bsgd_status bsgd_im_weights(bsgd_ctx c, double* w_out, uint32_t* q_out) {
+    return guard(c, [&] {
+        if (!c) fail(BSGD_E_CONTRACT, "NULL");
+        c->ensure_im_table(nullptr);
+        if (w_out) memcpy(w_out, c->w.data(), sizeof(double) * c->w.size());
+        if (q_out) memcpy(q_out, c->q.data(), sizeof(uint32_t) * c->q.size());
+    });
+}
+
+bsgd_status bsgd_reset(bsgd_ctx c, const float* y, void* stream) {
+    return guard(c, [&] {
+        if (!c || !y) fail(BSGD_E_CONTRACT, "NULL");
+        c->reset(y, S(stream));
+    });
+}
+
+bsgd_status bsgd_step(bsgd_ctx c, const float* y, float* x_owned, const bsgd_selection* sel, float mu,
+                      uint32_t flags, void* stream) {
+    return guard(c, [&] {
+        if (!c || !y || !x_owned || !sel) fail(BSGD_E_CONTRACT, "NULL");
+        if (!isfinite(mu)) fail(BSGD_E_CONTRACT, "mu not finite");
+        if (flags & ~(uint32_t)BSGD_SGD) fail(BSGD_E_CONTRACT, "bsgd_step accepts BSGD_SGD only");
+        const bool sgd = flags & BSGD_SGD;
+        if (sel->n_rows < 1 || !sel->rows) fail(BSGD_E_CONTRACT, "empty row selection");
+        check_sorted_unique(sel->rows, sel->n_rows, c->M, "row block");
+        if (!sgd) {
+            if (sel->n_cols < 1 || !sel->cols) fail(BSGD_E_CONTRACT, "empty column selection");
+            check_sorted_unique(sel->cols, sel->n_cols, c->N, "column block");
+        }
+        std::vector<int> rows(sel->rows, sel->rows + sel->n_rows);
+        std::vector<int> cols;
+        if (!sgd) cols.assign(sel->cols, sel->cols + sel->n_cols);
+        std::vector<int> tiles;
+        if (sel->im_tiles && !sgd) {
+            int V = 0;
+            for (int i : rows) V += (int)c->rows[i].size();
+            tiles.assign(sel->im_tiles, sel->im_tiles + (size_t)V * cols.size());
+            for (int t : tiles)
+                if (t < 0 || t >= c->T) fail(BSGD_E_CONTRACT, "tile id out of range");
+        }
+        c->epoch_step(y, x_owned, rows, cols, tiles, mu, sgd, S(stream), nullptr);
+        c->epoch += 1;
+    });
+}
+
+bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt_in, const bsgd_run_params* P,
+                     bsgd_run_log* log, void* stream) {
+    return guard(c, [&] {
+        if (!c || !y_in || !x_in || !P) fail(BSGD_E_CONTRACT, "NULL");
+        if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
+        if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
+        const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING;
+        if (P->flags & ~known) fail(BSGD_E_CONTRACT, "unknown flags");
+        const bool sgd = P->flags & BSGD_SGD, im = (P->flags & (BSGD_IS | BSGD_IS_UNIFORM)) && !sgd;
+        const bool uni = P->flags & BSGD_IS_UNIFORM, tv = P->flags & BSGD_TV, amu = P->flags & BSGD_AUTO_MU;
+        int aM = P->rows_per_epoch, gN = P->cols_per_epoch;
+        if (aM == 0 || gN == 0) {
+            int a2, g2;
+            host::eq8(c->world, c->M, c->N, &a2, &g2);
+            if (!aM) aM = a2;
+            if (!gN) gN = g2;
+        }
+        if (aM < 1 || aM > c->M || gN < 1 || gN > c->N) fail(BSGD_E_CONTRACT, "rows/cols per epoch out of range");
+        if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
+            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        if (tv && (P->tv_iters < 0 || !isfinite(P->lambda))) fail(BSGD_E_CONTRACT, "bad TV parameters");
+        cudaStream_t st = S(stream);
+        const long long sb = (long long)c->s * c->bsize;
+        // host or device buffers
+        const float* y = y_in;
+        float* x = x_in;
+        const float* xt = xt_in;
+        if (!is_device_ptr(y_in)) {
+            if (!c->y_dev) c->y_dev = c->dnew<float>(c->n_rays, false);
+            BSGD_CUDA(cudaMemcpyAsync(c->y_dev, y_in, sizeof(float) * c->n_rays, cudaMemcpyHostToDevice, st));
+            y = c->y_dev;
+        }
+        const bool x_host = !is_device_ptr(x_in);
+        if (x_host) {
+            if (!c->x_dev) c->x_dev = c->dnew<float>(sb, false);
+            BSGD_CUDA(cudaMemcpyAsync(c->x_dev, x_in, sizeof(float) * sb, cudaMemcpyHostToDevice, st));
+            x = c->x_dev;
+        }
+        if (xt_in && !is_device_ptr(xt_in)) {
+            if (!c->xt_dev) c->xt_dev = c->dnew<float>(sb, false);
+            BSGD_CUDA(cudaMemcpyAsync(c->xt_dev, xt_in, sizeof(float) * sb, cudaMemcpyHostToDevice, st));
+            xt = c->xt_dev;
+        }
+        if (amu && !c->eud_cur) {
+            c->eud_cur = c->dnew<float>(sb);
+            c->eud_prev = c->dnew<float>(sb);
+        }
+        if (!(P->flags & BSGD_RESUME)) {
+            c->reset(y, st);
+            c->mu = P->mu0;
+            c->rnorm_hist.clear();
+        } else if (c->epoch == 0) {
+            c->mu = P->mu0;
+        }
+        if (c->rnorm_hist.empty()) {   // ||r||^0 = ||y|| (reading A13/A14): r = y after reset
+            BSGD_CUDA(cudaMemcpyAsync(c->h_normsq.data(), c->d_normsq, sizeof(double) * c->M,
+                                      cudaMemcpyDeviceToHost, st));
+            BSGD_CUDA(cudaStreamSynchronize(st));
+            double s2 = 0;
+            for (double v : c->h_normsq) s2 += v;
+            c->rnorm_hist.push_back(sqrt(s2));
+        }
+        if (im && !uni) c->ensure_im_table(st);
+        std::vector<int> all_slots(c->s);
+        for (int b = 0; b < c->s; ++b) all_slots[b] = b;
+        c->refresh_xT(x, all_slots, st);
+        const int E = P->epochs;
+        if (c->d_log_cap < 2LL * E + 2) {
+            c->d_log = c->dnew<double>(2LL * E + 2);
+            c->d_vislog = c->dnew<unsigned long long>(E + 1);
+            c->d_log_cap = 2LL * E + 2;
+        }
+        BSGD_CUDA(cudaMemsetAsync(c->d_log, 0, sizeof(double) * (2 * E + 2), st));
+        std::vector<cudaEvent_t> ev;
+        const bool timing = (P->flags & BSGD_TIMING) && log && log->t_ms;
+        if (timing) {
+            ev.resize((size_t)E * 7);
+            for (auto& e : ev) BSGD_CUDA(cudaEventCreate(&e));
+        }
+        const int period = tv ? (P->tv_period > 0 ? P->tv_period
+                                                  : std::max(1, (int)floor((double)c->M * c->N / ((double)aM * gN) + 0.5)))
+                              : 0;
+        std::vector<double> mu_log(E);
+        std::vector<int> rows(aM), cols(gN);
+        for (int e = 0; e < E; ++e) {
+            const int eg = c->epoch;          // global 0-based epoch (RNG counter)
+            const int k = eg + 1;             // 1-based epoch of Algos 3 and 4
+            host::select(P->seed, 1, eg, c->M, aM, rows.data());
+            if (!sgd) host::select(P->seed, 2, eg, c->N, gN, cols.data());
+            if (log && log->sel_rows) memcpy(log->sel_rows + (size_t)e * aM, rows.data(), sizeof(int) * aM);
+            if (log && log->sel_cols && !sgd) memcpy(log->sel_cols + (size_t)e * gN, cols.data(), sizeof(int) * gN);
+            std::vector<int> tiles;
+            const bool use_im = im && !(P->is_off_last_epochs > 0 && e >= E - P->is_off_last_epochs);
+            if (use_im) {   // Algo 2 line 5: one tile per (selected block, view) by weight
+                int V = 0;
+                for (int i : rows) V += (int)c->rows[i].size();
+                tiles.assign((size_t)V * gN, 0);
+                for (int cs = 0; cs < gN; ++cs) {
+                    if (!c->owned(cols[cs])) continue;
+                    int vs = 0;
+                    for (int i : rows)
+                        for (int v : c->rows[i]) {
+                            const uint32_t* qrow = uni ? nullptr : &c->q[((size_t)(cols[cs] - c->first) * c->n_views + v) * c->T];
+                            tiles[(size_t)cs * V + vs] = host::im_draw(P->seed, eg, (uint32_t)(cs * V + vs), qrow, c->T, uni);
+                            ++vs;
+                        }
+                }
+            }
+            cudaEvent_t* evp = timing ? &ev[(size_t)e * 7] : nullptr;
+            BSGD_CUDA(cudaMemcpyAsync(c->d_vislog + e, c->d_visits, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            c->epoch_step(y, x, rows, sgd ? std::vector<int>() : cols, tiles, (float)c->mu, sgd, st, evp, false);
+            BSGD_CUDA(cudaMemcpyAsync(c->d_vislog + e + 1, c->d_visits, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            mu_log[e] = c->mu;
+            launch_obj(c->d_normsq, c->M, c->d_log + 2 * e, st);
+            if (amu) launch_axpy_eud(c->eud_cur, c->g, sb, st);            // Algo 3 line 2
+            if (tv && k % period == 0) {                                      // Algo 4 lines 15-17
+                c->tv_prox(x, c->mu * P->lambda, P->tv_iters, st);
+                c->refresh_xT(x, all_slots, st);
+            }
+            if (evp) BSGD_CUDA(cudaEventRecord(evp[5], st));
+            if (xt) {
+                BSGD_CUDA(cudaMemsetAsync(c->d_red + 8, 0, sizeof(double), st));
+                launch_sqdiff(x, xt, sb, c->d_red + 8, st);
+                c->allreduce_d(c->d_red + 8, 1, st);
+                BSGD_CUDA(cudaMemcpyAsync(c->d_log + 2 * e + 1, c->d_red + 8, sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+            if (amu && k % c->M == 0) {                                       // Algo 3 lines 2-12
+                double d3[3] = {0, 0, 0};
+                bool have_theta = false;
+                double theta = 0.0;
+                if (c->have_prev_eud) {
+                    BSGD_CUDA(cudaMemsetAsync(c->d_red, 0, 3 * sizeof(double), st));
+                    launch_dot3(c->eud_cur, c->eud_prev, sb, c->d_red, st);
+                    c->allreduce_d(c->d_red, 3, st);
+                    BSGD_CUDA(cudaMemcpyAsync(d3, c->d_red, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+                }
+                BSGD_CUDA(cudaMemcpyAsync(c->h_normsq.data(), c->d_normsq, sizeof(double) * c->M, cudaMemcpyDeviceToHost, st));
+                BSGD_CUDA(cudaStreamSynchronize(st));
+                if (c->have_prev_eud && d3[1] > 0 && d3[2] > 0) {
+                    theta = d3[0] / (sqrt(d3[1]) * sqrt(d3[2]));
+                    have_theta = true;
+                }
+                double s2 = 0;
+                for (double v : c->h_normsq) s2 += v;
+                c->rnorm_hist.push_back(sqrt(s2));
+                const size_t h = c->rnorm_hist.size();
+                if (k > c->M && h >= 3) {
+                    const double rk = c->rnorm_hist[h - 1], rkM = c->rnorm_hist[h - 2], rk2M = c->rnorm_hist[h - 3];
+                    if (rk < rkM && rkM < rk2M) c->mu = (1.0 + P->eps) * c->mu;
+                    if (rk > rkM && rkM > rk2M) {
+                        bool c2 = false;
+                        if (have_theta) {
+                            if (c->have_theta_prev && fabs(theta - c->theta_prev) > P->t1) c2 = true;
+                            if (theta < P->t2) c2 = true;
+                        }
+                        if (c2) c->mu = (1.0 - P->delta) * c->mu;
+                    }
+                }
+                c->have_theta_prev = have_theta;
+                c->theta_prev = theta;
+                std::swap(c->eud_cur, c->eud_prev);
+                c->have_prev_eud = true;
+                BSGD_CUDA(cudaMemsetAsync(c->eud_cur, 0, sizeof(float) * sb, st));
+            }
+            if (evp) BSGD_CUDA(cudaEventRecord(evp[6], st));
+            c->epoch += 1;
+        }
+        if (x_host) BSGD_CUDA(cudaMemcpyAsync(x_in, x, sizeof(float) * sb, cudaMemcpyDeviceToHost, st));
+        std::vector<double> hl(2 * (size_t)E + 2);
+        std::vector<unsigned long long> hv(E + 1);
+        BSGD_CUDA(cudaMemcpyAsync(hl.data(), c->d_log, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, st));
+        BSGD_CUDA(cudaMemcpyAsync(hv.data(), c->d_vislog, sizeof(unsigned long long) * hv.size(), cudaMemcpyDeviceToHost, st));
+        BSGD_CUDA(cudaStreamSynchronize(st));
+        if (log) {
+            const double nvox = (double)c->bsize * c->N;
+            for (int e = 0; e < E; ++e) {
+                if (log->obj) log->obj[e] = hl[2 * e];
+                if (log->rmse) log->rmse[e] = xt ? sqrt(hl[2 * e + 1] / nvox) : NAN;
+                if (log->mu) log->mu[e] = mu_log[e];
+                if (log->visits) log->visits[e] = hv[e + 1] - hv[e];
+                if (timing) {
+                    cudaEvent_t* q = &ev[(size_t)e * 7];
+                    float t[6];
+                    for (int p = 0; p < 4; ++p) BSGD_CUDA(cudaEventElapsedTime(&t[p], q[p], q[p + 1]));
+                    BSGD_CUDA(cudaEventElapsedTime(&t[4], q[4], q[6]));
+                    BSGD_CUDA(cudaEventElapsedTime(&t[5], q[0], q[6]));
+                    for (int p = 0; p < 6; ++p) log->t_ms[(size_t)e * 6 + p] = t[p];
+                }
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+bsgd_status bsgd_get_state(bsgd_ctx c, int32_t what, int32_t index, void* dst, size_t bytes) {
+    return guard(c, [&] {
+        if (!c || !dst) fail(BSGD_E_CONTRACT, "NULL");
+        const void* src = nullptr;
+        size_t need = 0;
+        switch (what) {
+            case 0: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); src = c->z + index * c->n_rays; need = 4 * c->n_rays; break;
+            case 1: if (index < 0 || index >= c->M * c->s) fail(BSGD_E_DIMENSION, "index"); src = c->ghat_of(index / c->s, index % c->s); need = 4 * c->bsize; break;
+            case 2: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); src = c->g + index * c->bsize; need = 4 * c->bsize; break;
+            case 3: src = c->r; need = 4 * c->n_rays; break;
+            case 4: src = c->d_normsq; need = 8 * c->M; break;
+            case 5: need = 8; if (bytes != need) fail(BSGD_E_DIMENSION, "size"); memcpy(dst, &c->mu, 8); return;
+            default: fail(BSGD_E_CONTRACT, "unknown state item");
+        }
+        if (bytes != need) fail(BSGD_E_DIMENSION, "size mismatch");
+        BSGD_CUDA(cudaDeviceSynchronize());
+        BSGD_CUDA(cudaMemcpy(dst, src, need, cudaMemcpyDeviceToHost));
+    });
+}
+
+bsgd_status bsgd_set_state(bsgd_ctx c, int32_t what, int32_t index, const void* src, size_t bytes) {
+    return guard(c, [&] {
+        if (!c || !src) fail(BSGD_E_CONTRACT, "NULL");
+        void* dst = nullptr;
+        size_t need = 0;
+        switch (what) {
+            case 0: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); dst = c->z + index * c->n_rays; need = 4 * c->n_rays; break;
+            case 1: if (index < 0 || index >= c->M * c->s) fail(BSGD_E_DIMENSION, "index"); dst = c->ghat_of(index / c->s, index % c->s); need = 4 * c->bsize; break;
+            case 2: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); dst = c->g + index * c->bsize; need = 4 * c->bsize; break;
+            case 3: dst = c->r; need = 4 * c->n_rays; break;
+            case 4: dst = c->d_normsq; need = 8 * c->M; break;
+            case 5: need = 8; if (bytes != need) fail(BSGD_E_DIMENSION, "size"); memcpy(&c->mu, src, 8); return;
+            default: fail(BSGD_E_CONTRACT, "unknown state item");
+        }
+        if (bytes != need) fail(BSGD_E_DIMENSION, "size mismatch");
+        BSGD_CUDA(cudaDeviceSynchronize());
+        BSGD_CUDA(cudaMemcpy(dst, src, need, cudaMemcpyHostToDevice));
+    });
+}
+
+bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, double* out, void* stream) {
+    return guard(c, [&] {
+        if (!c || !out || iters < 1) fail(BSGD_E_CONTRACT, "bad arguments");
+        cudaStream_t st = S(stream);
+        const long long sb = (long long)c->s * c->bsize;
+        if (!c->pw_v) {
+            c->pw_v = c->dnew<float>(sb, false);
+            c->pw_vT = c->dnew<float>(sb, false);
+            c->pw_proj = c->dnew<float>(c->n_rays, false);
+        }
+        launch_fill_random(c->pw_v, sb, seed + 1000003ull * (uint64_t)c->rank, st);
+        BSGD_CUDA(cudaMemsetAsync(c->d_red, 0, 3 * sizeof(double), st));
+        launch_dot3(c->pw_v, c->pw_v, sb, c->d_red, st);
+        c->allreduce_d(c->d_red, 1, st);
+        launch_scale(c->pw_v, sb, c->d_red, st);
+        std::vector<int> all(c->n_views);
+        for (int v = 0; v < c->n_views; ++v) all[v] = v;
+        double lam = 0.0;
+        for (int it = 0; it < iters; ++it) {
+            BSGD_CUDA(cudaMemsetAsync(c->pw_proj, 0, sizeof(float) * c->n_rays, st));
+            for (int b = 0; b < c->s; ++b) {
+                c->update(UPD_XT, b, c->pw_v + b * c->bsize, 0.f, 1, nullptr, 0, st, nullptr, nullptr,
+                          c->pw_vT + b * c->bsize);
+                c->project(PROJ_FP, all, {b}, {}, {c->pw_v + b * c->bsize}, {c->pw_vT + b * c->bsize}, {}, {},
+                           {c->pw_proj}, nullptr, 0.f, 1, st, 0);
+            }
+            c->allreduce_f(c->pw_proj, c->n_rays, st);
+            for (int b = 0; b < c->s; ++b) {
+                c->project(PROJ_BP, all, {b}, {}, {}, {}, {c->accN + b * c->bsize}, {c->accT + b * c->bsize}, {},
+                           c->pw_proj, 1.f, 0, st, 0);
+                c->update(UPD_OUT, b, nullptr, 0.f, 0, c->pw_v + b * c->bsize, 0, st);
+            }
+            BSGD_CUDA(cudaMemsetAsync(c->d_red, 0, 3 * sizeof(double), st));
+            launch_dot3(c->pw_v, c->pw_v, sb, c->d_red, st);
+            c->allreduce_d(c->d_red, 1, st);
+            double nn = 0;
+            BSGD_CUDA(cudaMemcpyAsync(&nn, c->d_red, sizeof(double), cudaMemcpyDeviceToHost, st));
+            BSGD_CUDA(cudaStreamSynchronize(st));
+            lam = sqrt(nn);
+            launch_scale(c->pw_v, sb, c->d_red, st);
+        }
+        *out = lam;
+    });
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

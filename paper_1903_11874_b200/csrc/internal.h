@@ -1,0 +1,145 @@
+// Internal declarations of the BSGD B200 library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "bsgd.h"
+
+namespace bsgd {
+
+struct Error {
+    bsgd_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(bsgd_status code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define BSGD_CUDA(x) ::bsgd::cuda_check((x), #x, __FILE__, __LINE__)
+void note_launch();   // counts this library's kernel launches (bsgd_kernel_launches)
+
+// ---------------------------------------------------------------- host helpers
+namespace host {
+void cos_sin_deg(double theta, double* c, double* s);
+void circular(int beam, int n_views, double arc, double OP, double OD, int nu, int nv, double pu,
+              double pv, double* out);
+uint64_t mix64(uint64_t z);
+uint64_t rnd(uint64_t seed, uint32_t stream, uint32_t epoch, uint32_t k);
+uint32_t bounded(uint64_t u, uint32_t n);
+void select(uint64_t seed, int stream, int epoch, int n, int m, int32_t* out);
+void view_partition(int n_views, int M, int kind, uint64_t seed, int32_t* views, int32_t* offsets);
+void eq8(int nodes, int M, int N, int* aM, int* gN);
+int im_draw(uint64_t seed, int epoch, uint32_t k, const uint32_t* q, int T, bool uniform);
+}  // namespace host
+
+// ---------------------------------------------------------------- kernels
+struct KGeom {
+    const double* vecs;  // device [n_views][12]
+    int beam, nu, nv, n_views;
+    int dims[3];
+    double R;            // parallel-beam half length (|diag|/2 + 1)
+};
+
+// One column block as seen by a projection launch.
+struct BlockDesc {
+    const float* xN;     // FP source, block layout [z][y][x]
+    const float* xT;     // FP source, transposed layout [z][x][y]
+    float* outN;         // BP target (normal layout)
+    float* outT;         // BP target (transposed layout)
+    float* z;            // FP target, full-length projection vector
+    int lo[3], hi[3];    // box in grid coordinates
+};
+
+struct ProjLaunch {
+    KGeom g;
+    int n_slots;               // views in this launch (grid.y)
+    const int* views;          // device [n_slots]
+    const int4* rects;         // device [n_blocks][n_slots] (u0,u1,v0,v1)
+    int n_blocks;              // grid.z
+    const BlockDesc* blocks;   // device [n_blocks]
+    int max_rect_rays;
+    const float* rproj;        // BP input (full length)
+    float scale;               // BP scale (2 in Algo 1)
+    int accumulate;            // FP: add into z instead of overwriting
+    unsigned long long* visits;  // nullable counter
+};
+
+enum { PROJ_FP = 0, PROJ_BP = 1, PROJ_COUNT = 2 };
+void launch_project(int mode, const ProjLaunch& L, cudaStream_t st);
+
+// Block update / transpose modes of k_block_update.
+enum { UPD_BSGD = 0, UPD_SGD = 1, UPD_OUT = 2, UPD_XT = 3, UPD_SGD_ACC = 4 };
+struct UpdLaunch {
+    int bd[3];            // block dims (x, y, z)
+    float* accN;          // normal-layout BP accumulator (zeroed after reading)
+    float* accT;          // transposed-layout BP accumulator (zeroed after reading)
+    float* ghat;          // g_hat^i_J (UPD_BSGD)
+    float* g;             // g_J
+    float* x;             // x_J (normal layout)
+    float* xT;            // x_J transposed (written when x changes / UPD_XT)
+    float* out;           // UPD_OUT target
+    float mu;
+    int final_;           // apply x += mu g and refresh xT
+    int accumulate;       // UPD_OUT: add into out
+};
+void launch_block_update(int mode, const UpdLaunch& U, cudaStream_t st);
+
+struct ResLaunch {
+    int n_slots;
+    const int* views;       // device [n_slots]
+    const int* slot_row;    // device [n_slots] row-block id of the slot
+    int per;                // rays per view
+    const float* z;         // owned z vectors, stride n_rays
+    long long n_rays;
+    int s;                  // owned blocks
+    const float* y;
+    float* r;
+    float* pc;              // compact partial sums [n_slots*per] (world > 1)
+    double* normsq;         // [M]
+    int mode;               // 0 = fused r = y - sum z (world 1); 1 = pc = sum z; 2 = r = y - pc
+};
+void launch_residual(const ResLaunch& R, cudaStream_t st);
+
+void launch_zero_rows(double* normsq, const int* rows, int n, cudaStream_t st);
+void launch_obj(const double* normsq, int M, double* out, cudaStream_t st);
+void launch_axpy_eud(float* eud, const float* g, long long n, cudaStream_t st);
+void launch_dot3(const float* a, const float* b, long long n, double* out3, cudaStream_t st);
+void launch_sqdiff(const float* a, const float* b, long long n, double* out, cudaStream_t st);
+void launch_fill_random(float* v, long long n, uint64_t seed, cudaStream_t st);
+void launch_scale(float* v, long long n, const double* inv_norm_src, cudaStream_t st);
+
+struct ImLaunch {
+    KGeom g;
+    int n_blocks;
+    const BlockDesc* blocks;   // boxes only
+    int tiles_u, tiles_v;
+    double* w;                 // [n_blocks][n_views][T]
+};
+void launch_im_weights(const ImLaunch& I, cudaStream_t st);
+
+// TV prox on the owned volume (block-major layout, global block grid).
+struct TvLaunch {
+    int dims[3];        // global volume dims
+    int bdims[3];       // block dims
+    int bgrid[3];       // block grid
+    int z0, z1;         // owned global z range (z-slab sharding) or [0, nz)
+    long long block0;   // first owned block id
+    const float* b;     // input image (owned, block-major)
+    float* u;           // scratch (owned)
+    float* p;           // 3 * owned
+    float* q;           // 3 * owned
+    float* out;         // output image
+    const float* halo_q_next;  // q plane z1 (3 comps) or NULL
+    const float* halo_u_prev;  // u plane z0-1 or NULL
+    double w;           // weight mu*lambda
+    double L;           // Lipschitz bound 4*(#axes > 1)
+    double beta;        // FISTA momentum (s_k - 1)/s_{k+1}
+    long long n;        // owned voxels
+};
+void launch_tv_u(const TvLaunch& T, const float* src_q, float* dst, cudaStream_t st);
+void launch_tv_pq(const TvLaunch& T, cudaStream_t st);
+
+}  // namespace bsgd

@@ -1,0 +1,258 @@
+// Siddon ray-driven projector for sm_100a: FP z = A_I^J x_J (Algo 1 line 5,
+// PAPER.md:139), matched BP g = s (A_I^J)^T r (Algo 1 line 9),
+// and the ones-pass block masses of BSGD-IM.
+//
+// Design (DESIGN.md §"Projector"):
+//  * a2 ray setup in fp64 (IEEE round-to-nearest, no FMA contraction, the same
+//    parametrisation p(alpha) = a + alpha b, alpha in [0,1], as the problem
+//    definition) and slab clipping against the block box;
+//  * traversal "slice by slice" along the view's main in-plane axis: every warp
+//    (32 adjacent detector columns of one detector row) walks the planes of the
+//    main axis in LOCKSTEP, so at every step the 32 lanes touch 32 neighbouring
+//    voxels of one image row -> coalesced 128-byte gathers (FP) and coalesced
+//    reductions (BP).  Inside a slice the exact Siddon segments are produced by
+//    the crossings of the other two axes (fp64 t-parameters recomputed from the
+//    integer plane index, never accumulated).
+//  * views whose central ray is x-major use a transposed copy of the block
+//    ([z][x][y]) with x<->y swapped in the ray, so the lockstep axis is always
+//    the slow in-plane axis of the layout that is read.
+//  * no tensor cores: this is a sparse gather/scatter.
+#include <climits>
+
+#include "internal.h"
+
+namespace bsgd {
+
+namespace {
+
+__device__ __forceinline__ int cell_enter(double c, int dir, int lo, int hi) {
+    double f = floor(c);
+    int i = (int)f;
+    if (dir < 0 && f == c) i -= 1;   // moving down from a plane: cell below it
+    return min(max(i, lo), hi - 1);
+}
+
+__device__ __forceinline__ int cell_exit(double c, int dir, int lo, int hi) {
+    int i = (dir > 0) ? (int)ceil(c) - 1 : (int)floor(c);
+    return min(max(i, lo), hi - 1);
+}
+
+__device__ __forceinline__ int sgn(double v) { return (v > 0.0) - (v < 0.0); }
+
+// Ray (view, iv, iu) in grid coordinates, exactly as the problem defines it.
+__device__ __forceinline__ void make_ray(const KGeom& g, const double* vec, int iu, int iv,
+                                         double a[3], double b[3]) {
+    double ou = (double)iu - (g.nu - 1) / 2.0, ov = (double)iv - (g.nv - 1) / 2.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double d = __dadd_rn(__dadd_rn(vec[3 + c], __dmul_rn(ou, vec[6 + c])), __dmul_rn(ov, vec[9 + c]));
+        if (g.beam == BSGD_PARALLEL) {
+            a[c] = __dsub_rn(d, __dmul_rn(g.R, vec[c]));
+            b[c] = __dmul_rn(__dmul_rn(2.0, g.R), vec[c]);
+        } else {
+            a[c] = vec[c];
+            b[c] = __dsub_rn(d, vec[c]);
+        }
+        a[c] = __dadd_rn(a[c], g.dims[c] / 2.0);
+    }
+}
+
+// Clip p(alpha), alpha in [0,1], against [lo, hi); half-open for axes with b = 0.
+__device__ __forceinline__ bool clip(const double a[3], const double b[3], const double inv[3],
+                                     const int lo[3], const int hi[3], double& amin, double& amax) {
+    amin = 0.0;
+    amax = 1.0;
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (b[c] == 0.0) {
+            ok = ok && (a[c] >= lo[c]) && (a[c] < hi[c]);
+        } else {
+            double t0 = (lo[c] - a[c]) * inv[c], t1 = (hi[c] - a[c]) * inv[c];
+            amin = fmax(amin, fmin(t0, t1));
+            amax = fmin(amax, fmax(t0, t1));
+        }
+    }
+    return ok && amin < amax;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_project(const ProjLaunch L) {
+    const int slot = blockIdx.y;
+    const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
+    const int w = rc.y - rc.x, h = rc.w - rc.z;
+    const long long nrect = (long long)w * h;
+    const long long base = (long long)blockIdx.x * blockDim.x;
+    if (base >= nrect) return;                       // uniform over the CTA
+    const long long tid = base + threadIdx.x;
+    const bool inrect = tid < nrect;
+    const int iu = rc.x + (inrect ? (int)(tid % w) : 0);
+    const int iv = rc.z + (inrect ? (int)(tid / w) : 0);
+    const int view = L.views[slot];
+    const double* vec = L.g.vecs + 12 * (size_t)view;
+    const BlockDesc& B = L.blocks[blockIdx.z];
+
+    // main in-plane axis of the view (uniform over the CTA)
+    double cx = (L.g.beam == BSGD_PARALLEL) ? vec[0] : vec[3] - vec[0];
+    double cy = (L.g.beam == BSGD_PARALLEL) ? vec[1] : vec[4] - vec[1];
+    const bool mainX = fabs(cx) > fabs(cy);
+
+    double a[3], b[3];
+    make_ray(L.g, vec, iu, iv, a, b);
+    const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
+    if (mainX) {   // work in the frame (y, x, z): the lockstep axis is frame-y
+        double t = a[0]; a[0] = a[1]; a[1] = t;
+        t = b[0]; b[0] = b[1]; b[1] = t;
+        int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
+        q = hi[0]; hi[0] = hi[1]; hi[1] = q;
+    }
+    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1], bdz = hi[2] - lo[2];
+    const long long plane = (long long)bdx * bdy;
+    double inv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
+
+    double amin, amax;
+    bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
+    float rs = 0.f;
+    if (MODE == PROJ_BP) {
+        if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
+        hit = hit && (rs != 0.f);
+    }
+    const float* src = mainX ? B.xT : B.xN;
+    float* dst = mainX ? B.outT : B.outN;
+
+    const int sx = sgn(b[0]), sy = sgn(b[1]), sz = sgn(b[2]);
+    int j0 = 0, j1 = -1, ix = 0, iz = 0;
+    double t = 0.0, tx = 0.0, tz = 0.0;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    if (hit) {
+        j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
+        j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
+        if (sy == 0) j1 = j0;
+        ix = cell_enter(a[0] + amin * b[0], sx, lo[0], hi[0]);
+        iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
+        tx = sx ? ((double)(ix + (sx > 0)) - a[0]) * inv[0] : INF;
+        tz = sz ? ((double)(iz + (sz > 0)) - a[2]) * inv[2] : INF;
+        t = amin;
+    }
+    double acc = 0.0;
+    unsigned int nvis = 0;
+    const double a1 = a[1], inv1 = inv[1];
+
+    for (int pass = 0; pass < 2; ++pass) {
+        const int dir = pass == 0 ? 1 : -1;
+        const bool mine = hit && (pass == 0 ? sy >= 0 : sy < 0);
+        if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
+        int jl = mine ? min(j0, j1) : INT_MAX;
+        int jh = mine ? max(j0, j1) : INT_MIN;
+        jl = __reduce_min_sync(0xffffffffu, jl);
+        jh = __reduce_max_sync(0xffffffffu, jh);
+        const int jstart = dir > 0 ? jl : jh;
+        const int nsl = jh - jl + 1;
+        for (int k = 0; k < nsl; ++k) {
+            const int j = jstart + dir * k;
+            const bool in = mine && (dir > 0 ? (j >= j0 && j <= j1) : (j <= j0 && j >= j1));
+            if (in) {
+                double thi = amax;
+                if (sy != 0) thi = fmin(amax, ((double)(sy > 0 ? j + 1 : j) - a1) * inv1);
+                const long long rowoff = (long long)(j - lo[1]) * bdx;
+                for (;;) {
+                    const double tn = fmin(fmin(tx, tz), thi);
+                    if (tn > t) {
+                        const unsigned ux = (unsigned)(ix - lo[0]), uz = (unsigned)(iz - lo[2]);
+                        if (ux < (unsigned)bdx && uz < (unsigned)bdz) {
+                            const long long addr = (long long)uz * plane + rowoff + ux;
+                            const double len = (tn - t) * blen;
+                            if (MODE == PROJ_FP) acc += len * (double)__ldg(src + addr);
+                            if (MODE == PROJ_BP) atomicAdd(dst + addr, (float)(len * (double)rs));
+                            ++nvis;
+                        }
+                        t = tn;
+                    }
+                    if (tx <= tz) {
+                        if (tx < thi) {
+                            ix += sx;
+                            tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
+                            continue;
+                        }
+                    } else if (tz < thi) {
+                        iz += sz;
+                        tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
+                        continue;
+                    }
+                    break;
+                }
+                t = thi;
+            }
+        }
+    }
+    if (MODE == PROJ_FP && inrect) {
+        float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
+        *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
+    }
+    if (L.visits) {
+        unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits, (unsigned long long)s);
+    }
+}
+
+// Ones-pass: w[b][view][t] = sum over tile rays of chord(ray, box_b) = (A_t^{J_b} 1) summed.
+__global__ void __launch_bounds__(256) k_im_weights(const ImLaunch I) {
+    const int view = blockIdx.y;
+    const long long per = (long long)I.g.nu * I.g.nv;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in = tid < per;
+    const int iu = in ? (int)(tid % I.g.nu) : 0, iv = in ? (int)(tid / I.g.nu) : 0;
+    int tu = 0, tv = 0;
+    for (int q = 0; q < I.tiles_u; ++q)
+        if (iu >= (int)((long long)q * I.g.nu / I.tiles_u)) tu = q;
+    for (int q = 0; q < I.tiles_v; ++q)
+        if (iv >= (int)((long long)q * I.g.nv / I.tiles_v)) tv = q;
+    const int T = I.tiles_u * I.tiles_v, tile = tv * I.tiles_u + tu;
+    double a[3], b[3], inv[3];
+    make_ray(I.g, I.g.vecs + 12 * (size_t)view, iu, iv, a, b);
+    const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
+    const int key = in ? tile : -1;
+    const bool uniform_tile = __reduce_min_sync(0xffffffffu, key < 0 ? INT_MAX : key) ==
+                                  __reduce_max_sync(0xffffffffu, key) &&
+                              __all_sync(0xffffffffu, in);
+    for (int bb = 0; bb < I.n_blocks; ++bb) {
+        const BlockDesc& B = I.blocks[bb];
+        double amin, amax, c = 0.0;
+        if (in && clip(a, b, inv, B.lo, B.hi, amin, amax)) c = (amax - amin) * blen;
+        double* dst = I.w + ((size_t)bb * I.g.n_views + view) * T;
+        if (uniform_tile) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if ((threadIdx.x & 31) == 0) atomicAdd(dst + tile, c);
+        } else if (in && c != 0.0) {
+            atomicAdd(dst + tile, c);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
+    if (L.n_slots == 0 || L.n_blocks == 0 || L.max_rect_rays == 0) return;
+    dim3 grid((unsigned)((L.max_rect_rays + 255) / 256), (unsigned)L.n_slots, (unsigned)L.n_blocks);
+    if (mode == PROJ_FP) k_project<PROJ_FP><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BP) k_project<PROJ_BP><<<grid, 256, 0, st>>>(L);
+    else k_project<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_im_weights(const ImLaunch& I, cudaStream_t st) {
+    long long per = (long long)I.g.nu * I.g.nv;
+    dim3 grid((unsigned)((per + 255) / 256), (unsigned)I.g.n_views);
+    k_im_weights<<<grid, 256, 0, st>>>(I);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+}  // namespace bsgd

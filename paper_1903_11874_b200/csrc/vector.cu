@@ -1,0 +1,374 @@
+// HBM-streaming kernels of the hot path:
+//  * k_block_update: g_hat / g / x step of Algo 1 lines 11-14
+//    fused with the combination of the two BP accumulators (normal + transposed
+//    layout) and the refresh of the transposed image copy used by the FP;
+//  * k_residual: r_I = y_I - sum_j z^j_I (Algo 1 line 7) with the
+//    per-row-block ||r_I||^2 (fp64) that Algo 3 and the log need;
+//  * small reductions (EUD of Algo 3, dot products, RMSE) and the FGP TV prox
+//    stencil of Algo 4 line 16 (Eq. 6 backward differences).
+#include <algorithm>
+
+#include "internal.h"
+
+namespace bsgd {
+
+namespace {
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    v = (threadIdx.x < nw) ? red[threadIdx.x] : 0.0;
+    if (wid == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;   // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U, const int mode) {
+    __shared__ float tT[32][33];
+    __shared__ float tX[32][33];
+    const int bdx = U.bd[0], bdy = U.bd[1];
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const long long zoff = (long long)blockIdx.z * bdx * bdy;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const bool use_acc = mode != UPD_XT;
+    if (use_acc) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int xx = x0 + ty + 8 * k, yy = y0 + tx;
+            float v = 0.f;
+            if (xx < bdx && yy < bdy) {
+                float* p = U.accT + zoff + (long long)xx * bdy + yy;
+                v = *p;
+                *p = 0.f;
+            }
+            tT[ty + 8 * k][tx] = v;
+        }
+    }
+    __syncthreads();
+    const bool writes_x = (mode == UPD_XT) || ((mode == UPD_BSGD || mode == UPD_SGD) && U.final_);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int xx = x0 + tx, yy = y0 + ty + 8 * k;
+        float xv = 0.f;
+        if (xx < bdx && yy < bdy) {
+            const long long idx = zoff + (long long)yy * bdx + xx;
+            float nv = 0.f;
+            if (use_acc) {
+                nv = U.accN[idx] + tT[tx][ty + 8 * k];
+                U.accN[idx] = 0.f;
+            }
+            if (mode == UPD_BSGD) {
+                const float old = U.ghat[idx];
+                U.ghat[idx] = nv;
+                const float gv = U.g[idx] + (nv - old);
+                U.g[idx] = gv;
+                if (U.final_) {
+                    xv = U.x[idx] + U.mu * gv;
+                    U.x[idx] = xv;
+                }
+            } else if (mode == UPD_SGD) {
+                U.g[idx] = nv;
+                xv = U.x[idx] + U.mu * nv;
+                U.x[idx] = xv;
+            } else if (mode == UPD_OUT) {
+                U.out[idx] = U.accumulate ? U.out[idx] + nv : nv;
+            } else if (mode == UPD_XT) {
+                xv = U.x[idx];
+            }
+        }
+        tX[ty + 8 * k][tx] = xv;
+    }
+    if (!writes_x) return;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int xx = x0 + ty + 8 * k, yy = y0 + tx;
+        if (xx < bdx && yy < bdy) U.xT[zoff + (long long)xx * bdy + yy] = tX[tx][ty + 8 * k];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
+    const int slot = blockIdx.y;
+    const long long base = (long long)R.views[slot] * R.per;
+    const long long cbase = (long long)slot * R.per;
+    double ss = 0.0;
+    const bool v4 = (R.per & 3) == 0;
+    const long long nvec = v4 ? R.per / 4 : R.per;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nvec;
+         q += (long long)gridDim.x * blockDim.x) {
+        if (v4) {
+            const long long e = base + 4 * q;
+            float4 acc;
+            if (R.mode == 2) {
+                acc = *reinterpret_cast<const float4*>(R.pc + cbase + 4 * q);
+            } else {
+                acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < R.s; ++j) {   // sum over owned blocks in ascending order
+                    const float4 zz = __ldg(reinterpret_cast<const float4*>(R.z + (long long)j * R.n_rays + e));
+                    acc.x += zz.x; acc.y += zz.y; acc.z += zz.z; acc.w += zz.w;
+                }
+            }
+            if (R.mode == 1) {
+                *reinterpret_cast<float4*>(R.pc + cbase + 4 * q) = acc;
+            } else {
+                const float4 yy = __ldg(reinterpret_cast<const float4*>(R.y + e));
+                float4 rr = make_float4(yy.x - acc.x, yy.y - acc.y, yy.z - acc.z, yy.w - acc.w);
+                *reinterpret_cast<float4*>(R.r + e) = rr;
+                ss += (double)rr.x * rr.x + (double)rr.y * rr.y + (double)rr.z * rr.z + (double)rr.w * rr.w;
+            }
+        } else {
+            const long long e = base + q;
+            float acc = 0.f;
+            if (R.mode == 2) acc = R.pc[cbase + q];
+            else
+                for (int j = 0; j < R.s; ++j) acc += __ldg(R.z + (long long)j * R.n_rays + e);
+            if (R.mode == 1) {
+                R.pc[cbase + q] = acc;
+            } else {
+                const float rr = R.y[e] - acc;
+                R.r[e] = rr;
+                ss += (double)rr * rr;
+            }
+        }
+    }
+    if (R.mode != 1) {
+        ss = block_sum(ss);
+        if (threadIdx.x == 0) atomicAdd(R.normsq + R.slot_row[slot], ss);
+    }
+}
+
+__global__ void k_zero_rows(double* normsq, const int* rows, int n) {
+    int i = threadIdx.x;
+    if (i < n) normsq[rows[i]] = 0.0;
+}
+
+__global__ void k_obj(const double* normsq, int M, double* out) {
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < M; ++i) s += normsq[i];
+        *out = 0.5 * s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_axpy(float* eud, const float* g, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        eud[i] += g[i];
+}
+
+__global__ void __launch_bounds__(256) k_dot3(const float* a, const float* b, long long n, double* out) {
+    double ab = 0, aa = 0, bb = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double x = a[i], y = b[i];
+        ab += x * y; aa += x * x; bb += y * y;
+    }
+    ab = block_sum(ab);
+    if (threadIdx.x == 0) atomicAdd(out, ab);
+    aa = block_sum(aa);
+    if (threadIdx.x == 0) atomicAdd(out + 1, aa);
+    bb = block_sum(bb);
+    if (threadIdx.x == 0) atomicAdd(out + 2, bb);
+}
+
+__global__ void __launch_bounds__(256) k_sqdiff(const float* a, const float* b, long long n, double* out) {
+    double s = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double d = (double)a[i] - (double)b[i];
+        s += d * d;
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) atomicAdd(out, s);
+}
+
+__device__ __forceinline__ uint64_t dmix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_fill_random(float* v, long long n, uint64_t seed) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        v[i] = (float)((dmix(seed + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull) >> 40) * (1.0 / 16777216.0)) - 0.5f;
+}
+
+__global__ void k_scale(float* v, long long n, const double* nrm) {
+    const float s = (float)(1.0 / sqrt(*nrm));
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        v[i] *= s;
+}
+
+// ------------------------------------------------------------------ TV prox
+struct Vox {
+    int x, y, z;
+};
+
+__device__ __forceinline__ Vox owned_coords(const TvLaunch& T, long long o) {
+    const long long bs = (long long)T.bdims[0] * T.bdims[1] * T.bdims[2];
+    const long long blk = T.block0 + o / bs;
+    const long long l = o % bs;
+    const int lx = (int)(l % T.bdims[0]), ly = (int)((l / T.bdims[0]) % T.bdims[1]),
+              lz = (int)(l / ((long long)T.bdims[0] * T.bdims[1]));
+    const int jx = (int)(blk % T.bgrid[0]), jy = (int)((blk / T.bgrid[0]) % T.bgrid[1]),
+              jz = (int)(blk / ((long long)T.bgrid[0] * T.bgrid[1]));
+    return {jx * T.bdims[0] + lx, jy * T.bdims[1] + ly, jz * T.bdims[2] + lz};
+}
+
+// owned index of global voxel (x,y,z); -1 if outside the owned range
+__device__ __forceinline__ long long owned_index(const TvLaunch& T, int x, int y, int z) {
+    const int jx = x / T.bdims[0], jy = y / T.bdims[1], jz = z / T.bdims[2];
+    const long long blk = ((long long)jz * T.bgrid[1] + jy) * T.bgrid[0] + jx;
+    const long long rel = blk - T.block0;
+    const long long bs = (long long)T.bdims[0] * T.bdims[1] * T.bdims[2];
+    if (rel < 0 || rel * bs >= T.n) return -1;
+    const int lx = x - jx * T.bdims[0], ly = y - jy * T.bdims[1], lz = z - jz * T.bdims[2];
+    return rel * bs + ((long long)lz * T.bdims[1] + ly) * T.bdims[0] + lx;
+}
+
+// dst = b - w * grad^T(src)  (src = 3 component fields, component stride T.n)
+__global__ void __launch_bounds__(256) k_tv_u(const TvLaunch T, const float* src, float* dst) {
+    for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < T.n;
+         o += (long long)gridDim.x * blockDim.x) {
+        const Vox v = owned_coords(T, o);
+        double div = 0.0;
+        const int c[3] = {v.x, v.y, v.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (c[a] >= 1) div += src[a * T.n + o];
+            if (c[a] + 1 <= T.dims[a] - 1) {
+                const int nx = v.x + (a == 0), ny = v.y + (a == 1), nz = v.z + (a == 2);
+                const long long on = owned_index(T, nx, ny, nz);
+                float q;
+                if (on >= 0) q = src[a * T.n + on];
+                else q = T.halo_q_next[(long long)ny * T.dims[0] + nx];   // z comp of plane z1
+                div -= q;
+            }
+        }
+        dst[o] = (float)((double)T.b[o] - T.w * div);
+    }
+}
+
+// p_new = P(q + grad(u)/(L w)); q = p_new + beta (p_new - p); p = p_new
+__global__ void __launch_bounds__(256) k_tv_pq(const TvLaunch T) {
+    const double s = 1.0 / (T.L * T.w);
+    for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < T.n;
+         o += (long long)gridDim.x * blockDim.x) {
+        const Vox v = owned_coords(T, o);
+        const int c[3] = {v.x, v.y, v.z};
+        const double uo = T.u[o];
+        double pn[3];
+        double nrm = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            double gr = 0.0;
+            if (c[a] >= 1) {
+                const int nx = v.x - (a == 0), ny = v.y - (a == 1), nz = v.z - (a == 2);
+                const long long on = owned_index(T, nx, ny, nz);
+                const float un = on >= 0 ? T.u[on] : T.halo_u_prev[(long long)ny * T.dims[0] + nx];
+                gr = uo - (double)un;
+            }
+            pn[a] = (double)T.q[a * T.n + o] + gr * s;
+            nrm += pn[a] * pn[a];
+        }
+        const double d = fmax(1.0, sqrt(nrm));
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double p1 = pn[a] / d;
+            const double p0 = T.p[a * T.n + o];
+            T.q[a * T.n + o] = (float)(p1 + T.beta * (p1 - p0));
+            T.p[a * T.n + o] = (float)p1;
+        }
+    }
+}
+
+unsigned grid_for(long long n, int per_thread = 1) {
+    long long b = (n / per_thread + 255) / 256;
+    if (b < 1) b = 1;
+    if (b > 148LL * 16) b = 148LL * 16;
+    return (unsigned)b;
+}
+
+}  // namespace
+
+void launch_block_update(int mode, const UpdLaunch& U, cudaStream_t st) {
+    dim3 grid((unsigned)((U.bd[0] + 31) / 32), (unsigned)((U.bd[1] + 31) / 32), (unsigned)U.bd[2]);
+    k_block_update<<<grid, dim3(32, 8), 0, st>>>(U, mode);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_residual(const ResLaunch& R, cudaStream_t st) {
+    if (R.n_slots == 0) return;
+    long long nvec = (R.per % 4 == 0) ? R.per / 4 : R.per;
+    unsigned gx = (unsigned)std::min<long long>((nvec + 255) / 256, 64);
+    k_residual<<<dim3(gx, (unsigned)R.n_slots), 256, 0, st>>>(R);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_zero_rows(double* normsq, const int* rows, int n, cudaStream_t st) {
+    k_zero_rows<<<1, 1024, 0, st>>>(normsq, rows, n);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_obj(const double* normsq, int M, double* out, cudaStream_t st) {
+    k_obj<<<1, 32, 0, st>>>(normsq, M, out);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_axpy_eud(float* eud, const float* g, long long n, cudaStream_t st) {
+    k_axpy<<<grid_for(n, 4), 256, 0, st>>>(eud, g, n);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_dot3(const float* a, const float* b, long long n, double* out3, cudaStream_t st) {
+    k_dot3<<<grid_for(n, 8), 256, 0, st>>>(a, b, n, out3);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_sqdiff(const float* a, const float* b, long long n, double* out, cudaStream_t st) {
+    k_sqdiff<<<grid_for(n, 8), 256, 0, st>>>(a, b, n, out);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_fill_random(float* v, long long n, uint64_t seed, cudaStream_t st) {
+    k_fill_random<<<grid_for(n, 4), 256, 0, st>>>(v, n, seed);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_scale(float* v, long long n, const double* nrm, cudaStream_t st) {
+    k_scale<<<grid_for(n, 4), 256, 0, st>>>(v, n, nrm);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_u(const TvLaunch& T, const float* src, float* dst, cudaStream_t st) {
+    k_tv_u<<<grid_for(T.n, 2), 256, 0, st>>>(T, src, dst);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_pq(const TvLaunch& T, cudaStream_t st) {
+    k_tv_pq<<<grid_for(T.n, 2), 256, 0, st>>>(T);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+}  // namespace bsgd

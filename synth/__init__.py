@@ -46,8 +46,14 @@ def cos_sin_deg(theta_deg: float) -> tuple[float, float]:
     t = math.fmod(theta_deg, 360.0)
     if t < 0.0:
         t += 360.0
-    k = int(t // 90.0)
+    k = math.floor(t / 90.0)
     r = t - 90.0 * k
+    if r < 0.0:
+        k -= 1
+        r = t - 90.0 * k
+    if r >= 90.0:
+        k += 1
+        r = t - 90.0 * k
     if r == 0.0:
         c, s = 1.0, 0.0
     else:
@@ -210,27 +216,42 @@ def ray_endpoints(geom: Geometry, views: np.ndarray):
 
 
 def analytic_projection(geom: Geometry, ells: np.ndarray, views=None, device: str = "cpu",
-                        chunk_rays: int = 1 << 22):
+                        chunk_rays: int = 1 << 22, out_torch=None):
     """Closed-form line integrals of the additive ellipsoid phantom.
 
     For each ellipsoid (rho, semi-axes D, centre c, rotation R about z) the
     ray maps to unit-sphere coordinates p' = D^-1 R^T (A - c), d' = D^-1 R^T B;
     |p' + t d'|^2 = 1 gives t1 < t2, clipped to [0, 1]; the contribution is
     rho (t2 - t1) |B|.  Returns float64 numpy array (len(views), det_v, det_u).
-    Uses torch (fp64) so the 1024^3 preset can run on a GPU."""
+    Uses torch (fp64) so the 1024^3 preset can run on a GPU.  If ``out_torch``
+    (a float32 torch tensor of n_views*det_v*det_u elements) is given, the
+    result is written there (indexed by view) instead of a numpy array."""
     import torch
     if views is None:
         views = np.arange(geom.n_views)
     views = np.asarray(views)
-    out = np.zeros((len(views), geom.det_v, geom.det_u), dtype=np.float64)
+    out = None if out_torch is not None else np.zeros((len(views), geom.det_v, geom.det_u), dtype=np.float64)
     per_view = geom.det_u * geom.det_v
     vchunk = max(1, chunk_rays // per_view)
     E = torch.as_tensor(ells, dtype=torch.float64, device=device)
+    vecs = torch.as_tensor(geom.vecs, dtype=torch.float64, device=device)
+    ou = torch.arange(geom.det_u, dtype=torch.float64, device=device) - (geom.det_u - 1) / 2.0
+    ov = torch.arange(geom.det_v, dtype=torch.float64, device=device) - (geom.det_v - 1) / 2.0
     for s in range(0, len(views), vchunk):
         vs = views[s:s + vchunk]
-        A, B = ray_endpoints(geom, vs)
-        A = torch.as_tensor(np.ascontiguousarray(A), device=device).reshape(-1, 3)
-        B = torch.as_tensor(np.ascontiguousarray(B), device=device).reshape(-1, 3)
+        v = vecs[torch.as_tensor(vs, device=device)]
+        pix = (v[:, None, None, 3:6] + ou[None, None, :, None] * v[:, None, None, 6:9]
+               + ov[None, :, None, None] * v[:, None, None, 9:12])
+        if geom.beam == PARALLEL:
+            nx, ny, nz = geom.dims
+            R = 0.5 * math.sqrt(nx * nx + ny * ny + nz * nz) + 1.0
+            d = v[:, None, None, 0:3].expand_as(pix)
+            A, B = pix - R * d, 2.0 * R * d
+        else:
+            src = v[:, None, None, 0:3].expand_as(pix)
+            A, B = src, pix - src
+        A = A.reshape(-1, 3)
+        B = B.reshape(-1, 3)
         blen = torch.linalg.norm(B, dim=1)
         acc = torch.zeros(A.shape[0], dtype=torch.float64, device=device)
         for e in range(E.shape[0]):
@@ -252,8 +273,12 @@ def analytic_projection(geom: Geometry, ells: np.ndarray, views=None, device: st
             t1 = ((-bb - sq) / (2.0 * aa)).clamp(0.0, 1.0)
             t2 = ((-bb + sq) / (2.0 * aa)).clamp(0.0, 1.0)
             acc += torch.where(ok, rho * (t2 - t1) * blen, torch.zeros_like(acc))
-        out[s:s + len(vs)] = acc.reshape(len(vs), geom.det_v, geom.det_u).cpu().numpy()
-    return out
+        if out_torch is not None:
+            ot = out_torch.view(geom.n_views, per_view)
+            ot[torch.as_tensor(vs, device=ot.device)] = acc.reshape(len(vs), per_view).to(ot.device, torch.float32)
+        else:
+            out[s:s + len(vs)] = acc.reshape(len(vs), geom.det_v, geom.det_u).cpu().numpy()
+    return out if out_torch is None else out_torch
 
 
 # ----------------------------------------------------------------------------

@@ -1,0 +1,298 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star):
+  FP per ray   |d| <= 1e-5 (A|x|)_i   + 1e-7 |x|_inf
+  BP per voxel |d| <= 1e-5 (A^T|r|)_j + 1e-7 |r|_inf
+  rays missing the block give exactly 0; selections / partitions / IM tables
+  bit-exact; trajectories (objective, RMSE, mu) within 1e-3 relative."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import bsgd as ob
+from oracle.projector import BlockGrid, Projector
+
+from _problems import problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1903_11874_b200 as m
+    return m
+
+
+def clear_miss(g, views, lo, hi, margin=1e-6):
+    """Rays (views x det, row-major) that miss the box grown by `margin` (slab test,
+    vectorised); corner touches and grazing rays are excluded from the exact-zero check."""
+    A, B = synth.ray_endpoints(g, views)
+    half = np.array(g.dims) / 2.0
+    A = A.reshape(-1, 3) + half
+    B = B.reshape(-1, 3)
+    t0 = np.zeros(len(A))
+    t1 = np.ones(len(A))
+    miss = np.zeros(len(A), bool)
+    for c in range(3):
+        l, h = lo[c] - margin, hi[c] + margin
+        z = B[:, c] == 0
+        miss |= z & ((A[:, c] < l) | (A[:, c] > h))
+        with np.errstate(divide="ignore", invalid="ignore"):
+            u0 = (l - A[:, c]) / B[:, c]
+            u1 = (h - A[:, c]) / B[:, c]
+        t0 = np.where(z, t0, np.maximum(t0, np.minimum(u0, u1)))
+        t1 = np.where(z, t1, np.minimum(t1, np.maximum(u0, u1)))
+    return miss | (t0 >= t1)
+
+
+def _fp_bp_check(bs, g, blocks, M, views, block_ids, rects=None, seed=0):
+    ctx = bs.Context.from_geometry(g, blocks, M)
+    P = Projector(g, BlockGrid(g.dims, blocks))
+    rng = np.random.default_rng(seed)
+    rows = P.rows_of(views)
+    if rects is not None:
+        mask = np.zeros((len(views), g.det_v, g.det_u), bool)
+        for k, (u0, u1, v0, v1) in enumerate(rects):
+            mask[k, v0:v1, u0:u1] = True
+        rows_in = rows[mask.ravel()]
+        rows_out = rows[~mask.ravel()]
+    else:
+        rows_in, rows_out = rows, rows[:0]
+    worst_fp = worst_bp = 0.0
+    for j in block_ids:
+        x = rng.random(P.grid.bsize, dtype=np.float32)
+        proj = torch.full((g.n_rays,), -7.0, device="cuda")
+        ctx.forward(views, j, torch.from_numpy(x).cuda(), proj, rects=rects)
+        torch.cuda.synchronize()
+        got = proj.cpu().numpy().astype(np.float64)
+        ref = P.fp(views, j, x.astype(np.float64), rects=rects)
+        d = np.abs(got[rows_in] - ref[rows_in])
+        tol = 1e-5 * ref[rows_in] + 1e-7 * float(x.max())          # A|x| = A x for x >= 0
+        worst_fp = max(worst_fp, float(np.max(d / tol)))
+        assert np.all(d <= tol), f"FP block {j}: max |d|/tol = {np.max(d / tol):.3g}"
+        lo, hi = P.grid.box(j)
+        miss = clear_miss(g, views, lo, hi)[np.isin(rows, rows_in)]
+        assert np.all(got[rows_in][miss] == 0.0)                    # clear misses are exactly 0
+        assert np.all(got[rows_out] == -7.0)                         # untouched outside rects
+        # BP of a signed residual on the same rays
+        r = np.zeros(g.n_rays, dtype=np.float32)
+        r[rows_in] = rng.standard_normal(len(rows_in)).astype(np.float32)
+        gb = torch.zeros(P.grid.bsize, device="cuda")
+        ctx.back(views, j, torch.from_numpy(r).cuda(), gb, rects=rects, scale=1.0)
+        torch.cuda.synchronize()
+        gg = gb.cpu().numpy().astype(np.float64)
+        gref = P.bp(views, j, r.astype(np.float64), rects=rects)
+        gabs = P.bp(views, j, np.abs(r).astype(np.float64), rects=rects)
+        d = np.abs(gg - gref)
+        tol = 1e-5 * gabs + 1e-7 * float(np.abs(r).max())
+        worst_bp = max(worst_bp, float(np.max(d / tol)))
+        assert np.all(d <= tol), f"BP block {j}: max |d|/tol = {np.max(d / tol):.3g}"
+        assert np.all(gg[gabs == 0.0] == 0.0) or np.max(np.abs(gg[gabs == 0.0])) <= 1e-7 * float(np.abs(r).max())
+    ctx.close()
+    return worst_fp, worst_bp
+
+
+@pytest.mark.parametrize("name,nviews,blocks_sel", [
+    ("cfg1", 90, None),        # all views, all 2x2 blocks (ties at 0/90 degrees)
+    ("cfg2", 48, None),        # 48 of 360 views, all 16 blocks
+    ("cfg3", 24, None),        # 24 of 360 views, all 8 z-slabs
+    ("cfg4", 3, [0, 3]),       # full size, sampled views, edge + inner slab
+    ("cfg5", 2, [0, 4]),       # full size, sampled views, edge + inner slab
+])
+def test_operator_parity(bs, name, nviews, blocks_sel):
+    p = synth.PRESETS[name]
+    g = p.geometry()
+    views = np.linspace(0, g.n_views - 1, nviews).round().astype(int)
+    views = np.unique(np.concatenate([views, [0, g.n_views // 4]]))[:max(nviews, 2)]
+    bsel = list(range(p.N)) if blocks_sel is None else blocks_sel
+    wf, wb = _fp_bp_check(bs, g, p.blocks, p.M, views, bsel)
+    print(f"{name}: worst FP |d|/tol {wf:.3g}, worst BP |d|/tol {wb:.3g}")
+
+
+def test_operator_parity_rects_and_ragged(bs):
+    """IM-style detector rects, odd detector sizes and a ragged volume/block grid."""
+    vecs = synth.circular("cone", 10, 360.0, 60.0, 40.0, 37, 23, 1.3, 1.1)
+    g = synth.Geometry(synth.CONE, vecs, 37, 23, (30, 22, 18))
+    rng = np.random.default_rng(4)
+    rects = []
+    for _ in range(10):
+        u0 = int(rng.integers(0, 30)); v0 = int(rng.integers(0, 18))
+        rects.append((u0, int(rng.integers(u0 + 1, 38)), v0, int(rng.integers(v0 + 1, 24))))
+    _fp_bp_check(bs, g, (3, 2, 3), 2, np.arange(10), range(18), rects=rects)
+    # parallel 3D with a tilted direction (z component), volume 1 voxel thick in y
+    v = synth.circular("parallel", 6, 180.0, 0, 0, 16, 9, 0.9, 0.8)
+    v[:, 2] = 0.3
+    v[:, 0:3] /= np.linalg.norm(v[:, 0:3], axis=1, keepdims=True)
+    g2 = synth.Geometry(synth.PARALLEL, v, 16, 9, (12, 1, 10))
+    _fp_bp_check(bs, g2, (2, 1, 2), 1, np.arange(6), range(4))
+
+
+def test_im_table(bs):
+    """Ones-pass block masses vs the oracle's traced masses; integer table bit-exact."""
+    for name, kw in [("cfg2", {}), ("cfg3", dict(K=64, n_views=40))]:
+        p = synth.PRESETS[name]
+        if kw:
+            p = synth.scaled(p, **kw)
+        g = p.geometry()
+        ctx = bs.Context.from_geometry(g, p.blocks, p.M, tiles=p.tiles)
+        w, q = ctx.im_weights()
+        P = Projector(g, BlockGrid(g.dims, p.blocks))
+        qo = ob.im_table(P, p.tiles)
+        for j in range(p.N):
+            wo = P.tile_mass(np.arange(g.n_views), j, p.tiles)
+            assert np.allclose(w[j], wo, rtol=1e-11, atol=1e-9)
+        frac = 65536.0 * w / np.maximum(w.sum(axis=2, keepdims=True), 1e-300)
+        margin = np.abs(frac - np.round(frac))
+        ambiguous = margin < 1e-7
+        assert np.array_equal(q[~ambiguous], qo[~ambiguous]), "IM table differs away from rounding boundaries"
+        ctx.close()
+
+
+def _run_pair(bs, p, g, vol32, y, epochs, mu, flags=0, oracle_kw=None, run_kw=None, row_seed=11):
+    """Run the library and the oracle from the same inputs; return both logs."""
+    oracle_kw = oracle_kw or {}
+    run_kw = run_kw or {}
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    x_true_b = P.grid.to_blocks(vol32)
+    prm = ob.Params(seed=3, mu=float(np.float32(mu)), rows_per_epoch=run_kw.get("rows_per_epoch", p.rows_per_epoch),
+                    cols_per_epoch=run_kw.get("cols_per_epoch", p.cols_per_epoch), total_epochs=epochs, **oracle_kw)
+    o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=row_seed,
+                      tiles=p.tiles, x_true=x_true_b.astype(np.float64))
+    for _ in range(epochs):
+        o.epoch()
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=row_seed, tiles=p.tiles)
+    yd = torch.from_numpy(y).cuda()
+    xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    xt = torch.from_numpy(x_true_b.ravel().copy()).cuda()
+    kw = dict(rows_per_epoch=p.rows_per_epoch, cols_per_epoch=p.cols_per_epoch)
+    kw.update(run_kw)
+    res = ctx.run(yd, xd, epochs=epochs, mu0=float(np.float32(mu)), seed=3, x_true=xt, flags=flags, **kw)
+    x_gpu = xd.cpu().numpy().astype(np.float64)
+    ctx.close()
+    return o, res, x_gpu
+
+
+def _compare(o, res, x_gpu, sgd=False, tol=1e-3):
+    assert [r["rows"] for r in o.log] == res.sel_rows.tolist()
+    if not sgd:
+        assert [r["cols"] for r in o.log] == res.sel_cols.tolist()
+    obj = np.array([r["obj"] for r in o.log])
+    rmse = np.array([r["rmse"] for r in o.log])
+    mu = np.array([r["mu"] for r in o.log])
+    e_obj = np.max(np.abs(res.obj - obj) / obj)
+    e_rmse = np.max(np.abs(res.rmse - rmse) / rmse)
+    assert np.allclose(res.mu, mu, rtol=1e-12), (res.mu, mu)
+    assert e_obj < tol and e_rmse < tol, (e_obj, e_rmse)
+    xo = o.x.ravel()
+    e_x = np.max(np.abs(x_gpu - xo)) / np.max(np.abs(xo))
+    assert e_x < 10 * tol, e_x
+    return e_obj, e_rmse, e_x
+
+
+def test_trajectory_cfg1_gd_and_stochastic(bs):
+    p, g, vol32, y = problem("cfg1")
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    smax2 = ob.power_iteration(P, 100, seed=1)
+    mu = 0.5 / smax2
+    # (i) alpha = gamma = 1: GD
+    o, res, x = _run_pair(bs, p, g, vol32, y, 20, mu, run_kw=dict(rows_per_epoch=4, cols_per_epoch=4))
+    print("cfg1 GD", _compare(o, res, x))
+    assert np.all(np.diff(res.obj) <= 0)           # monotone on noiseless data
+    # (ii) alpha M = gamma N = 1
+    o, res, x = _run_pair(bs, p, g, vol32, y, 20, mu)
+    print("cfg1 stochastic", _compare(o, res, x))
+
+
+@pytest.mark.parametrize("uniform", [False, True])
+def test_trajectory_cfg2_im(bs, uniform):
+    p, g, vol32, y = problem("cfg2")
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 0.5 / ob.power_iteration(P, 30, seed=1)
+    flags = bs.IS | (bs.IS_UNIFORM if uniform else 0)
+    o, res, x = _run_pair(bs, p, g, vol32, y, 20, mu, flags=flags,
+                          oracle_kw=dict(im=True, im_uniform=uniform))
+    print("cfg2 IM" if not uniform else "cfg2 RAN", _compare(o, res, x))
+
+
+def test_trajectory_cfg3_bsgd_and_sgd(bs):
+    p, g, vol32, y = problem("cfg3")
+    mu = 0.5 / 8.93e4 / 2          # below 0.5/sigma_max^2 (sigma_max^2 >= 8.93e4)
+    o, res, x = _run_pair(bs, p, g, vol32, y, 20, mu)
+    print("cfg3 BSGD", _compare(o, res, x))
+    o, res, x = _run_pair(bs, p, g, vol32, y, 4, mu, flags=bs.SGD, oracle_kw=dict(sgd=True))
+    print("cfg3 SGD", _compare(o, res, x, sgd=True))
+
+
+def test_trajectory_tv_auto_mu(bs):
+    """BSGD-TV (Algo 4) + auto-mu (Algo 3) on a scaled cfg4 (M = 10, N = 8)."""
+    p, g, vol32, y = problem("cfg4", K=48, n_views=60)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 2.0 / ob.power_iteration(P, 30, seed=1)        # large: auto-mu must act
+    o, res, x = _run_pair(bs, p, g, vol32, y, 60, mu, flags=bs.TV | bs.AUTO_MU,
+                          oracle_kw=dict(tv=True, auto_mu=True, lam=0.1), run_kw=dict(lam=0.1, tv_iters=20))
+    print("cfg4-scaled TV+auto-mu", _compare(o, res, x), "mu:", res.mu[::10])
+
+
+def test_power_iteration(bs):
+    p, g, vol32, y = problem("cfg1")
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    ref = ob.power_iteration(P, 200, seed=1)
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M)
+    got = ctx.power_iteration(200, seed=3)
+    ctx.close()
+    assert abs(got - ref) / ref < 1e-3
+
+
+def test_full_size_engine_step_cfg5(bs):
+    """cfg5 (1024^3, 720 x 1024^2) in the launch configuration bench.py times
+    (one row block of 72 views, all 8 z-slabs), checked on sampled outputs:
+    FP z^j on sampled detector rows; BP g_hat on two 16-plane sub-slabs."""
+    p = synth.PRESETS["cfg5"]
+    g = p.geometry()
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=1)
+    rows = [ctx.row_block_views(i) for i in range(p.M)]
+    views = rows[0]
+    ells = synth.ellipsoids_world("random", g.dims)
+    # --- BP at full size: x = 0 so r_I = y_I and g_hat^0_J = 2 A^T y_I
+    rng = np.random.default_rng(2)
+    y = np.zeros(g.n_rays, dtype=np.float32)
+    yv = synth.analytic_projection(g, ells, views=views, device="cuda").astype(np.float32)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    rr = P.rows_of(views)
+    y[rr] = yv.ravel()
+    yd = torch.from_numpy(y).cuda()
+    xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    ctx.reset(yd)
+    ctx.step(yd, xd, [0], list(range(8)), mu=1e-7)
+    sub = Projector(g, BlockGrid(g.dims, (1, 1, 64)))          # 16-plane sub-slabs
+    for zb in [5, 30]:                                         # inside slab 0 and slab 3
+        j = zb // 8
+        gh = ctx.get_state(1, 0 * ctx.owned_count + j).astype(np.float64)
+        lo, hi = sub.grid.box(zb)
+        bd = P.grid.bdims
+        gh_sub = gh.reshape(bd[2], bd[1], bd[0])[lo[2] - j * bd[2]:hi[2] - j * bd[2]].ravel()
+        ref = 2.0 * sub.bp(views, zb, y.astype(np.float64))
+        absref = 2.0 * sub.bp(views, zb, np.abs(y).astype(np.float64))
+        d = np.abs(gh_sub - ref)
+        tol = 1e-5 * absref + 1e-7 * 2.0 * float(np.abs(y).max())
+        assert np.all(d <= tol), f"sub-slab {zb}: max |d|/tol {np.max(d / tol):.3g}"
+    # --- FP at full size: x = phantom, z^j on sampled detector rows of sampled views
+    x0 = (rng.random(ctx.owned_count * ctx.block_voxels, dtype=np.float32))
+    xd = torch.from_numpy(x0).cuda()
+    ctx.reset(yd)
+    ctx.step(yd, xd, [0], list(range(8)), mu=0.0)
+    sv = [views[0], views[len(views) // 2]]
+    rects = [(0, 1024, 300, 302), (0, 1024, 700, 701)]
+    xb = x0.reshape(8, -1)
+    for j in range(8):
+        zg = ctx.get_state(0, j).astype(np.float64)
+        for v in sv:
+            for (u0, u1, v0, v1) in rects:
+                ref = P.fp([v], j, xb[j].astype(np.float64), rects=[(u0, u1, v0, v1)])
+                ids = np.array([(v * 1024 + iv) * 1024 + iu for iv in range(v0, v1) for iu in range(u0, u1)])
+                d = np.abs(zg[ids] - ref[ids])
+                tol = 1e-5 * ref[ids] + 1e-7
+                assert np.all(d <= tol), f"slab {j} view {v}: max |d|/tol {np.max(d / tol):.3g}"
+    ctx.close()
