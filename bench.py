@@ -191,8 +191,11 @@ def run_ours(args, rank, world, local_rank):
     # synthetic data shaped like the paper's workload: analytic projections of 32
     # seeded random ellipsoids (replicated y), x0 = 0 (Algo 1 line 1)
     y = torch.empty(g.n_rays, dtype=torch.float32, device="cuda")
-    ells = synth.ellipsoids_world("random", g.dims)
-    synth.analytic_projection(g, ells, device="cuda", out_torch=y, chunk_rays=1 << 23)
+    if args.cheap_data:   # profiling runs: seeded uniform data (Siddon work does not depend on values)
+        y.uniform_(0.0, 100.0, generator=torch.Generator(device="cuda").manual_seed(7))
+    else:
+        ells = synth.ellipsoids_world("random", g.dims)
+        synth.analytic_projection(g, ells, device="cuda", out_torch=y, chunk_rays=1 << 23)
     x = torch.zeros(n_owned, dtype=torch.float32, device="cuda")
     mu0 = 0.25 / 7.35e5          # below 1/sigma_max^2 (sigma_max^2 >= 7.35e5)
     aM, gN = p.rows_per_epoch, p.cols_per_epoch
@@ -277,6 +280,12 @@ def run_ours(args, rank, world, local_rank):
                    "visits_per_epoch_fp": vis_ep * world if world == 1 else None,
                    "fp64": "ray parameters fp64, values fp32"},
         "phase_ms": {"fp": fp_ms, "residual_allreduce": res_ms, "bp": bp_ms, "step": st_ms},
+        "allreduce": None if world == 1 else {
+            "bytes_per_epoch": 4 * 72 * g.det_u * g.det_v,
+            "bus_gbs_lower_bound":(4 * 72 * g.det_u * g.det_v) / (res_ms / 1e3) * 2 * (world - 1) / world / 1e9,
+            "vs_gbs": 900.0,
+            "note": "residual phase time includes the partial-sum and residual kernels, so this is a lower bound "
+                    "on the collective's own bus bandwidth"},
         "roofline": {"bound": "hbm", "kernel": "k_project<FP>" if dom == "fp" else "k_project<BP>",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
@@ -302,6 +311,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cheap-data", action="store_true", help="uniform random y instead of analytic projections")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

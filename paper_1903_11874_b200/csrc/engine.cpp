@@ -150,6 +150,51 @@ struct bsgd_ctx_s {
     }
     bool owned(int j) const { return j >= first && j < first + s; }
 
+    // Detector pixels (u0,u1,v0,v1) whose rays can meet the box [lo,hi) (grid coords):
+    // bounding box of the projected corners + 1 pixel margin, u aligned to warps.
+    // Falls back to the whole detector when a corner is not in front of the source.
+    int band_rows = 4;
+    int4 footprint(const int lo[3], const int hi[3], int view) const {
+        const int4 full = make_int4(0, nu, 0, nv);
+        const double* q = &vecs[12 * (size_t)view];
+        const double *d = q + 3, *u = q + 6, *v = q + 9;
+        auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
+        double n[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+        const double uu = dot(u, u), vv = dot(v, v), uv = dot(u, v), det = uu * vv - uv * uv;
+        if (!(det > 0)) return full;
+        double amn = 1e300, amx = -1e300, bmn = 1e300, bmx = -1e300;
+        for (int c = 0; c < 8; ++c) {
+            double P[3] = {(c & 1 ? hi[0] : lo[0]) - dims[0] / 2.0, (c & 2 ? hi[1] : lo[1]) - dims[1] / 2.0,
+                           (c & 4 ? hi[2] : lo[2]) - dims[2] / 2.0};
+            double Q[3];
+            if (beam == BSGD_PARALLEL) {
+                const double dn = dot(q, n);
+                if (fabs(dn) < 1e-12) return full;
+                double dp[3] = {d[0] - P[0], d[1] - P[1], d[2] - P[2]};
+                const double mu_ = dot(dp, n) / dn;
+                for (int k = 0; k < 3; ++k) Q[k] = P[k] + mu_ * q[k];
+            } else {
+                double ps[3] = {P[0] - q[0], P[1] - q[1], P[2] - q[2]}, ds[3] = {d[0] - q[0], d[1] - q[1], d[2] - q[2]};
+                const double den = dot(ps, n), num = dot(ds, n);
+                if (!(den * num > 0)) return full;
+                const double lam = num / den;
+                for (int k = 0; k < 3; ++k) Q[k] = q[k] + lam * ps[k];
+            }
+            double r[3] = {Q[0] - d[0], Q[1] - d[1], Q[2] - d[2]};
+            const double ru = dot(r, u), rv = dot(r, v);
+            const double al = (ru * vv - rv * uv) / det, be = (rv * uu - ru * uv) / det;
+            amn = std::min(amn, al); amx = std::max(amx, al);
+            bmn = std::min(bmn, be); bmx = std::max(bmx, be);
+        }
+        const double cu = (nu - 1) / 2.0, cv = (nv - 1) / 2.0;
+        auto clampi = [](double x, int lo_, int hi_) { return (int)std::min<double>(std::max<double>(x, lo_), hi_); };
+        int u0 = clampi(floor(amn + cu) - 1, 0, nu), u1 = clampi(ceil(amx + cu) + 2, 0, nu);
+        int v0 = clampi(floor(bmn + cv) - 1, 0, nv), v1 = clampi(ceil(bmx + cv) + 2, 0, nv);
+        u0 = (u0 / 32) * 32;
+        u1 = std::min(nu, ((u1 + 31) / 32) * 32);
+        return make_int4(u0, u1, v0, v1);
+    }
+
     // pack host tables into the device arena; returns device pointers
     template <class T> T* tab_put(size_t& off, const std::vector<T>& v, std::vector<char>& staging) {
         off = (off + 15) & ~(size_t)15;
@@ -193,7 +238,26 @@ struct bsgd_ctx_s {
         std::vector<int4> rc = rects;
         int maxr = 0;
         if (rc.empty()) rc.assign((size_t)nb * ns, make_int4(0, nu, 0, nv));
+        // footprint culling: only detector pixels whose rays can meet the block box
+        const int R = band_rows;
+        int maxw = 0, nbands = 0;
+        for (int b = 0; b < nb; ++b) {
+            int vlo = nv, vhi = 0;
+            for (int k = 0; k < ns; ++k) {
+                int4& q = rc[(size_t)b * ns + k];
+                int4 f = footprint(bl[b].lo, bl[b].hi, views[k]);
+                q.x = std::max(q.x, f.x); q.y = std::min(q.y, f.y);
+                q.z = std::max(q.z, f.z); q.w = std::min(q.w, f.w);
+                if (q.x >= q.y || q.z >= q.w) { q = make_int4(0, 0, 0, 0); continue; }
+                maxw = std::max(maxw, q.y - q.x);
+                vlo = std::min(vlo, q.z);
+                vhi = std::max(vhi, q.w);
+            }
+            bl[b].band_lo = vlo < vhi ? vlo / R : 0;
+            if (vlo < vhi) nbands = std::max(nbands, (vhi - 1) / R - vlo / R + 1);
+        }
         for (auto& q : rc) maxr = std::max(maxr, (q.y - q.x) * (q.w - q.z));
+        if (maxr == 0) return;
         std::vector<char> staging;
         size_t off = tab_off;
         staging.resize(off);
@@ -205,6 +269,9 @@ struct bsgd_ctx_s {
         L.n_blocks = nb;
         L.blocks = tab_put(off, bl, staging);
         L.max_rect_rays = maxr;
+        L.rows_per_band = R;
+        L.n_chunks = (R * maxw + 255) / 256;
+        L.n_bands = nbands;
         L.rproj = rproj;
         L.scale = scale;
         L.accumulate = accumulate;
@@ -671,6 +738,8 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         }
         c->s = c->N / c->world;
         c->first = c->rank * c->s;
+        if (const char* e = getenv("BSGD_BAND_ROWS")) c->band_rows = std::max(1, atoi(e));
+        if (c->bsize >= (1LL << 31)) fail(BSGD_E_PARTITION, "a column block must hold fewer than 2^31 voxels");
         // row blocks
         std::vector<int32_t> vv(c->n_views), off(c->M + 1);
         host::view_partition(c->n_views, c->M, c->kind, c->row_seed, vv.data(), off.data());
@@ -760,6 +829,18 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
         std::vector<int4> rc;
         if (rects)
             for (int k = 0; k < n; ++k) rc.push_back(make_int4(rects[4 * k], rects[4 * k + 1], rects[4 * k + 2], rects[4 * k + 3]));
+        else
+            rc.assign(n, make_int4(0, c->nu, 0, c->nv));
+        if (!accumulate) {   // overwrite semantics: rays of the rects outside the footprint become 0
+            std::vector<char> staging;
+            size_t off = c->tab_bytes / 2;
+            staging.resize(off);
+            const int* dv = c->tab_put(off, vv, staging);
+            const int4* dr = c->tab_put(off, rc, staging);
+            BSGD_CUDA(cudaMemcpyAsync(c->d_tab + c->tab_bytes / 2, staging.data() + c->tab_bytes / 2,
+                                      off - c->tab_bytes / 2, cudaMemcpyHostToDevice, st));
+            launch_zero_rects(proj, dv, dr, n, c->nu, c->nv, st);
+        }
         c->project(PROJ_FP, vv, {b}, rc, {x_block}, {c->fp_scratchT}, {}, {}, {proj}, nullptr, 0.f, accumulate,
                    st, 0);
     });

@@ -51,6 +51,7 @@ struct BlockDesc {
     float* outT;         // BP target (transposed layout)
     float* z;            // FP target, full-length projection vector
     int lo[3], hi[3];    // box in grid coordinates
+    int band_lo;         // first detector-row band with work for this block
 };
 
 struct ProjLaunch {
@@ -61,6 +62,9 @@ struct ProjLaunch {
     int n_blocks;              // grid.z
     const BlockDesc* blocks;   // device [n_blocks]
     int max_rect_rays;
+    int rows_per_band;         // R: detector rows per band (band-major CTA order)
+    int n_chunks;              // CTAs per (band, slot)
+    int n_bands;               // max bands per block (grid.x = n_bands * n_slots * n_chunks)
     const float* rproj;        // BP input (full length)
     float scale;               // BP scale (2 in Algo 1)
     int accumulate;            // FP: add into z instead of overwriting
@@ -104,6 +108,7 @@ struct ResLaunch {
 void launch_residual(const ResLaunch& R, cudaStream_t st);
 
 void launch_zero_rows(double* normsq, const int* rows, int n, cudaStream_t st);
+void launch_zero_rects(float* proj, const int* views, const int4* rects, int n, int nu, int nv, cudaStream_t st);
 void launch_obj(const double* normsq, int M, double* out, cudaStream_t st);
 void launch_axpy_eud(float* eud, const float* g, long long n, cudaStream_t st);
 void launch_dot3(const float* a, const float* b, long long n, double* out3, cudaStream_t st);

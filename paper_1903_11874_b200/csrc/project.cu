@@ -18,6 +18,7 @@
 //    the slow in-plane axis of the layout that is read.
 //  * no tensor cores: this is a sparse gather/scatter.
 #include <climits>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -198,6 +199,191 @@ __global__ void __launch_bounds__(256) k_project(const ProjLaunch L) {
     }
 }
 
+// v2 traversal: the same slice-lockstep Siddon, with a straight-line slice body for the
+// common case (at most one x and one z plane crossing inside the slice: up to three
+// segments, their loads issued together), a rare general loop for further crossings,
+// 32-bit voxel offsets and fp32 slice sums flushed into an fp64 accumulator.
+template <int MODE>
+__global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
+    // band-major CTA order: blockIdx.x = (band * n_slots + slot) * n_chunks + chunk, so the
+    // CTAs resident at any time cover the same detector-row band of consecutive views
+    // (rays of one band cross the same z-range of the volume -> L2 reuse across views).
+    const BlockDesc& B = L.blocks[blockIdx.z];
+    unsigned bid = blockIdx.x;
+    const int chunk = (int)(bid % (unsigned)L.n_chunks);
+    bid /= (unsigned)L.n_chunks;
+    const int slot = (int)(bid % (unsigned)L.n_slots);
+    const int band = B.band_lo + (int)(bid / (unsigned)L.n_slots);
+    const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
+    const int r0 = max(rc.z, band * L.rows_per_band), r1 = min(rc.w, band * L.rows_per_band + L.rows_per_band);
+    const int w = rc.y - rc.x;
+    if (r0 >= r1 || w <= 0) return;
+    const int nrect = (r1 - r0) * w;
+    const int base = chunk * (int)blockDim.x;
+    if (base >= nrect) return;                       // uniform over the CTA
+    const int tid = base + (int)threadIdx.x;
+    const bool inrect = tid < nrect;
+    const int iu = rc.x + (inrect ? tid % w : 0);
+    const int iv = r0 + (inrect ? tid / w : 0);
+    const int view = L.views[slot];
+    const double* vec = L.g.vecs + 12 * (size_t)view;
+    const double cxv = (L.g.beam == BSGD_PARALLEL) ? vec[0] : vec[3] - vec[0];
+    const double cyv = (L.g.beam == BSGD_PARALLEL) ? vec[1] : vec[4] - vec[1];
+    const bool mainX = fabs(cxv) > fabs(cyv);
+
+    double a[3], b[3];
+    make_ray(L.g, vec, iu, iv, a, b);
+    const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
+    if (mainX) {
+        double t = a[0]; a[0] = a[1]; a[1] = t;
+        t = b[0]; b[0] = b[1]; b[1] = t;
+        int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
+        q = hi[0]; hi[0] = hi[1]; hi[1] = q;
+    }
+    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1], bdz = hi[2] - lo[2];
+    const unsigned plane = (unsigned)bdx * (unsigned)bdy;
+    double inv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
+    double amin, amax;
+    bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
+    float rs = 0.f;
+    if (MODE == PROJ_BP) {
+        if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
+        hit = hit && (rs != 0.f);
+    }
+    const float* __restrict__ src = mainX ? B.xT : B.xN;
+    float* dst = mainX ? B.outT : B.outN;
+
+    const int sx = sgn(b[0]), sy = sgn(b[1]), sz = sgn(b[2]);
+    int j0 = 0, j1 = -1, ix = 0, iz = 0;
+    double t = 0.0, tx = 0.0, tz = 0.0;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    if (hit) {
+        j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
+        j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
+        if (sy == 0) j1 = j0;
+        ix = cell_enter(a[0] + amin * b[0], sx, lo[0], hi[0]);
+        iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
+        tx = sx ? ((double)(ix + (sx > 0)) - a[0]) * inv[0] : INF;
+        tz = sz ? ((double)(iz + (sz > 0)) - a[2]) * inv[2] : INF;
+        t = amin;
+    }
+    // voxel offsets relative to the block origin (frame coordinates)
+    const int ox = lo[0], oz = lo[2];
+    const int pstep = sz * (int)plane;
+    double acc = 0.0;
+    float acc32 = 0.f;
+    unsigned int nvis = 0;
+    const double a0 = a[0], a1 = a[1], a2 = a[2], inv0 = inv[0], inv1 = inv[1], inv2 = inv[2];
+
+    for (int pass = 0; pass < 2; ++pass) {
+        const int dir = pass == 0 ? 1 : -1;
+        const bool mine = hit && (pass == 0 ? sy >= 0 : sy < 0);
+        if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
+        int jl = mine ? min(j0, j1) : INT_MAX;
+        int jh = mine ? max(j0, j1) : INT_MIN;
+        jl = __reduce_min_sync(0xffffffffu, jl);
+        jh = __reduce_max_sync(0xffffffffu, jh);
+        const int jstart = dir > 0 ? jl : jh;
+        const int nsl = jh - jl + 1;
+        for (int k = 0; k < nsl; ++k) {
+            const int j = jstart + dir * k;
+            const bool in = mine && (dir > 0 ? (j >= j0 && j <= j1) : (j <= j0 && j >= j1));
+            if (in) {
+                double thi = amax;
+                if (sy != 0) thi = fmin(amax, ((double)(sy > 0 ? j + 1 : j) - a1) * inv1);
+                const bool cx = tx < thi, cz = tz < thi;
+                const double tcx = cx ? tx : thi, tcz = cz ? tz : thi;
+                const bool xfirst = tcx <= tcz;
+                const double m1 = fmax(xfirst ? tcx : tcz, t);
+                const double m2 = fmax(xfirst ? tcz : tcx, t);
+                const int ix2 = ix + (cx ? sx : 0), iz2 = iz + (cz ? sz : 0);
+                const int ix1 = xfirst ? ix2 : ix, iz1 = xfirst ? iz : iz2;
+                const unsigned row = (unsigned)(j - lo[1]) * (unsigned)bdx;
+                const unsigned o0 = (unsigned)(iz - oz) * plane + row + (unsigned)(ix - ox);
+                const unsigned o1 = o0 + (xfirst ? (cx ? sx : 0) : (cz ? pstep : 0));
+                const unsigned o2 = o0 + (cx ? sx : 0) + (cz ? pstep : 0);
+                const bool in0 = (unsigned)(ix - ox) < (unsigned)bdx && (unsigned)(iz - oz) < (unsigned)bdz;
+                const bool in1 = (unsigned)(ix1 - ox) < (unsigned)bdx && (unsigned)(iz1 - oz) < (unsigned)bdz;
+                const bool in2 = (unsigned)(ix2 - ox) < (unsigned)bdx && (unsigned)(iz2 - oz) < (unsigned)bdz;
+                // next crossings after one step on each crossing axis
+                const double ntx = cx ? ((double)(ix2 + (sx > 0)) - a0) * inv0 : tx;
+                const double ntz = cz ? ((double)(iz2 + (sz > 0)) - a2) * inv2 : tz;
+                // rare: a second crossing of the same axis inside the slice -> only the first
+                // crossing is committed here and the general loop takes the rest from m1
+                const bool more = (cx && ntx < thi) || (cz && ntz < thi);
+                if (!more) {
+                    ix = ix2; iz = iz2; tx = ntx; tz = ntz;
+                } else if (xfirst) {
+                    ix = ix1; tx = ntx;       // xfirst && more implies cx
+                } else {
+                    iz = iz1; tz = ntz;
+                }
+                const float l0 = (float)((m1 - t) * blen);
+                const float l1 = more ? 0.f : (float)((m2 - m1) * blen);
+                const float l2 = more ? 0.f : (float)((thi - m2) * blen);
+                const bool v0 = in0 && l0 > 0.f, v1 = in1 && l1 > 0.f, v2 = in2 && l2 > 0.f;
+                if (MODE == PROJ_FP) {
+                    const float x0 = v0 ? __ldg(src + o0) : 0.f;
+                    const float x1 = v1 ? __ldg(src + o1) : 0.f;
+                    const float x2 = v2 ? __ldg(src + o2) : 0.f;
+                    acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
+                }
+                if (MODE == PROJ_BP) {
+                    if (v0) atomicAdd(dst + o0, l0 * rs);
+                    if (v1) atomicAdd(dst + o1, l1 * rs);
+                    if (v2) atomicAdd(dst + o2, l2 * rs);
+                }
+                nvis += (unsigned)v0 + (unsigned)v1 + (unsigned)v2;
+                if (more) {   // general loop for the rest of the slice, from m1 at (ix, iz)
+                    double tt = m1;
+                    for (;;) {
+                        const double tn = fmin(fmin(tx, tz), thi);
+                        if (tn > tt) {
+                            if ((unsigned)(ix - ox) < (unsigned)bdx && (unsigned)(iz - oz) < (unsigned)bdz) {
+                                const unsigned o = (unsigned)(iz - oz) * plane + row + (unsigned)(ix - ox);
+                                const float len = (float)((tn - tt) * blen);
+                                if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
+                                if (MODE == PROJ_BP) atomicAdd(dst + o, len * rs);
+                                ++nvis;
+                            }
+                            tt = tn;
+                        }
+                        if (tx <= tz) {
+                            if (tx < thi) {
+                                ix += sx;
+                                tx = ((double)(ix + (sx > 0)) - a0) * inv0;
+                                continue;
+                            }
+                        } else if (tz < thi) {
+                            iz += sz;
+                            tz = ((double)(iz + (sz > 0)) - a2) * inv2;
+                            continue;
+                        }
+                        break;
+                    }
+                }
+                t = thi;
+                if (MODE == PROJ_FP && (k & 15) == 15) {
+                    acc += (double)acc32;
+                    acc32 = 0.f;
+                }
+            }
+        }
+    }
+    if (MODE == PROJ_FP && inrect) {
+        acc += (double)acc32;
+        float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
+        *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
+    }
+    if (L.visits) {
+        unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits, (unsigned long long)s);
+    }
+}
+
 // Ones-pass: w[b][view][t] = sum over tile rays of chord(ray, box_b) = (A_t^{J_b} 1) summed.
 __global__ void __launch_bounds__(256) k_im_weights(const ImLaunch I) {
     const int view = blockIdx.y;
@@ -240,9 +426,21 @@ __global__ void __launch_bounds__(256) k_im_weights(const ImLaunch I) {
 void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
     if (L.n_slots == 0 || L.n_blocks == 0 || L.max_rect_rays == 0) return;
     dim3 grid((unsigned)((L.max_rect_rays + 255) / 256), (unsigned)L.n_slots, (unsigned)L.n_blocks);
-    if (mode == PROJ_FP) k_project<PROJ_FP><<<grid, 256, 0, st>>>(L);
-    else if (mode == PROJ_BP) k_project<PROJ_BP><<<grid, 256, 0, st>>>(L);
-    else k_project<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
+    static const int version = [] {
+        const char* e = getenv("BSGD_PROJECTOR");
+        return e ? atoi(e) : 2;
+    }();
+    if (version == 1) {
+        if (mode == PROJ_FP) k_project<PROJ_FP><<<grid, 256, 0, st>>>(L);
+        else if (mode == PROJ_BP) k_project<PROJ_BP><<<grid, 256, 0, st>>>(L);
+        else k_project<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
+    } else {
+        dim3 g2((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
+        if (g2.x == 0) return;
+        if (mode == PROJ_FP) k_project2<PROJ_FP><<<g2, 256, 0, st>>>(L);
+        else if (mode == PROJ_BP) k_project2<PROJ_BP><<<g2, 256, 0, st>>>(L);
+        else k_project2<PROJ_COUNT><<<g2, 256, 0, st>>>(L);
+    }
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

@@ -31,57 +31,156 @@ __device__ __forceinline__ double block_sum(double v) {
     return v;   // valid in thread 0
 }
 
-__global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U, const int mode) {
+// Vectorised variant for block dims that are multiples of 32: thread (q, r) of an
+// 8 x 32 CTA owns the float4 x = x0+4q..+3 at y = y0+r of the normal layout and the
+// float4 y = y0+4q..+3 at x = x0+r of the transposed layout; both 32x33 shared-memory
+// transposes are bank-conflict free.  All loads are issued before any store.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_block_update4(const UpdLaunch U) {
+    __shared__ float tT[32][33];
+    __shared__ float tX[32][33];
+    const int bdx = U.bd[0], bdy = U.bd[1];
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    const long long zoff = (long long)blockIdx.z * bdx * bdy;
+    const int q = threadIdx.x, r = threadIdx.y;
+    constexpr bool use_acc = MODE != UPD_XT;
+    const bool final_ = U.final_ != 0;
+    const bool writes_x = (MODE == UPD_XT) || ((MODE == UPD_BSGD || MODE == UPD_SGD) && final_);
+    const bool needs_x = (MODE == UPD_BSGD && final_) || MODE == UPD_SGD || MODE == UPD_XT;
+    const long long in_ = zoff + (long long)(y0 + r) * bdx + x0 + 4 * q;     // normal layout
+    const long long it_ = zoff + (long long)(x0 + r) * bdy + y0 + 4 * q;     // transposed layout
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 vT = z4, vN = z4, vgh = z4, vg = z4, vx = z4, vo = z4;
+    if (use_acc) {
+        vT = *reinterpret_cast<const float4*>(U.accT + it_);
+        vN = *reinterpret_cast<const float4*>(U.accN + in_);
+    }
+    if (MODE == UPD_BSGD) {
+        vgh = *reinterpret_cast<const float4*>(U.ghat + in_);
+        vg = *reinterpret_cast<const float4*>(U.g + in_);
+    }
+    if (needs_x) vx = *reinterpret_cast<const float4*>(U.x + in_);
+    if (MODE == UPD_OUT && U.accumulate) vo = *reinterpret_cast<const float4*>(U.out + in_);
+    if (use_acc) {
+        tT[r][4 * q + 0] = vT.x; tT[r][4 * q + 1] = vT.y; tT[r][4 * q + 2] = vT.z; tT[r][4 * q + 3] = vT.w;
+        *reinterpret_cast<float4*>(U.accT + it_) = z4;
+        *reinterpret_cast<float4*>(U.accN + in_) = z4;
+    }
+    __syncthreads();
+    float nv[4] = {vN.x, vN.y, vN.z, vN.w};
+    if (use_acc) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) nv[e] += tT[4 * q + e][r];
+    }
+    const float gh[4] = {vgh.x, vgh.y, vgh.z, vgh.w}, gg[4] = {vg.x, vg.y, vg.z, vg.w};
+    const float xx[4] = {vx.x, vx.y, vx.z, vx.w}, oo[4] = {vo.x, vo.y, vo.z, vo.w};
+    float ng[4], nx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (MODE == UPD_BSGD) {
+            ng[e] = gg[e] + (nv[e] - gh[e]);
+            nx[e] = final_ ? xx[e] + U.mu * ng[e] : 0.f;
+        } else if (MODE == UPD_SGD) {
+            ng[e] = nv[e];
+            nx[e] = xx[e] + U.mu * nv[e];
+        } else if (MODE == UPD_OUT) {
+            ng[e] = oo[e] + nv[e];
+            nx[e] = 0.f;
+        } else {
+            ng[e] = 0.f;
+            nx[e] = xx[e];
+        }
+        tX[4 * q + e][r] = nx[e];
+    }
+    if (MODE == UPD_BSGD) {
+        *reinterpret_cast<float4*>(U.ghat + in_) = make_float4(nv[0], nv[1], nv[2], nv[3]);
+        *reinterpret_cast<float4*>(U.g + in_) = make_float4(ng[0], ng[1], ng[2], ng[3]);
+        if (final_) *reinterpret_cast<float4*>(U.x + in_) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+    } else if (MODE == UPD_SGD) {
+        *reinterpret_cast<float4*>(U.g + in_) = make_float4(ng[0], ng[1], ng[2], ng[3]);
+        *reinterpret_cast<float4*>(U.x + in_) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+    } else if (MODE == UPD_OUT) {
+        *reinterpret_cast<float4*>(U.out + in_) = make_float4(ng[0], ng[1], ng[2], ng[3]);
+    }
+    if (!writes_x) return;
+    __syncthreads();
+    *reinterpret_cast<float4*>(U.xT + it_) =
+        make_float4(tX[r][4 * q + 0], tX[r][4 * q + 1], tX[r][4 * q + 2], tX[r][4 * q + 3]);
+}
+
+// One 32x32 tile of one z-plane per CTA (32 x 8 threads, 4 elements each).  All global
+// loads of the tile are issued before any store (the arrays are distinct; the
+// compiler cannot prove it, so the code makes the order explicit) -> 5 loads in
+// flight per element instead of a dependent load/store chain.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U) {
     __shared__ float tT[32][33];
     __shared__ float tX[32][33];
     const int bdx = U.bd[0], bdy = U.bd[1];
     const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
     const long long zoff = (long long)blockIdx.z * bdx * bdy;
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const bool use_acc = mode != UPD_XT;
+    constexpr bool use_acc = MODE != UPD_XT;
+    const bool final_ = U.final_ != 0;
+    const bool writes_x = (MODE == UPD_XT) || ((MODE == UPD_BSGD || MODE == UPD_SGD) && final_);
+    float* __restrict__ accN = U.accN;
+    float* __restrict__ accT = U.accT;
+    float* __restrict__ ghat = U.ghat;
+    float* __restrict__ g = U.g;
+    float* __restrict__ x = U.x;
+    float* __restrict__ out = U.out;
+    float vT[4], vN[4], vgh[4], vg[4], vx[4], vo[4];
+    bool okT[4], ok[4];
+    long long iT[4], idx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int xxT = x0 + ty + 8 * k, yyT = y0 + tx;
+        okT[k] = xxT < bdx && yyT < bdy;
+        iT[k] = zoff + (long long)xxT * bdy + yyT;
+        const int xx = x0 + tx, yy = y0 + ty + 8 * k;
+        ok[k] = xx < bdx && yy < bdy;
+        idx[k] = zoff + (long long)yy * bdx + xx;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        vT[k] = (use_acc && okT[k]) ? accT[iT[k]] : 0.f;
+        vN[k] = (use_acc && ok[k]) ? accN[idx[k]] : 0.f;
+        vgh[k] = (MODE == UPD_BSGD && ok[k]) ? ghat[idx[k]] : 0.f;
+        vg[k] = (MODE == UPD_BSGD && ok[k]) ? g[idx[k]] : 0.f;
+        vx[k] = (((MODE == UPD_BSGD && final_) || MODE == UPD_SGD || MODE == UPD_XT) && ok[k]) ? x[idx[k]] : 0.f;
+        vo[k] = (MODE == UPD_OUT && U.accumulate && ok[k]) ? out[idx[k]] : 0.f;
+    }
     if (use_acc) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int xx = x0 + ty + 8 * k, yy = y0 + tx;
-            float v = 0.f;
-            if (xx < bdx && yy < bdy) {
-                float* p = U.accT + zoff + (long long)xx * bdy + yy;
-                v = *p;
-                *p = 0.f;
-            }
-            tT[ty + 8 * k][tx] = v;
+            tT[ty + 8 * k][tx] = vT[k];
+            if (okT[k]) accT[iT[k]] = 0.f;
         }
     }
     __syncthreads();
-    const bool writes_x = (mode == UPD_XT) || ((mode == UPD_BSGD || mode == UPD_SGD) && U.final_);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int xx = x0 + tx, yy = y0 + ty + 8 * k;
         float xv = 0.f;
-        if (xx < bdx && yy < bdy) {
-            const long long idx = zoff + (long long)yy * bdx + xx;
-            float nv = 0.f;
-            if (use_acc) {
-                nv = U.accN[idx] + tT[tx][ty + 8 * k];
-                U.accN[idx] = 0.f;
-            }
-            if (mode == UPD_BSGD) {
-                const float old = U.ghat[idx];
-                U.ghat[idx] = nv;
-                const float gv = U.g[idx] + (nv - old);
-                U.g[idx] = gv;
-                if (U.final_) {
-                    xv = U.x[idx] + U.mu * gv;
-                    U.x[idx] = xv;
+        if (ok[k]) {
+            const long long i = idx[k];
+            const float nv = use_acc ? vN[k] + tT[tx][ty + 8 * k] : 0.f;
+            if (use_acc) accN[i] = 0.f;
+            if (MODE == UPD_BSGD) {
+                ghat[i] = nv;
+                const float gv = vg[k] + (nv - vgh[k]);
+                g[i] = gv;
+                if (final_) {
+                    xv = vx[k] + U.mu * gv;
+                    x[i] = xv;
                 }
-            } else if (mode == UPD_SGD) {
-                U.g[idx] = nv;
-                xv = U.x[idx] + U.mu * nv;
-                U.x[idx] = xv;
-            } else if (mode == UPD_OUT) {
-                U.out[idx] = U.accumulate ? U.out[idx] + nv : nv;
-            } else if (mode == UPD_XT) {
-                xv = U.x[idx];
+            } else if (MODE == UPD_SGD) {
+                g[i] = nv;
+                xv = vx[k] + U.mu * nv;
+                x[i] = xv;
+            } else if (MODE == UPD_OUT) {
+                out[i] = vo[k] + nv;
+            } else if (MODE == UPD_XT) {
+                xv = vx[k];
             }
         }
         tX[ty + 8 * k][tx] = xv;
@@ -89,10 +188,8 @@ __global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U, const i
     if (!writes_x) return;
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int xx = x0 + ty + 8 * k, yy = y0 + tx;
-        if (xx < bdx && yy < bdy) U.xT[zoff + (long long)xx * bdy + yy] = tX[tx][ty + 8 * k];
-    }
+    for (int k = 0; k < 4; ++k)
+        if (okT[k]) U.xT[iT[k]] = tX[tx][ty + 8 * k];
 }
 
 __global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
@@ -143,6 +240,16 @@ __global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
         ss = block_sum(ss);
         if (threadIdx.x == 0) atomicAdd(R.normsq + R.slot_row[slot], ss);
     }
+}
+
+__global__ void __launch_bounds__(256) k_zero_rects(float* proj, const int* views, const int4* rects, int nu,
+                                                    int nv) {
+    const int slot = blockIdx.y;
+    const int4 rc = rects[slot];
+    const int w = rc.y - rc.x, h = rc.w - rc.z;
+    const long long base = (long long)views[slot] * nv * nu;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < w * h; i += gridDim.x * blockDim.x)
+        proj[base + (long long)(rc.z + i / w) * nu + rc.x + i % w] = 0.f;
 }
 
 __global__ void k_zero_rows(double* normsq, const int* rows, int n) {
@@ -303,7 +410,24 @@ unsigned grid_for(long long n, int per_thread = 1) {
 
 void launch_block_update(int mode, const UpdLaunch& U, cudaStream_t st) {
     dim3 grid((unsigned)((U.bd[0] + 31) / 32), (unsigned)((U.bd[1] + 31) / 32), (unsigned)U.bd[2]);
-    k_block_update<<<grid, dim3(32, 8), 0, st>>>(U, mode);
+    const bool vec = (U.bd[0] % 32 == 0) && (U.bd[1] % 32 == 0) && !(U.out && ((uintptr_t)U.out & 15));
+    if (vec) {
+        switch (mode) {
+            case UPD_BSGD: k_block_update4<UPD_BSGD><<<grid, dim3(8, 32), 0, st>>>(U); break;
+            case UPD_SGD: k_block_update4<UPD_SGD><<<grid, dim3(8, 32), 0, st>>>(U); break;
+            case UPD_OUT: k_block_update4<UPD_OUT><<<grid, dim3(8, 32), 0, st>>>(U); break;
+            default: k_block_update4<UPD_XT><<<grid, dim3(8, 32), 0, st>>>(U); break;
+        }
+        BSGD_CUDA(cudaGetLastError());
+        note_launch();
+        return;
+    }
+    switch (mode) {
+        case UPD_BSGD: k_block_update<UPD_BSGD><<<grid, dim3(32, 8), 0, st>>>(U); break;
+        case UPD_SGD: k_block_update<UPD_SGD><<<grid, dim3(32, 8), 0, st>>>(U); break;
+        case UPD_OUT: k_block_update<UPD_OUT><<<grid, dim3(32, 8), 0, st>>>(U); break;
+        default: k_block_update<UPD_XT><<<grid, dim3(32, 8), 0, st>>>(U); break;
+    }
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
@@ -313,6 +437,13 @@ void launch_residual(const ResLaunch& R, cudaStream_t st) {
     long long nvec = (R.per % 4 == 0) ? R.per / 4 : R.per;
     unsigned gx = (unsigned)std::min<long long>((nvec + 255) / 256, 64);
     k_residual<<<dim3(gx, (unsigned)R.n_slots), 256, 0, st>>>(R);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_zero_rects(float* proj, const int* views, const int4* rects, int n, int nu, int nv, cudaStream_t st) {
+    if (n == 0) return;
+    k_zero_rects<<<dim3(64, (unsigned)n), 256, 0, st>>>(proj, views, rects, nu, nv);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
