@@ -257,26 +257,35 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
     float* dst = mainX ? B.outT : B.outN;
 
     const int sx = sgn(b[0]), sy = sgn(b[1]), sz = sgn(b[2]);
-    int j0 = 0, j1 = -1, ix = 0, iz = 0;
-    double t = 0.0, tx = 0.0, tz = 0.0;
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    // lane state: voxel (rx, rz) relative to the block origin, its offset o, the current t,
+    // the t of the next x / z plane crossing (tx, tz) and of the current slice's exit plane
+    // (tpl).  Plane crossings advance by exact-enough fp64 increments (|1/b|: ~1e-13 drift
+    // over a whole ray); every in-slice decision runs in fp32 on t-differences.
+    int j0 = 0, j1 = -1, rx = 0, rz = 0;
+    double t = 0.0, tx = INF, tz = INF, tpl = INF;
+    unsigned o = 0;
+    const double dtx = fabs(inv[0]), dtz = fabs(inv[2]), dty = fabs(inv[1]);
     if (hit) {
         j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
         j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
         if (sy == 0) j1 = j0;
-        ix = cell_enter(a[0] + amin * b[0], sx, lo[0], hi[0]);
-        iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
-        tx = sx ? ((double)(ix + (sx > 0)) - a[0]) * inv[0] : INF;
-        tz = sz ? ((double)(iz + (sz > 0)) - a[2]) * inv[2] : INF;
+        const int ix = cell_enter(a[0] + amin * b[0], sx, lo[0], hi[0]);
+        const int iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
+        if (sx) tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
+        if (sz) tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
+        if (sy) tpl = ((double)(j0 + (sy > 0)) - a[1]) * inv[1];
         t = amin;
+        rx = ix - lo[0];
+        rz = iz - lo[2];
+        o = (unsigned)rz * plane + (unsigned)(j0 - lo[1]) * (unsigned)bdx + (unsigned)rx;
     }
-    // voxel offsets relative to the block origin (frame coordinates)
-    const int ox = lo[0], oz = lo[2];
     const int pstep = sz * (int)plane;
+    const int rowstep = sy * bdx;
+    const float blen_f = (float)blen;
     double acc = 0.0;
     float acc32 = 0.f;
     unsigned int nvis = 0;
-    const double a0 = a[0], a1 = a[1], a2 = a[2], inv0 = inv[0], inv1 = inv[1], inv2 = inv[2];
 
     for (int pass = 0; pass < 2; ++pass) {
         const int dir = pass == 0 ? 1 : -1;
@@ -292,58 +301,54 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
             const int j = jstart + dir * k;
             const bool in = mine && (dir > 0 ? (j >= j0 && j <= j1) : (j <= j0 && j >= j1));
             if (in) {
-                double thi = amax;
-                if (sy != 0) thi = fmin(amax, ((double)(sy > 0 ? j + 1 : j) - a1) * inv1);
-                const bool cx = tx < thi, cz = tz < thi;
-                const double tcx = cx ? tx : thi, tcz = cz ? tz : thi;
-                const bool xfirst = tcx <= tcz;
-                const double m1 = fmax(xfirst ? tcx : tcz, t);
-                const double m2 = fmax(xfirst ? tcz : tcx, t);
-                const int ix2 = ix + (cx ? sx : 0), iz2 = iz + (cz ? sz : 0);
-                const int ix1 = xfirst ? ix2 : ix, iz1 = xfirst ? iz : iz2;
-                const unsigned row = (unsigned)(j - lo[1]) * (unsigned)bdx;
-                const unsigned o0 = (unsigned)(iz - oz) * plane + row + (unsigned)(ix - ox);
-                const unsigned o1 = o0 + (xfirst ? (cx ? sx : 0) : (cz ? pstep : 0));
-                const unsigned o2 = o0 + (cx ? sx : 0) + (cz ? pstep : 0);
-                const bool in0 = (unsigned)(ix - ox) < (unsigned)bdx && (unsigned)(iz - oz) < (unsigned)bdz;
-                const bool in1 = (unsigned)(ix1 - ox) < (unsigned)bdx && (unsigned)(iz1 - oz) < (unsigned)bdz;
-                const bool in2 = (unsigned)(ix2 - ox) < (unsigned)bdx && (unsigned)(iz2 - oz) < (unsigned)bdz;
-                // next crossings after one step on each crossing axis
-                const double ntx = cx ? ((double)(ix2 + (sx > 0)) - a0) * inv0 : tx;
-                const double ntz = cz ? ((double)(iz2 + (sz > 0)) - a2) * inv2 : tz;
-                // rare: a second crossing of the same axis inside the slice -> only the first
-                // crossing is committed here and the general loop takes the rest from m1
+                const double thi = (j == j1) ? amax : tpl;
+                const float dh = (float)(thi - t);
+                const float dx = (float)(tx - t);
+                const float dz = (float)(tz - t);
+                const bool cx = dx < dh, cz = dz < dh;
+                const float ex = cx ? dx : dh, ez = cz ? dz : dh;
+                const bool xfirst = ex <= ez;
+                const float m1 = fmaxf(fminf(ex, ez), 0.f), m2 = fmaxf(fmaxf(ex, ez), 0.f);
+                const int ddx = cx ? sx : 0, ddz = cz ? sz : 0, dox = cx ? sx : 0, doz = cz ? pstep : 0;
+                const int rx2 = rx + ddx, rz2 = rz + ddz;
+                const int rx1 = xfirst ? rx2 : rx, rz1 = xfirst ? rz : rz2;
+                const unsigned o1 = o + (unsigned)(xfirst ? dox : doz);
+                const unsigned o2 = o + (unsigned)(dox + doz);
+                const bool in0 = (unsigned)rx < (unsigned)bdx && (unsigned)rz < (unsigned)bdz;
+                const bool in1 = (unsigned)rx1 < (unsigned)bdx && (unsigned)rz1 < (unsigned)bdz;
+                const bool in2 = (unsigned)rx2 < (unsigned)bdx && (unsigned)rz2 < (unsigned)bdz;
+                const double ntx = tx + dtx, ntz = tz + dtz;
+                // rare: a second crossing of one axis inside the slice -> commit only the first
+                // crossing and let the general loop finish the slice
                 const bool more = (cx && ntx < thi) || (cz && ntz < thi);
-                if (!more) {
-                    ix = ix2; iz = iz2; tx = ntx; tz = ntz;
-                } else if (xfirst) {
-                    ix = ix1; tx = ntx;       // xfirst && more implies cx
-                } else {
-                    iz = iz1; tz = ntz;
-                }
-                const float l0 = (float)((m1 - t) * blen);
-                const float l1 = more ? 0.f : (float)((m2 - m1) * blen);
-                const float l2 = more ? 0.f : (float)((thi - m2) * blen);
+                const float l0 = m1 * blen_f;
+                const float l1 = more ? 0.f : (m2 - m1) * blen_f;
+                const float l2 = more ? 0.f : (dh - m2) * blen_f;
                 const bool v0 = in0 && l0 > 0.f, v1 = in1 && l1 > 0.f, v2 = in2 && l2 > 0.f;
                 if (MODE == PROJ_FP) {
-                    const float x0 = v0 ? __ldg(src + o0) : 0.f;
+                    const float x0 = v0 ? __ldg(src + o) : 0.f;
                     const float x1 = v1 ? __ldg(src + o1) : 0.f;
                     const float x2 = v2 ? __ldg(src + o2) : 0.f;
                     acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
                 }
                 if (MODE == PROJ_BP) {
-                    if (v0) atomicAdd(dst + o0, l0 * rs);
+                    if (v0) atomicAdd(dst + o, l0 * rs);
                     if (v1) atomicAdd(dst + o1, l1 * rs);
                     if (v2) atomicAdd(dst + o2, l2 * rs);
                 }
                 nvis += (unsigned)v0 + (unsigned)v1 + (unsigned)v2;
-                if (more) {   // general loop for the rest of the slice, from m1 at (ix, iz)
-                    double tt = m1;
-                    for (;;) {
+                if (!more) {
+                    rx = rx2; rz = rz2; o = o2;
+                    if (cx) tx = ntx;
+                    if (cz) tz = ntz;
+                } else {
+                    double tt;
+                    if (xfirst) { tt = fmax(t, tx); rx = rx2; o += (unsigned)sx; tx = ntx; }
+                    else { tt = fmax(t, tz); rz = rz2; o += (unsigned)pstep; tz = ntz; }
+                    for (;;) {      // general loop for the rest of the slice
                         const double tn = fmin(fmin(tx, tz), thi);
                         if (tn > tt) {
-                            if ((unsigned)(ix - ox) < (unsigned)bdx && (unsigned)(iz - oz) < (unsigned)bdz) {
-                                const unsigned o = (unsigned)(iz - oz) * plane + row + (unsigned)(ix - ox);
+                            if ((unsigned)rx < (unsigned)bdx && (unsigned)rz < (unsigned)bdz) {
                                 const float len = (float)((tn - tt) * blen);
                                 if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
                                 if (MODE == PROJ_BP) atomicAdd(dst + o, len * rs);
@@ -352,24 +357,20 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
                             tt = tn;
                         }
                         if (tx <= tz) {
-                            if (tx < thi) {
-                                ix += sx;
-                                tx = ((double)(ix + (sx > 0)) - a0) * inv0;
-                                continue;
-                            }
+                            if (tx < thi) { rx += sx; o += (unsigned)sx; tx += dtx; continue; }
                         } else if (tz < thi) {
-                            iz += sz;
-                            tz = ((double)(iz + (sz > 0)) - a2) * inv2;
-                            continue;
+                            rz += sz; o += (unsigned)pstep; tz += dtz; continue;
                         }
                         break;
                     }
                 }
                 t = thi;
-                if (MODE == PROJ_FP && (k & 15) == 15) {
-                    acc += (double)acc32;
-                    acc32 = 0.f;
-                }
+                tpl += dty;
+                o += (unsigned)rowstep;
+            }
+            if (MODE == PROJ_FP && (k & 15) == 15) {   // warp-uniform
+                acc += (double)acc32;
+                acc32 = 0.f;
             }
         }
     }
