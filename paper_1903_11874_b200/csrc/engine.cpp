@@ -81,7 +81,9 @@ struct bsgd_ctx_s {
     double* d_log = nullptr;           // per-epoch [obj, rmse] scratch
     long long d_log_cap = 0;
     unsigned long long* d_visits = nullptr;
-    unsigned long long* d_vislog = nullptr;
+    unsigned long long* count_target = nullptr;   // per (block, slot) counters of a COUNT launch
+    std::vector<unsigned long long> vtab;          // visits [owned block][view][tile]
+    bool vtab_ready = false;
     // launch tables
     char* d_tab = nullptr;
     size_t tab_bytes = 0;
@@ -275,7 +277,7 @@ struct bsgd_ctx_s {
         L.rproj = rproj;
         L.scale = scale;
         L.accumulate = accumulate;
-        L.visits = (mode == PROJ_FP) ? d_visits : nullptr;
+        L.visits = (mode == PROJ_COUNT) ? count_target : nullptr;
         if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
         BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_off, staging.data() + tab_off, off - tab_off,
                                   cudaMemcpyHostToDevice, st));
@@ -462,6 +464,34 @@ struct bsgd_ctx_s {
         have_prev_eud = false;
         have_theta_prev = false;
         rnorm_hist.clear();
+    }
+
+    // Exact ray-voxel intersection counts (positive-length Siddon segments) per
+    // (owned block, view, detector tile), from one COUNT traversal of every view; the
+    // FP/BP hot loops do not count.  Used for the visits/s metric.
+    void ensure_visit_table(cudaStream_t st) {
+        if (vtab_ready) return;
+        std::vector<int> all(n_views), slots(s);
+        for (int v = 0; v < n_views; ++v) all[v] = v;
+        for (int b = 0; b < s; ++b) slots[b] = b;
+        unsigned long long* dc = dnew<unsigned long long>((long long)s * n_views);
+        vtab.assign((size_t)s * n_views * T, 0ull);
+        std::vector<unsigned long long> h((size_t)s * n_views);
+        for (int t = 0; t < T; ++t) {
+            const int tu = t % tiles_u, tv = t / tiles_u;
+            const int4 r = make_int4((int)((long long)tu * nu / tiles_u), (int)((long long)(tu + 1) * nu / tiles_u),
+                                     (int)((long long)tv * nv / tiles_v), (int)((long long)(tv + 1) * nv / tiles_v));
+            std::vector<int4> rc((size_t)s * n_views, r);
+            BSGD_CUDA(cudaMemsetAsync(dc, 0, sizeof(unsigned long long) * s * n_views, st));
+            count_target = dc;
+            project(PROJ_COUNT, all, slots, rc, {}, {}, {}, {}, {}, nullptr, 0.f, 0, st, 0);
+            count_target = nullptr;
+            BSGD_CUDA(cudaMemcpyAsync(h.data(), dc, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+            BSGD_CUDA(cudaStreamSynchronize(st));
+            for (int b = 0; b < s; ++b)
+                for (int v = 0; v < n_views; ++v) vtab[((size_t)b * n_views + v) * T + t] = h[(size_t)b * n_views + v];
+        }
+        vtab_ready = true;
     }
 
     void ensure_im_table(cudaStream_t st) {
@@ -980,9 +1010,11 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         const int E = P->epochs;
         if (c->d_log_cap < 2LL * E + 2) {
             c->d_log = c->dnew<double>(2LL * E + 2);
-            c->d_vislog = c->dnew<unsigned long long>(E + 1);
             c->d_log_cap = 2LL * E + 2;
         }
+        const bool want_visits = log && log->visits;
+        if (want_visits) c->ensure_visit_table(st);
+        std::vector<unsigned long long> vis_log(E, 0ull);
         BSGD_CUDA(cudaMemsetAsync(c->d_log, 0, sizeof(double) * (2 * E + 2), st));
         std::vector<cudaEvent_t> ev;
         const bool timing = (P->flags & BSGD_TIMING) && log && log->t_ms;
@@ -1020,9 +1052,26 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 }
             }
             cudaEvent_t* evp = timing ? &ev[(size_t)e * 7] : nullptr;
-            BSGD_CUDA(cudaMemcpyAsync(c->d_vislog + e, c->d_visits, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
             c->epoch_step(y, x, rows, sgd ? std::vector<int>() : cols, tiles, (float)c->mu, sgd, st, evp, false);
-            BSGD_CUDA(cudaMemcpyAsync(c->d_vislog + e + 1, c->d_visits, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            if (want_visits) {   // FP visits of this epoch on this rank (BP visits are the same segments)
+                unsigned long long nvt = 0;
+                int V = 0;
+                for (int i : rows) V += (int)c->rows[i].size();
+                const int ncol = sgd ? c->N : gN;
+                for (int cs = 0; cs < ncol; ++cs) {
+                    const int j = sgd ? cs : cols[cs];
+                    if (!c->owned(j)) continue;
+                    int vs = 0;
+                    for (int i : rows)
+                        for (int v : c->rows[i]) {
+                            const unsigned long long* q = &c->vtab[((size_t)(j - c->first) * c->n_views + v) * c->T];
+                            if (!tiles.empty()) nvt += q[tiles[(size_t)cs * V + vs]];
+                            else for (int t = 0; t < c->T; ++t) nvt += q[t];
+                            ++vs;
+                        }
+                }
+                vis_log[e] = nvt;
+            }
             mu_log[e] = c->mu;
             launch_obj(c->d_normsq, c->M, c->d_log + 2 * e, st);
             if (amu) launch_axpy_eud(c->eud_cur, c->g, sb, st);            // Algo 3 line 2
@@ -1080,9 +1129,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         }
         if (x_host) BSGD_CUDA(cudaMemcpyAsync(x_in, x, sizeof(float) * sb, cudaMemcpyDeviceToHost, st));
         std::vector<double> hl(2 * (size_t)E + 2);
-        std::vector<unsigned long long> hv(E + 1);
         BSGD_CUDA(cudaMemcpyAsync(hl.data(), c->d_log, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, st));
-        BSGD_CUDA(cudaMemcpyAsync(hv.data(), c->d_vislog, sizeof(unsigned long long) * hv.size(), cudaMemcpyDeviceToHost, st));
         BSGD_CUDA(cudaStreamSynchronize(st));
         if (log) {
             const double nvox = (double)c->bsize * c->N;
@@ -1090,7 +1137,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 if (log->obj) log->obj[e] = hl[2 * e];
                 if (log->rmse) log->rmse[e] = xt ? sqrt(hl[2 * e + 1] / nvox) : NAN;
                 if (log->mu) log->mu[e] = mu_log[e];
-                if (log->visits) log->visits[e] = hv[e + 1] - hv[e];
+                if (log->visits) log->visits[e] = vis_log[e];
                 if (timing) {
                     cudaEvent_t* q = &ev[(size_t)e * 7];
                     float t[6];

@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256) k_project(const ProjLaunch L) {
 // segments, their loads issued together), a rare general loop for further crossings,
 // 32-bit voxel offsets and fp32 slice sums flushed into an fp64 accumulator.
 template <int MODE>
-__global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
+__global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     // band-major CTA order: blockIdx.x = (band * n_slots + slot) * n_chunks + chunk, so the
     // CTAs resident at any time cover the same detector-row band of consecutive views
     // (rays of one band cross the same z-range of the volume -> L2 reuse across views).
@@ -258,10 +258,12 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
 
     const int sx = sgn(b[0]), sy = sgn(b[1]), sz = sgn(b[2]);
     const double INF = __longlong_as_double(0x7ff0000000000000ll);
-    // lane state: voxel (rx, rz) relative to the block origin, its offset o, the current t,
-    // the t of the next x / z plane crossing (tx, tz) and of the current slice's exit plane
+    // Lane state: voxel (rx, rz) relative to the block origin and its offset o, the current
+    // t, the t of the next x / z plane crossing (tx, tz) and of the current slice's exit plane
     // (tpl).  Plane crossings advance by exact-enough fp64 increments (|1/b|: ~1e-13 drift
-    // over a whole ray); every in-slice decision runs in fp32 on t-differences.
+    // over a whole ray); every in-slice decision runs in fp32 on t-differences.  A crossing
+    // that would leave the box is never armed (its t is +inf: the ray exits there), so the
+    // voxel indices stay in range by construction and the hot loop has no bounds checks.
     int j0 = 0, j1 = -1, rx = 0, rz = 0;
     double t = 0.0, tx = INF, tz = INF, tpl = INF;
     unsigned o = 0;
@@ -272,12 +274,12 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
         if (sy == 0) j1 = j0;
         const int ix = cell_enter(a[0] + amin * b[0], sx, lo[0], hi[0]);
         const int iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
-        if (sx) tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
-        if (sz) tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
-        if (sy) tpl = ((double)(j0 + (sy > 0)) - a[1]) * inv[1];
-        t = amin;
         rx = ix - lo[0];
         rz = iz - lo[2];
+        if (sx && (unsigned)(rx + sx) < (unsigned)bdx) tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
+        if (sz && (unsigned)(rz + sz) < (unsigned)bdz) tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
+        if (sy) tpl = ((double)(j0 + (sy > 0)) - a[1]) * inv[1];
+        t = amin;
         o = (unsigned)rz * plane + (unsigned)(j0 - lo[1]) * (unsigned)bdx + (unsigned)rx;
     }
     const int pstep = sz * (int)plane;
@@ -309,34 +311,30 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
                 const float ex = cx ? dx : dh, ez = cz ? dz : dh;
                 const bool xfirst = ex <= ez;
                 const float m1 = fmaxf(fminf(ex, ez), 0.f), m2 = fmaxf(fmaxf(ex, ez), 0.f);
-                const int ddx = cx ? sx : 0, ddz = cz ? sz : 0, dox = cx ? sx : 0, doz = cz ? pstep : 0;
-                const int rx2 = rx + ddx, rz2 = rz + ddz;
-                const int rx1 = xfirst ? rx2 : rx, rz1 = xfirst ? rz : rz2;
+                const int dox = cx ? sx : 0, doz = cz ? pstep : 0;
                 const unsigned o1 = o + (unsigned)(xfirst ? dox : doz);
                 const unsigned o2 = o + (unsigned)(dox + doz);
-                const bool in0 = (unsigned)rx < (unsigned)bdx && (unsigned)rz < (unsigned)bdz;
-                const bool in1 = (unsigned)rx1 < (unsigned)bdx && (unsigned)rz1 < (unsigned)bdz;
-                const bool in2 = (unsigned)rx2 < (unsigned)bdx && (unsigned)rz2 < (unsigned)bdz;
-                const double ntx = tx + dtx, ntz = tz + dtz;
+                const int rx2 = rx + (cx ? sx : 0), rz2 = rz + (cz ? sz : 0);
+                const double ntx = ((unsigned)(rx2 + sx) < (unsigned)bdx) ? tx + dtx : INF;
+                const double ntz = ((unsigned)(rz2 + sz) < (unsigned)bdz) ? tz + dtz : INF;
                 // rare: a second crossing of one axis inside the slice -> commit only the first
                 // crossing and let the general loop finish the slice
                 const bool more = (cx && ntx < thi) || (cz && ntz < thi);
                 const float l0 = m1 * blen_f;
                 const float l1 = more ? 0.f : (m2 - m1) * blen_f;
                 const float l2 = more ? 0.f : (dh - m2) * blen_f;
-                const bool v0 = in0 && l0 > 0.f, v1 = in1 && l1 > 0.f, v2 = in2 && l2 > 0.f;
                 if (MODE == PROJ_FP) {
-                    const float x0 = v0 ? __ldg(src + o) : 0.f;
-                    const float x1 = v1 ? __ldg(src + o1) : 0.f;
-                    const float x2 = v2 ? __ldg(src + o2) : 0.f;
+                    const float x0 = __ldg(src + o);
+                    const float x1 = (!more && (cx || cz)) ? __ldg(src + o1) : 0.f;
+                    const float x2 = (!more && cx && cz) ? __ldg(src + o2) : 0.f;
                     acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
                 }
                 if (MODE == PROJ_BP) {
-                    if (v0) atomicAdd(dst + o, l0 * rs);
-                    if (v1) atomicAdd(dst + o1, l1 * rs);
-                    if (v2) atomicAdd(dst + o2, l2 * rs);
+                    if (l0 > 0.f) atomicAdd(dst + o, l0 * rs);
+                    if (l1 > 0.f) atomicAdd(dst + o1, l1 * rs);
+                    if (l2 > 0.f) atomicAdd(dst + o2, l2 * rs);
                 }
-                nvis += (unsigned)v0 + (unsigned)v1 + (unsigned)v2;
+                if (MODE == PROJ_COUNT) nvis += (unsigned)(l0 > 0.f) + (unsigned)(l1 > 0.f) + (unsigned)(l2 > 0.f);
                 if (!more) {
                     rx = rx2; rz = rz2; o = o2;
                     if (cx) tx = ntx;
@@ -348,18 +346,22 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
                     for (;;) {      // general loop for the rest of the slice
                         const double tn = fmin(fmin(tx, tz), thi);
                         if (tn > tt) {
-                            if ((unsigned)rx < (unsigned)bdx && (unsigned)rz < (unsigned)bdz) {
-                                const float len = (float)((tn - tt) * blen);
-                                if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
-                                if (MODE == PROJ_BP) atomicAdd(dst + o, len * rs);
-                                ++nvis;
-                            }
+                            const float len = (float)((tn - tt) * blen);
+                            if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
+                            if (MODE == PROJ_BP) atomicAdd(dst + o, len * rs);
+                            if (MODE == PROJ_COUNT) ++nvis;
                             tt = tn;
                         }
                         if (tx <= tz) {
-                            if (tx < thi) { rx += sx; o += (unsigned)sx; tx += dtx; continue; }
+                            if (tx < thi) {
+                                rx += sx; o += (unsigned)sx;
+                                tx = ((unsigned)(rx + sx) < (unsigned)bdx) ? tx + dtx : INF;
+                                continue;
+                            }
                         } else if (tz < thi) {
-                            rz += sz; o += (unsigned)pstep; tz += dtz; continue;
+                            rz += sz; o += (unsigned)pstep;
+                            tz = ((unsigned)(rz + sz) < (unsigned)bdz) ? tz + dtz : INF;
+                            continue;
                         }
                         break;
                     }
@@ -379,9 +381,9 @@ __global__ void __launch_bounds__(256, 3) k_project2(const ProjLaunch L) {
         float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
         *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
     }
-    if (L.visits) {
+    if (MODE == PROJ_COUNT && L.visits) {   // per (block, slot) counters
         unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
-        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits, (unsigned long long)s);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits + (size_t)blockIdx.z * L.n_slots + slot, (unsigned long long)s);
     }
 }
 
