@@ -74,7 +74,9 @@ struct bsgd_ctx_s {
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
           *tv_b = nullptr;
-    float *fp_scratchT = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr;
+    float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
+          *pw_vN = nullptr;
+    float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
     float *y_dev = nullptr, *x_dev = nullptr, *xt_dev = nullptr;
     double* d_normsq = nullptr;
     double* d_red = nullptr;           // 8 doubles scratch
@@ -125,6 +127,14 @@ struct bsgd_ctx_s {
         T* p = (T*)dalloc(sizeof(T) * (size_t)count);
         if (zero) BSGD_CUDA(cudaMemset(p, 0, sizeof(T) * (size_t)count));
         return p;
+    }
+    // Image buffers the projector reads or scatters into carry `slack` zeroed floats on both
+    // sides: a ray leaving the box can take one rounding-induced step past a face with a
+    // ~1e-9-voxel segment; the kernel does not test for it, the slack keeps it in memory.
+    long long slack = 0;
+    float* dnew_slack(long long count) {
+        float* p = dnew<float>(count + 2 * slack);
+        return p + slack;
     }
     void release() {
         for (auto& b : bufs) {
@@ -288,7 +298,7 @@ struct bsgd_ctx_s {
 
     void update(int mode, int b, float* x, float mu_, int final_, float* out, int accumulate,
                 cudaStream_t st, float* accN_ = nullptr, float* accT_ = nullptr, float* xT_ = nullptr,
-                int ghat_i = 0) {
+                int ghat_i = 0, float* xN_ = nullptr) {
         UpdLaunch U;
         U.bd[0] = bd[0]; U.bd[1] = bd[1]; U.bd[2] = bd[2];
         U.accN = accN_ ? accN_ : accN + b * bsize;
@@ -297,6 +307,7 @@ struct bsgd_ctx_s {
         U.g = g + b * bsize;
         U.x = x;
         U.xT = xT_ ? xT_ : xT + b * bsize;
+        U.xN = xN_ ? xN_ : (xT_ ? nullptr : xN + b * bsize);
         U.out = out;
         U.mu = mu_;
         U.final_ = final_;
@@ -355,7 +366,7 @@ struct bsgd_ctx_s {
             std::vector<float*> zs;
             for (int b = 0; b < nb; ++b) {
                 for (int vs = 0; vs < V; ++vs) rc[(size_t)b * V + vs] = rect_for(b, vs);
-                xs.push_back(x_owned + oslots[b] * bsize);
+                xs.push_back(xN + oslots[b] * bsize);
                 xts.push_back(xT + oslots[b] * bsize);
                 zs.push_back(z + oslots[b] * n_rays);
             }
@@ -785,13 +796,15 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         const long long sb = (long long)c->s * c->bsize;
         c->d_vecs = c->dnew<double>(12LL * c->n_views, false);
         BSGD_CUDA(cudaMemcpy(c->d_vecs, c->vecs.data(), sizeof(double) * c->vecs.size(), cudaMemcpyHostToDevice));
-        c->xT = c->dnew<float>(sb);
+        c->slack = (((long long)c->bd[0] * c->bd[1] + 64 + 63) / 64) * 64;
+        c->xT = c->dnew_slack(sb);
+        c->xN = c->dnew_slack(sb);
         c->g = c->dnew<float>(sb);
         c->ghat = c->dnew<float>((long long)c->M * sb);
         c->z = c->dnew<float>((long long)c->s * c->n_rays);
         c->r = c->dnew<float>(c->n_rays);
-        c->accN = c->dnew<float>(sb);
-        c->accT = c->dnew<float>(sb);
+        c->accN = c->dnew_slack(sb);
+        c->accT = c->dnew_slack(sb);
         c->pc = c->world > 1 ? c->dnew<float>(c->n_rays) : nullptr;
         c->d_normsq = c->dnew<double>(c->M);
         c->d_red = c->dnew<double>(16);
@@ -850,11 +863,14 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
         check_views(c, n, views, rects);
         if (!c->owned(col_block)) fail(BSGD_E_DIMENSION, "column block not owned by this rank");
         if (n == 0) return;
-        if (!c->fp_scratchT) c->fp_scratchT = c->dnew<float>(c->bsize, false);
+        if (!c->fp_scratchT) {
+            c->fp_scratchT = c->dnew_slack(c->bsize);
+            c->fp_scratchN = c->dnew_slack(c->bsize);
+        }
         const int b = col_block - c->first;
         cudaStream_t st = S(stream);
         c->update(UPD_XT, b, const_cast<float*>(x_block), 0.f, 1, nullptr, 0, st, nullptr, nullptr,
-                  c->fp_scratchT);
+                  c->fp_scratchT, 0, c->fp_scratchN);
         std::vector<int> vv(views, views + n);
         std::vector<int4> rc;
         if (rects)
@@ -871,8 +887,8 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
                                       off - c->tab_bytes / 2, cudaMemcpyHostToDevice, st));
             launch_zero_rects(proj, dv, dr, n, c->nu, c->nv, st);
         }
-        c->project(PROJ_FP, vv, {b}, rc, {x_block}, {c->fp_scratchT}, {}, {}, {proj}, nullptr, 0.f, accumulate,
-                   st, 0);
+        c->project(PROJ_FP, vv, {b}, rc, {c->fp_scratchN}, {c->fp_scratchT}, {}, {}, {proj}, nullptr, 0.f,
+                   accumulate, st, 0);
     });
 }
 
@@ -1199,7 +1215,8 @@ bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, doubl
         const long long sb = (long long)c->s * c->bsize;
         if (!c->pw_v) {
             c->pw_v = c->dnew<float>(sb, false);
-            c->pw_vT = c->dnew<float>(sb, false);
+            c->pw_vT = c->dnew_slack(sb);
+            c->pw_vN = c->dnew_slack(sb);
             c->pw_proj = c->dnew<float>(c->n_rays, false);
         }
         launch_fill_random(c->pw_v, sb, seed + 1000003ull * (uint64_t)c->rank, st);
@@ -1214,8 +1231,8 @@ bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, doubl
             BSGD_CUDA(cudaMemsetAsync(c->pw_proj, 0, sizeof(float) * c->n_rays, st));
             for (int b = 0; b < c->s; ++b) {
                 c->update(UPD_XT, b, c->pw_v + b * c->bsize, 0.f, 1, nullptr, 0, st, nullptr, nullptr,
-                          c->pw_vT + b * c->bsize);
-                c->project(PROJ_FP, all, {b}, {}, {c->pw_v + b * c->bsize}, {c->pw_vT + b * c->bsize}, {}, {},
+                          c->pw_vT + b * c->bsize, 0, c->pw_vN + b * c->bsize);
+                c->project(PROJ_FP, all, {b}, {}, {c->pw_vN + b * c->bsize}, {c->pw_vT + b * c->bsize}, {}, {},
                            {c->pw_proj}, nullptr, 0.f, 1, st, 0);
             }
             c->allreduce_f(c->pw_proj, c->n_rays, st);

@@ -84,6 +84,7 @@ struct UpdLaunch {
     float* g;             // g_J
     float* x;             // x_J (normal layout)
     float* xT;            // x_J transposed (written when x changes / UPD_XT)
+    float* xN;            // x_J copy in the library's slack-padded buffer (FP source)
     float* out;           // UPD_OUT target
     float mu;
     int final_;           // apply x += mu g and refresh xT

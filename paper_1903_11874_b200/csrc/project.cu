@@ -11,8 +11,9 @@
 //    main axis in LOCKSTEP, so at every step the 32 lanes touch 32 neighbouring
 //    voxels of one image row -> coalesced 128-byte gathers (FP) and coalesced
 //    reductions (BP).  Inside a slice the exact Siddon segments are produced by
-//    the crossings of the other two axes (fp64 t-parameters recomputed from the
-//    integer plane index, never accumulated).
+//    the crossings of the other two axes: the t of the next plane crossing of each
+//    axis is kept in fp64 and advanced by |1/b| (drift ~1e-13 over a whole ray),
+//    every in-slice decision runs in fp32 on t-differences (lengths ~1e-7 relative).
 //  * views whose central ray is x-major use a transposed copy of the block
 //    ([z][x][y]) with x<->y swapped in the ray, so the lockstep axis is always
 //    the slow in-plane axis of the layout that is read.
@@ -261,12 +262,13 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     // Lane state: voxel (rx, rz) relative to the block origin and its offset o, the current
     // t, the t of the next x / z plane crossing (tx, tz) and of the current slice's exit plane
     // (tpl).  Plane crossings advance by exact-enough fp64 increments (|1/b|: ~1e-13 drift
-    // over a whole ray); every in-slice decision runs in fp32 on t-differences.  A crossing
-    // that would leave the box is never armed (its t is +inf: the ray exits there), so the
-    // voxel indices stay in range by construction and the hot loop has no bounds checks.
+    // over a whole ray); every in-slice decision runs in fp32 on t-differences.  There are no
+    // bounds checks: the only possible out-of-box step is a rounding-induced crossing of the
+    // exit face with a ~1e-9-voxel segment, which lands in the zeroed slack the library puts
+    // around every image buffer the projector touches (or in a neighbouring voxel).
     int j0 = 0, j1 = -1, rx = 0, rz = 0;
     double t = 0.0, tx = INF, tz = INF, tpl = INF;
-    unsigned o = 0;
+    int o = 0;   // signed: an out-of-box step may point one element before the block
     const double dtx = fabs(inv[0]), dtz = fabs(inv[2]), dty = fabs(inv[1]);
     if (hit) {
         j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
@@ -276,11 +278,11 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
         const int iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
         rx = ix - lo[0];
         rz = iz - lo[2];
-        if (sx && (unsigned)(rx + sx) < (unsigned)bdx) tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
-        if (sz && (unsigned)(rz + sz) < (unsigned)bdz) tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
+        if (sx) tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
+        if (sz) tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
         if (sy) tpl = ((double)(j0 + (sy > 0)) - a[1]) * inv[1];
         t = amin;
-        o = (unsigned)rz * plane + (unsigned)(j0 - lo[1]) * (unsigned)bdx + (unsigned)rx;
+        o = rz * (int)plane + (j0 - lo[1]) * bdx + rx;
     }
     const int pstep = sz * (int)plane;
     const int rowstep = sy * bdx;
@@ -303,7 +305,8 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
             const int j = jstart + dir * k;
             const bool in = mine && (dir > 0 ? (j >= j0 && j <= j1) : (j <= j0 && j >= j1));
             if (in) {
-                const double thi = (j == j1) ? amax : tpl;
+                // (j1 can land one slice late by rounding: never walk past amax)
+                const double thi = tpl < amax ? tpl : amax;
                 const float dh = (float)(thi - t);
                 const float dx = (float)(tx - t);
                 const float dz = (float)(tz - t);
@@ -312,11 +315,9 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 const bool xfirst = ex <= ez;
                 const float m1 = fmaxf(fminf(ex, ez), 0.f), m2 = fmaxf(fmaxf(ex, ez), 0.f);
                 const int dox = cx ? sx : 0, doz = cz ? pstep : 0;
-                const unsigned o1 = o + (unsigned)(xfirst ? dox : doz);
-                const unsigned o2 = o + (unsigned)(dox + doz);
-                const int rx2 = rx + (cx ? sx : 0), rz2 = rz + (cz ? sz : 0);
-                const double ntx = ((unsigned)(rx2 + sx) < (unsigned)bdx) ? tx + dtx : INF;
-                const double ntz = ((unsigned)(rz2 + sz) < (unsigned)bdz) ? tz + dtz : INF;
+                const int o1 = o + (xfirst ? dox : doz);
+                const int o2 = o + dox + doz;
+                const double ntx = tx + dtx, ntz = tz + dtz;
                 // rare: a second crossing of one axis inside the slice -> commit only the first
                 // crossing and let the general loop finish the slice
                 const bool more = (cx && ntx < thi) || (cz && ntz < thi);
@@ -336,13 +337,13 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 }
                 if (MODE == PROJ_COUNT) nvis += (unsigned)(l0 > 0.f) + (unsigned)(l1 > 0.f) + (unsigned)(l2 > 0.f);
                 if (!more) {
-                    rx = rx2; rz = rz2; o = o2;
+                    o = o2;
                     if (cx) tx = ntx;
                     if (cz) tz = ntz;
                 } else {
                     double tt;
-                    if (xfirst) { tt = fmax(t, tx); rx = rx2; o += (unsigned)sx; tx = ntx; }
-                    else { tt = fmax(t, tz); rz = rz2; o += (unsigned)pstep; tz = ntz; }
+                    if (xfirst) { tt = fmax(t, tx); o += sx; tx = ntx; }
+                    else { tt = fmax(t, tz); o += pstep; tz = ntz; }
                     for (;;) {      // general loop for the rest of the slice
                         const double tn = fmin(fmin(tx, tz), thi);
                         if (tn > tt) {
@@ -354,13 +355,13 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                         }
                         if (tx <= tz) {
                             if (tx < thi) {
-                                rx += sx; o += (unsigned)sx;
-                                tx = ((unsigned)(rx + sx) < (unsigned)bdx) ? tx + dtx : INF;
+                                o += sx;
+                                tx += dtx;
                                 continue;
                             }
                         } else if (tz < thi) {
-                            rz += sz; o += (unsigned)pstep;
-                            tz = ((unsigned)(rz + sz) < (unsigned)bdz) ? tz + dtz : INF;
+                            o += pstep;
+                            tz += dtz;
                             continue;
                         }
                         break;
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 }
                 t = thi;
                 tpl += dty;
-                o += (unsigned)rowstep;
+                o += rowstep;
             }
             if (MODE == PROJ_FP && (k & 15) == 15) {   // warp-uniform
                 acc += (double)acc32;

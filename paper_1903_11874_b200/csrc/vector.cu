@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(256) k_block_update4(const UpdLaunch U) {
         *reinterpret_cast<float4*>(U.out + in_) = make_float4(ng[0], ng[1], ng[2], ng[3]);
     }
     if (!writes_x) return;
+    if (U.xN) *reinterpret_cast<float4*>(U.xN + in_) = make_float4(nx[0], nx[1], nx[2], nx[3]);
     __syncthreads();
     *reinterpret_cast<float4*>(U.xT + it_) =
         make_float4(tX[r][4 * q + 0], tX[r][4 * q + 1], tX[r][4 * q + 2], tX[r][4 * q + 3]);
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U) {
             } else if (MODE == UPD_XT) {
                 xv = vx[k];
             }
+            if (writes_x && U.xN) U.xN[i] = xv;
         }
         tX[ty + 8 * k][tx] = xv;
     }

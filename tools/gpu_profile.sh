@@ -1,7 +1,8 @@
 #!/bin/bash
 # Run on the GPU box (via gpurun): launch list of this library's kernels + one full
-# ncu capture of the FP and BP launches of a cfg5 bench epoch.  Output: gpurun_out/.
-# The bench's data generation (torch) is not profiled: kernels are filtered by name.
+# ncu capture of the FP and BP launches of a timed cfg5 bench epoch.  Output: gpurun_out/.
+# k_project2 launch order in `bench.py --warmup 1 --steps 1`: 4 COUNT launches (visit
+# table, one per detector tile), warm-up FP, BP, timed FP, BP  ->  skip 6, capture 2.
 set -x
 TAG=${1:-r01}
 KSEL='regex:k_(project|residual|block_update|zero_rows|obj|axpy|dot3)'
@@ -10,8 +11,13 @@ mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k "$KSEL" \
   --log-file gpurun_out/launches_${TAG}.csv \
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/launches_${TAG}.log 2>&1
-# the projector kernels, once each (FP then BP of the timed epoch)
-timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:k_project -s 2 -c 2 -o gpurun_out/prof_${TAG} -f \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_${TAG}.log 2>&1
+# FP (full set) and BP (sections that replay reliably with the atomics)
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:k_project2 -s 6 -c 1 -o gpurun_out/prof_fp_${TAG} -f \
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_fp_${TAG}.log 2>&1
+timeout 900 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section ComputeWorkloadAnalysis \
+  --section WarpStateStats --section SchedulerStats --section Occupancy --section LaunchStats \
+  --metrics lts__t_sectors_op_red.sum,lts__t_requests_op_red.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \
+  --clock-control none -k regex:k_project2 -s 7 -c 1 -o gpurun_out/prof_bp_${TAG} -f \
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_bp_${TAG}.log 2>&1
 ls -la gpurun_out
