@@ -44,14 +44,16 @@ def load_peaks():
 
 
 def load_traffic():
-    """dram bytes per visit of the dominant kernels from the committed ncu capture."""
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
-            os.path.join(ROOT, "profiles")) else []:
-        if name.startswith("ncu_summary") and name.endswith(".json"):
-            try:
-                return json.load(open(os.path.join(ROOT, "profiles", name)))
-            except Exception:
-                pass
+    """DRAM bytes per visit of the FP / BP launches from the newest committed ncu
+    capture (profiles/traffic_<tag>.json, written by tools/traffic_from_ncu.py)."""
+    d = os.path.join(ROOT, "profiles")
+    names = sorted(n for n in os.listdir(d) if n.startswith("traffic_") and n.endswith(".json")) \
+        if os.path.isdir(d) else []
+    for name in reversed(names):
+        try:
+            return json.load(open(os.path.join(d, name)))
+        except Exception:
+            pass
     return {}
 
 
@@ -103,30 +105,41 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle (CPU) timing
+_ORACLE_CACHE = None
+
+
 def oracle_sample(target_s=12.0, max_views=8):
     """fp64 CPU oracle: FP + BP of whole views of the cfg5 workload through all 8
     z-slabs (the same per-view work as the GPU epoch), on all host cores.
     Returns (visits per second counting FP and BP separately, cores, sample text)."""
+    global _ORACLE_CACHE
     import synth
     from oracle.projector import BlockGrid, Projector
     p = synth.PRESETS["cfg5"]
     g = p.geometry()
-    P = Projector(g, BlockGrid(g.dims, p.blocks))
     cores = os.cpu_count() or 1
-    x = np.full(P.grid.bsize, 0.5)           # value-independent work (Siddon visits depend on geometry)
-    # visits of one view (a circular orbit makes every view's count the same up to
-    # a few corner segments); counted once, outside the timed loop
-    per_view_visits = sum(P.count([0], j) for j in range(p.N))
-    proj = np.zeros(g.n_rays)
+    if _ORACLE_CACHE is None:
+        # one single-view geometry per sampled view (same rays as in the full geometry;
+        # keeps the projection buffer at one view) and its visit count, counted once
+        # outside the timed loop (a circular orbit gives every view the same count up to
+        # a few corner segments)
+        views = [synth.Geometry(g.beam, g.vecs[v:v + 1].copy(), g.det_u, g.det_v, g.dims)
+                 for v in (0, 97, 194, 291, 388, 485, 582, 679)]
+        projs = [Projector(gv, BlockGrid(g.dims, p.blocks)) for gv in views]
+        per_view = sum(projs[0].count([0], j) for j in range(p.N))
+        _ORACLE_CACHE = (projs, per_view, np.full(projs[0].grid.bsize, 0.5))
+    projs, per_view_visits, x = _ORACLE_CACHE
+    proj = np.zeros(g.det_u * g.det_v)
     visits = 0
     views_done = 0
     t0 = time.perf_counter()
     while views_done < max_views:
-        v = [int(views_done * 97 % g.n_views)]
+        P = projs[views_done % len(projs)]
+        proj[:] = 0.0
         for j in range(p.N):
-            P.fp(v, j, x, proj=proj, accumulate=True)
+            P.fp([0], j, x, proj=proj, accumulate=True)
         for j in range(p.N):
-            P.bp(v, j, proj)
+            P.bp([0], j, proj)
         visits += 2 * per_view_visits
         views_done += 1
         if time.perf_counter() - t0 > target_s:
@@ -157,7 +170,7 @@ def run_reference(args, rank, world):
             per_step.append(dt)
             vps_all.append(vps)
     vps = float(np.median(vps_all))
-    ev = 2 * epoch_visits_estimate()
+    ev = 2 * 72 * _ORACLE_CACHE[1]      # FP + BP visits of one epoch: 72 views x (visits per view)
     value = vps / ev
     line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "epochs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per_step)),

@@ -58,6 +58,7 @@ struct bsgd_ctx_s {
     int N = 1, M = 1, kind = 0, tiles_u = 1, tiles_v = 1, T = 1;
     uint64_t row_seed = 0;
     int rank = 0, world = 1, first = 0, s = 1;
+    bool coll = false;     // collective code path (world > 1, or BSGD_FORCE_NCCL=1 with one rank)
     long long bsize = 0, n_rays = 0, per = 0;
     double R = 0.0;
     std::vector<std::vector<int>> rows;   // views of each row block (sorted)
@@ -166,6 +167,7 @@ struct bsgd_ctx_s {
     // bounding box of the projected corners + 1 pixel margin, u aligned to warps.
     // Falls back to the whole detector when a corner is not in front of the source.
     int band_rows = 4;
+    int pf_rows = 2;   // BSGD_PF_ROWS
     int4 footprint(const int lo[3], const int hi[3], int view) const {
         const int4 full = make_int4(0, nu, 0, nv);
         const double* q = &vecs[12 * (size_t)view];
@@ -284,6 +286,7 @@ struct bsgd_ctx_s {
         L.rows_per_band = R;
         L.n_chunks = (R * maxw + 255) / 256;
         L.n_bands = nbands;
+        L.pf_rows = std::min(pf_rows, std::max(1, bd[0] < bd[1] ? bd[0] : bd[1]) / 1);
         L.rproj = rproj;
         L.scale = scale;
         L.accumulate = accumulate;
@@ -320,10 +323,10 @@ struct bsgd_ctx_s {
     }
 
     void allreduce_f(float* p, size_t n, cudaStream_t st) {
-        if (world > 1) BSGD_NCCL(ncclAllReduce(p, p, n, ncclFloat, ncclSum, comm, st));
+        if (coll) BSGD_NCCL(ncclAllReduce(p, p, n, ncclFloat, ncclSum, comm, st));
     }
     void allreduce_d(double* p, size_t n, cudaStream_t st) {
-        if (world > 1) BSGD_NCCL(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, st));
+        if (coll) BSGD_NCCL(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, st));
     }
 
     // ------------------------------------------------------------ one epoch
@@ -394,7 +397,7 @@ struct bsgd_ctx_s {
             Rl.pc = pc;
             Rl.normsq = d_normsq;
             launch_zero_rows(d_normsq, drows, (int)sel_rows.size(), st);
-            if (world == 1) {
+            if (!coll) {
                 Rl.mode = 0;
                 launch_residual(Rl, st);
             } else {
@@ -780,6 +783,7 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         c->s = c->N / c->world;
         c->first = c->rank * c->s;
         if (const char* e = getenv("BSGD_BAND_ROWS")) c->band_rows = std::max(1, atoi(e));
+        if (const char* e = getenv("BSGD_PF_ROWS")) c->pf_rows = std::min(4, std::max(1, atoi(e)));
         if (c->bsize >= (1LL << 31)) fail(BSGD_E_PARTITION, "a column block must hold fewer than 2^31 voxels");
         // row blocks
         std::vector<int32_t> vv(c->n_views), off(c->M + 1);
@@ -805,7 +809,9 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         c->r = c->dnew<float>(c->n_rays);
         c->accN = c->dnew_slack(sb);
         c->accT = c->dnew_slack(sb);
-        c->pc = c->world > 1 ? c->dnew<float>(c->n_rays) : nullptr;
+        if (const char* e = getenv("BSGD_FORCE_NCCL")) c->coll = atoi(e) != 0;   // test hook
+        if (c->world > 1) c->coll = true;
+        c->pc = c->coll ? c->dnew<float>(c->n_rays) : nullptr;
         c->d_normsq = c->dnew<double>(c->M);
         c->d_red = c->dnew<double>(16);
         c->d_visits = c->dnew<unsigned long long>(1);
@@ -816,6 +822,10 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
             ncclUniqueId id;
             memcpy(&id, dist->nccl_id, sizeof id);
             BSGD_NCCL(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+        } else if (c->coll) {   // one-rank communicator: exercises the collective path on 1 GPU
+            ncclUniqueId id;
+            BSGD_NCCL(ncclGetUniqueId(&id));
+            BSGD_NCCL(ncclCommInitRank(&c->comm, 1, id, 0));
         }
         BSGD_CUDA(cudaDeviceSynchronize());
     });

@@ -41,6 +41,12 @@ __device__ __forceinline__ int cell_exit(double c, int dir, int lo, int hi) {
 
 __device__ __forceinline__ int sgn(double v) { return (v > 0.0) - (v < 0.0); }
 
+// Fire-and-forget fp32 reduction into GLOBAL memory (REDG.E.ADD.F32 at L2).  atomicAdd on
+// a generic pointer compiles to ATOM plus a shared-memory CAS-loop fallback branch.
+__device__ __forceinline__ void red_add(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 // Ray (view, iv, iu) in grid coordinates, exactly as the problem defines it.
 __device__ __forceinline__ void make_ray(const KGeom& g, const double* vec, int iu, int iv,
                                          double a[3], double b[3]) {
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(256) k_project(const ProjLaunch L) {
                             const long long addr = (long long)uz * plane + rowoff + ux;
                             const double len = (tn - t) * blen;
                             if (MODE == PROJ_FP) acc += len * (double)__ldg(src + addr);
-                            if (MODE == PROJ_BP) atomicAdd(dst + addr, (float)(len * (double)rs));
+                            if (MODE == PROJ_BP) red_add(dst + addr, (float)(len * (double)rs));
                             ++nvis;
                         }
                         t = tn;
@@ -286,6 +292,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     }
     const int pstep = sz * (int)plane;
     const int rowstep = sy * bdx;
+    const int pf_off = (L.pf_rows - 1) * rowstep;   // FP prefetch lead (rows beyond the next slice)
     const float blen_f = (float)blen;
     double acc = 0.0;
     float acc32 = 0.f;
@@ -321,21 +328,25 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 // rare: a second crossing of one axis inside the slice -> commit only the first
                 // crossing and let the general loop finish the slice
                 const bool more = (cx && ntx < thi) || (cz && ntz < thi);
+                // segment 1 exists iff some crossing falls in the slice, segment 2 iff both do
+                // (and no second crossing sends the rest to the general loop)
+                const bool p1 = !more && (cx || cz), p2 = !more && cx && cz;
                 const float l0 = m1 * blen_f;
-                const float l1 = more ? 0.f : (m2 - m1) * blen_f;
-                const float l2 = more ? 0.f : (dh - m2) * blen_f;
+                const float l1 = (m2 - m1) * blen_f;
+                const float l2 = (dh - m2) * blen_f;
                 if (MODE == PROJ_FP) {
                     const float x0 = __ldg(src + o);
-                    const float x1 = (!more && (cx || cz)) ? __ldg(src + o1) : 0.f;
-                    const float x2 = (!more && cx && cz) ? __ldg(src + o2) : 0.f;
+                    const float x1 = p1 ? __ldg(src + o1) : 0.f;
+                    const float x2 = p2 ? __ldg(src + o2) : 0.f;
                     acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
                 }
-                if (MODE == PROJ_BP) {
-                    if (l0 > 0.f) atomicAdd(dst + o, l0 * rs);
-                    if (l1 > 0.f) atomicAdd(dst + o1, l1 * rs);
-                    if (l2 > 0.f) atomicAdd(dst + o2, l2 * rs);
+                if (MODE == PROJ_BP) {   // zero-length segments (exact-boundary ties) add 0
+                    red_add(dst + o, l0 * rs);
+                    if (p1) red_add(dst + o1, l1 * rs);
+                    if (p2) red_add(dst + o2, l2 * rs);
                 }
-                if (MODE == PROJ_COUNT) nvis += (unsigned)(l0 > 0.f) + (unsigned)(l1 > 0.f) + (unsigned)(l2 > 0.f);
+                if (MODE == PROJ_COUNT)
+                    nvis += (unsigned)(l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
                 if (!more) {
                     o = o2;
                     if (cx) tx = ntx;
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                         if (tn > tt) {
                             const float len = (float)((tn - tt) * blen);
                             if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
-                            if (MODE == PROJ_BP) atomicAdd(dst + o, len * rs);
+                            if (MODE == PROJ_BP) red_add(dst + o, len * rs);
                             if (MODE == PROJ_COUNT) ++nvis;
                             tt = tn;
                         }
@@ -370,6 +381,9 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 t = thi;
                 tpl += dty;
                 o += rowstep;
+                // FP: pull the next slice's line into L1 now (no register cost); the
+                // gather there then hits L1 instead of waiting on L2/HBM
+                if (MODE == PROJ_FP) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + o + pf_off));
             }
             if (MODE == PROJ_FP && (k & 15) == 15) {   // warp-uniform
                 acc += (double)acc32;

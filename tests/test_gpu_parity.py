@@ -296,3 +296,29 @@ def test_full_size_engine_step_cfg5(bs):
                 tol = 1e-5 * ref[ids] + 1e-7
                 assert np.all(d <= tol), f"slab {j} view {v}: max |d|/tol {np.max(d / tol):.3g}"
     ctx.close()
+
+
+def test_collective_path_one_rank(bs, monkeypatch):
+    """The world > 1 code path (partial sums -> ncclAllReduce -> residual; fp64
+    allreduces of Algo 3 and RMSE) run through a one-rank NCCL communicator
+    (BSGD_FORCE_NCCL=1) reproduces the fused single-GPU path (to the run-to-run
+    spread of the order-nondeterministic BP reductions; mu decisions identical)."""
+    p, g, vol32, y = problem("cfg4", K=32, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 1.5 / ob.power_iteration(P, 20, seed=1)
+    xt = torch.from_numpy(P.grid.to_blocks(vol32).ravel().copy()).cuda()
+    out = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("BSGD_FORCE_NCCL", force)
+        ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=2, tiles=p.tiles)
+        yd = torch.from_numpy(y).cuda()
+        xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+        res = ctx.run(yd, xd, epochs=30, mu0=mu, seed=4, x_true=xt, rows_per_epoch=1, cols_per_epoch=3,
+                      flags=bs.AUTO_MU | bs.TV | bs.IS, lam=0.05)
+        out.append((xd.cpu().numpy(), res.obj.copy(), res.mu.copy(), res.rmse.copy()))
+        ctx.close()
+    x0, x1 = out[0][0], out[1][0]
+    assert np.max(np.abs(x0 - x1)) <= 1e-5 * np.max(np.abs(x0))
+    assert np.array_equal(out[0][2], out[1][2])                     # auto-mu decisions
+    for k in (1, 3):
+        assert np.allclose(out[0][k], out[1][k], rtol=1e-5, atol=0)
