@@ -46,6 +46,12 @@ __device__ __forceinline__ int sgn(double v) { return (v > 0.0) - (v < 0.0); }
 __device__ __forceinline__ void red_add(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+// Predicated variant: one @p RED instruction instead of a branch around it.
+__device__ __forceinline__ void red_add_if(bool pred, float* p, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.global.add.f32 [%0], %1;\n\t}" ::"l"(p),
+                 "f"(v), "r"((int)pred)
+                 : "memory");
+}
 
 // Ray (view, iv, iu) in grid coordinates, exactly as the problem defines it.
 __device__ __forceinline__ void make_ray(const KGeom& g, const double* vec, int iu, int iv,
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     const int pstep = sz * (int)plane;
     const int rowstep = sy * bdx;
     const int pf_off = (L.pf_rows - 1) * rowstep;   // FP prefetch lead (rows beyond the next slice)
-    const float blen_f = (float)blen;
+    const float wbp = (float)blen * rs;   // BP weight per unit t: |b| * scale * r_ray
     double acc = 0.0;
     float acc32 = 0.f;
     unsigned int nvis = 0;
@@ -331,9 +337,11 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 // segment 1 exists iff some crossing falls in the slice, segment 2 iff both do
                 // (and no second crossing sends the rest to the general loop)
                 const bool p1 = !more && (cx || cz), p2 = !more && cx && cz;
-                const float l0 = m1 * blen_f;
-                const float l1 = (m2 - m1) * blen_f;
-                const float l2 = (dh - m2) * blen_f;
+                // segment lengths in t units; FP scales the sum by |b| at each flush, BP
+                // folds |b| into the ray's weight w = |b| * scale * r
+                const float l0 = m1;
+                const float l1 = m2 - m1;
+                const float l2 = dh - m2;
                 if (MODE == PROJ_FP) {
                     const float x0 = __ldg(src + o);
                     const float x1 = p1 ? __ldg(src + o1) : 0.f;
@@ -341,9 +349,9 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                     acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
                 }
                 if (MODE == PROJ_BP) {   // zero-length segments (exact-boundary ties) add 0
-                    red_add(dst + o, l0 * rs);
-                    if (p1) red_add(dst + o1, l1 * rs);
-                    if (p2) red_add(dst + o2, l2 * rs);
+                    red_add(dst + o, l0 * wbp);
+                    red_add_if(p1, dst + o1, l1 * wbp);
+                    red_add_if(p2, dst + o2, l2 * wbp);
                 }
                 if (MODE == PROJ_COUNT)
                     nvis += (unsigned)(l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
@@ -358,9 +366,9 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                     for (;;) {      // general loop for the rest of the slice
                         const double tn = fmin(fmin(tx, tz), thi);
                         if (tn > tt) {
-                            const float len = (float)((tn - tt) * blen);
+                            const float len = (float)(tn - tt);   // t units (see above)
                             if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
-                            if (MODE == PROJ_BP) red_add(dst + o, len * rs);
+                            if (MODE == PROJ_BP) red_add(dst + o, len * wbp);
                             if (MODE == PROJ_COUNT) ++nvis;
                             tt = tn;
                         }
@@ -393,6 +401,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     }
     if (MODE == PROJ_FP && inrect) {
         acc += (double)acc32;
+        acc *= blen;                        // t units -> voxel lengths
         float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
         *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
     }
