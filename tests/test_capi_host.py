@@ -16,8 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def bs():
-    from paper_1903_11874_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__.build()       # compiles libbsgd.so if missing or stale
     import paper_1903_11874_b200 as m
     return m
 
