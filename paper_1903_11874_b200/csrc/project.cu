@@ -53,6 +53,13 @@ __device__ __forceinline__ void red_add_if(bool pred, float* p, float v) {
                  : "memory");
 }
 
+__device__ __forceinline__ bool lane_steep(const double b[3]) {
+    // K = |b_c / b_1| * 2^32 must round below 2^32 (a 32-bit increment without carry into
+    // the integer part); the tiny margin keeps the rounded increment < 2^32 - 1
+    const double lim = fabs(b[1]) * (1.0 - 1.0 / 1073741824.0);
+    return b[1] == 0.0 || !(fabs(b[0]) < lim) || !(fabs(b[2]) < lim);
+}
+
 // Ray (view, iv, iu) in grid coordinates, exactly as the problem defines it.
 __device__ __forceinline__ void make_ray(const KGeom& g, const double* vec, int iu, int iv,
                                          double a[3], double b[3]) {
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(256) k_project(const ProjLaunch L) {
 // common case (at most one x and one z plane crossing inside the slice: up to three
 // segments, their loads issued together), a rare general loop for further crossings,
 // 32-bit voxel offsets and fp32 slice sums flushed into an fp64 accumulator.
-template <int MODE>
+template <int MODE, bool STEEP_ONLY = false>
 __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     // band-major CTA order: blockIdx.x = (band * n_slots + slot) * n_chunks + chunk, so the
     // CTAs resident at any time cover the same detector-row band of consecutive views
@@ -261,6 +268,8 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
     double amin, amax;
     bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
+    // v3 companion mode: only the warps k_project3 leaves (a lane with a steep ray)
+    if (STEEP_ONLY && !__any_sync(0xffffffffu, hit && lane_steep(b))) return;
     float rs = 0.f;
     if (MODE == PROJ_BP) {
         if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
@@ -411,6 +420,198 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// v3 traversal: the same slice-lockstep Siddon, parametrised by the distance s travelled
+// along the main axis instead of by the ray parameter t.  Inside the block the ray is the
+// line x(s) = x_p + kx s, z(s) = z_p + kz s (|kx|, |kz| < 1 for "non-steep" rays), so the
+// in-plane coordinates at consecutive slice planes form arithmetic sequences.  They are kept
+// as 32-bit fixed-point FRACTIONS (2^-32 voxel) of mirrored coordinates (mirroring makes
+// both slopes non-negative): a plane of an axis is crossed inside a slice iff the fraction
+// add carries, and the crossing lies at u = (2^32 - frac) / K of the slice.  The integer
+// parts never need storing: the voxel offset o advances by the axis stride on a carry.
+// Per slice this is two integer adds, two I2F + FMUL and ~20 fp32/int ops, with no fp64
+// (the fp64 ray setup fixes the fractions to ~1e-16; the increments add < 2^-33 voxel per
+// slice, < 1.2e-7 voxel over 1024 slices).  Entry and exit inside a slice (through the x
+// or z faces, or the far y face) clamp the slice to [s_lo, s_hi]; segments outside it get
+// zero length (their voxel may lie one cell outside the block: in the neighbouring row /
+// block or in the buffer slack, read or scattered with weight 0).
+//
+// Rays with |kx| or |kz| >= 1 (or parallel to the slices) can cross one axis twice in a
+// slice.  A warp containing such a lane is left to the v2 kernel (launched second, it skips
+// every warp this kernel handled), so both decide "steep" with the same predicate.
+// Distance from coordinate c (mirrored so that it increases along the ray) to the next
+// plane in 2^-64 voxel units, and the cell the walk starts in.  A point exactly on a plane
+// with a non-zero slope starts in the cell below with distance 0 (a zero-length segment,
+// then the crossing); with zero slope it stays in the cell above (half-open [lo, hi)).
+__device__ __forceinline__ unsigned long long plane_dist(double c, unsigned long long K, int& cell) {
+    const double f = floor(c);
+    cell = (int)f;
+    const double rem = 1.0 - (c - f);                         // in (0, 1]
+    if (rem >= 1.0) {                                         // on a plane
+        if (K) cell -= 1;
+        return 0ull;
+    }
+    return __double2ull_rn(rem * 18446744073709551616.0);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
+    const BlockDesc& B = L.blocks[blockIdx.z];
+    unsigned bid = blockIdx.x;
+    const int chunk = (int)(bid % (unsigned)L.n_chunks);
+    bid /= (unsigned)L.n_chunks;
+    const int slot = (int)(bid % (unsigned)L.n_slots);
+    const int band = B.band_lo + (int)(bid / (unsigned)L.n_slots);
+    const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
+    const int r0 = max(rc.z, band * L.rows_per_band), r1 = min(rc.w, band * L.rows_per_band + L.rows_per_band);
+    const int w = rc.y - rc.x;
+    if (r0 >= r1 || w <= 0) return;
+    const int nrect = (r1 - r0) * w;
+    const int base = chunk * (int)blockDim.x;
+    if (base >= nrect) return;                       // uniform over the CTA
+    const int tid = base + (int)threadIdx.x;
+    const bool inrect = tid < nrect;
+    const int iu = rc.x + (inrect ? tid % w : 0);
+    const int iv = r0 + (inrect ? tid / w : 0);
+    const int view = L.views[slot];
+    const double* vec = L.g.vecs + 12 * (size_t)view;
+    const double cxv = (L.g.beam == BSGD_PARALLEL) ? vec[0] : vec[3] - vec[0];
+    const double cyv = (L.g.beam == BSGD_PARALLEL) ? vec[1] : vec[4] - vec[1];
+    const bool mainX = fabs(cxv) > fabs(cyv);
+
+    double a[3], b[3];
+    make_ray(L.g, vec, iu, iv, a, b);
+    int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
+    if (mainX) {
+        double t = a[0]; a[0] = a[1]; a[1] = t;
+        t = b[0]; b[0] = b[1]; b[1] = t;
+        int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
+        q = hi[0]; hi[0] = hi[1]; hi[1] = q;
+    }
+    double inv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
+    double amin, amax;
+    bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
+    if (__any_sync(0xffffffffu, hit && lane_steep(b))) return;   // the v2 kernel takes this warp
+    const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    float rs = 0.f;
+    if (MODE == PROJ_BP) {
+        if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
+        hit = hit && (rs != 0.f);
+    }
+    const float* __restrict__ src = mainX ? B.xT : B.xN;
+    float* dst = mainX ? B.outT : B.outN;
+
+    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1];
+    const int plane = bdx * bdy;
+    const int sy = (b[1] > 0.0) ? 1 : -1;
+    const double ainv1 = fabs(inv[1]);
+    const double TWO64 = 18446744073709551616.0;
+    int j0 = 0, j1 = -1;
+    unsigned long long DX = 0ull, DZ = 0ull, KX = 0ull, KZ = 0ull;
+    float ikx = 0.f, ikz = 0.f, slo = 0.f, shi_last = 1.f, Ls = 0.f;
+    int o = 0, sxo = 1, pstep = plane;
+    if (hit) {
+        j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
+        j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
+        if (sy * (j1 - j0) < 0) j1 = j0;              // rounding on a sub-slice chord
+        const double yin0 = (double)(sy > 0 ? j0 : j0 + 1);   // entry plane of slice j0
+        const double yin1 = (double)(sy > 0 ? j1 : j1 + 1);
+        const double ap = (yin0 - a[1]) * inv[1];           // alpha at that plane
+        const double kx = b[0] * ainv1, kz = b[2] * ainv1;  // per unit of main-axis travel
+        const bool mx = kx < 0.0, mz = kz < 0.0;
+        const double xr = a[0] + ap * b[0] - lo[0], zr = a[2] + ap * b[2] - lo[2];
+        const double xm = mx ? -xr : xr, zm = mz ? -zr : zr;
+        KX = __double2ull_rn(fabs(kx) * TWO64);
+        KZ = __double2ull_rn(fabs(kz) * TWO64);
+        int cxm, czm;
+        DX = plane_dist(xm, KX, cxm);
+        DZ = plane_dist(zm, KZ, czm);
+        const int ix = mx ? -cxm - 1 : cxm;                   // frame cell relative to lo
+        const int iz = mz ? -czm - 1 : czm;
+        ikx = KX ? (float)(1.0 / (double)KX) : 0.f;
+        ikz = KZ ? (float)(1.0 / (double)KZ) : 0.f;
+        sxo = mx ? -1 : 1;
+        pstep = mz ? -plane : plane;
+        o = iz * plane + (j0 - lo[1]) * bdx + ix;
+        slo = (float)fmin(fmax((amin - ap) * fabs(b[1]), 0.0), 1.0);
+        const double aq = (yin1 - a[1]) * inv[1];
+        shi_last = (float)fmin(fmax((amax - aq) * fabs(b[1]), 0.0), 1.0);
+        if (j1 == j0) shi_last = fmaxf(shi_last, slo);
+        Ls = (float)(blen * ainv1);
+    }
+    const int rowstep = sy * bdx;
+    const float* pfb = src + (L.pf_rows - 1) * rowstep;   // FP: L1 prefetch lead (slack covers it)
+    const float wbp = Ls * rs;   // BP weight per unit of main-axis travel
+    double acc = 0.0;
+    float acc32 = 0.f;
+    unsigned int nvis = 0;
+
+    for (int pass = 0; pass < 2; ++pass) {
+        const int dir = pass == 0 ? 1 : -1;
+        const bool mine = hit && (pass == 0 ? sy > 0 : sy < 0);
+        if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
+        int jl = mine ? min(j0, j1) : INT_MAX;
+        int jh = mine ? max(j0, j1) : INT_MIN;
+        jl = __reduce_min_sync(0xffffffffu, jl);
+        jh = __reduce_max_sync(0xffffffffu, jh);
+        const int jstart = dir > 0 ? jl : jh;
+        const int nsl = jh - jl + 1;
+        const int k0 = mine ? dir * (j0 - jstart) : INT_MAX;   // this lane's slices [k0, k1]
+        const int nk = mine ? dir * (j1 - j0) : 0;
+        for (int k = 0; k < nsl; ++k) {
+            if ((unsigned)(k - k0) <= (unsigned)nk) {
+                const float shi = (k - k0 == nk) ? shi_last : 1.f;
+                const bool cx = DX < KX, cz = DZ < KZ;              // borrows = plane crossings
+                const float ux = __ull2float_rn(DX) * ikx;          // crossing point in the slice
+                const float uz = __ull2float_rn(DZ) * ikz;
+                const float ex = cx ? ux : 2.f, ez = cz ? uz : 2.f;
+                const bool xfirst = ex <= ez;
+                const float m1 = fminf(ex, ez), m2 = fmaxf(ex, ez);
+                const float c1 = fminf(fmaxf(m1, slo), shi), c2 = fminf(fmaxf(m2, slo), shi);
+                const float l0 = c1 - slo, l1 = c2 - c1, l2 = shi - c2;
+                const int dox = cx ? sxo : 0, doz = cz ? pstep : 0;
+                const int o1 = o + (xfirst ? dox : doz);
+                const int o2 = o + dox + doz;
+                const bool p1 = cx || cz, p2 = cx && cz;
+                if (MODE == PROJ_FP) {
+                    const float x0 = __ldg(src + o);
+                    const float x1 = p1 ? __ldg(src + o1) : 0.f;
+                    const float x2 = p2 ? __ldg(src + o2) : 0.f;
+                    acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
+                }
+                if (MODE == PROJ_BP) {
+                    red_add(dst + o, l0 * wbp);
+                    red_add_if(p1, dst + o1, l1 * wbp);
+                    red_add_if(p2, dst + o2, l2 * wbp);
+                }
+                if (MODE == PROJ_COUNT)
+                    nvis += (unsigned)(l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
+                o = o2 + rowstep;
+                DX -= KX;                                           // wraps past a plane
+                DZ -= KZ;
+                slo = 0.f;
+                if (MODE == PROJ_FP) asm volatile("prefetch.global.L1 [%0];" ::"l"(pfb + o));
+            }
+            if (MODE == PROJ_FP && (k & 15) == 15) {   // warp-uniform
+                acc += (double)acc32;
+                acc32 = 0.f;
+            }
+        }
+    }
+    if (MODE == PROJ_FP && inrect) {
+        acc += (double)acc32;
+        acc *= (double)Ls;                  // main-axis units -> voxel lengths
+        float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
+        *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
+    }
+    if (MODE == PROJ_COUNT && L.visits) {
+        unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits + (size_t)blockIdx.z * L.n_slots + slot, (unsigned long long)s);
+    }
+}
+
 // Ones-pass: w[b][view][t] = sum over tile rays of chord(ray, box_b) = (A_t^{J_b} 1) summed.
 __global__ void __launch_bounds__(256) k_im_weights(const ImLaunch I) {
     const int view = blockIdx.y;
@@ -455,18 +656,35 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
     dim3 grid((unsigned)((L.max_rect_rays + 255) / 256), (unsigned)L.n_slots, (unsigned)L.n_blocks);
     static const int version = [] {
         const char* e = getenv("BSGD_PROJECTOR");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 3;
     }();
     if (version == 1) {
         if (mode == PROJ_FP) k_project<PROJ_FP><<<grid, 256, 0, st>>>(L);
         else if (mode == PROJ_BP) k_project<PROJ_BP><<<grid, 256, 0, st>>>(L);
         else k_project<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
-    } else {
+    } else if (version == 2) {
         dim3 g2((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
         if (g2.x == 0) return;
         if (mode == PROJ_FP) k_project2<PROJ_FP><<<g2, 256, 0, st>>>(L);
         else if (mode == PROJ_BP) k_project2<PROJ_BP><<<g2, 256, 0, st>>>(L);
         else k_project2<PROJ_COUNT><<<g2, 256, 0, st>>>(L);
+    } else {
+        // v3 (fixed-point slice stepping) for every warp without steep rays, then the v2
+        // traversal for the warps v3 skipped (same launch geometry, same predicate)
+        dim3 g2((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
+        if (g2.x == 0) return;
+        if (mode == PROJ_FP) {
+            k_project3<PROJ_FP><<<g2, 256, 0, st>>>(L);
+            k_project2<PROJ_FP, true><<<g2, 256, 0, st>>>(L);
+        } else if (mode == PROJ_BP) {
+            k_project3<PROJ_BP><<<g2, 256, 0, st>>>(L);
+            k_project2<PROJ_BP, true><<<g2, 256, 0, st>>>(L);
+        } else {
+            k_project3<PROJ_COUNT><<<g2, 256, 0, st>>>(L);
+            k_project2<PROJ_COUNT, true><<<g2, 256, 0, st>>>(L);
+        }
+        BSGD_CUDA(cudaGetLastError());
+        note_launch();
     }
     BSGD_CUDA(cudaGetLastError());
     note_launch();
