@@ -439,6 +439,43 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
 // Rays with |kx| or |kz| >= 1 (or parallel to the slices) can cross one axis twice in a
 // slice.  A warp containing such a lane is left to the v2 kernel (launched second, it skips
 // every warp this kernel handled), so both decide "steep" with the same predicate.
+// One slice's gathers / reductions, predicated inside PTX (no branches):
+//   segment 0 iff the lane is in its slice range (rel <= nk, unsigned),
+//   segment 1 iff also some plane is crossed (m_or != 0), segment 2 iff both are (m_and != 0).
+__device__ __forceinline__ void gather3(unsigned rel, unsigned nk, unsigned m_or, unsigned m_and,
+                                        const float* p0, const float* p1, const float* p2,
+                                        float& v0, float& v1, float& v2) {
+    v0 = 0.f; v1 = 0.f; v2 = 0.f;
+    asm("{\n\t.reg .pred a, b, c;\n\t"
+        "setp.le.u32 a, %3, %4;\n\t"
+        "setp.ne.and.u32 b, %5, 0, a;\n\t"
+        "setp.ne.and.u32 c, %6, 0, a;\n\t"
+        "@a ld.global.nc.f32 %0, [%7];\n\t"
+        "@b ld.global.nc.f32 %1, [%8];\n\t"
+        "@c ld.global.nc.f32 %2, [%9];\n\t}"
+        : "+f"(v0), "+f"(v1), "+f"(v2)
+        : "r"(rel), "r"(nk), "r"(m_or), "r"(m_and), "l"(p0), "l"(p1), "l"(p2));
+}
+__device__ __forceinline__ void scatter3(unsigned rel, unsigned nk, unsigned m_or, unsigned m_and,
+                                         float* p0, float* p1, float* p2, float v0, float v1, float v2) {
+    asm volatile("{\n\t.reg .pred a, b, c;\n\t"
+                 "setp.le.u32 a, %0, %1;\n\t"
+                 "setp.ne.and.u32 b, %2, 0, a;\n\t"
+                 "setp.ne.and.u32 c, %3, 0, a;\n\t"
+                 "@a red.global.add.f32 [%4], %7;\n\t"
+                 "@b red.global.add.f32 [%5], %8;\n\t"
+                 "@c red.global.add.f32 [%6], %9;\n\t}"
+                 :: "r"(rel), "r"(nk), "r"(m_or), "r"(m_and), "l"(p0), "l"(p1), "l"(p2),
+                    "f"(v0), "f"(v1), "f"(v2));
+}
+
+// D -= K on the 64-bit plane distance; returns ~0u when it borrows (a plane is crossed).
+__device__ __forceinline__ unsigned sub_borrow(unsigned long long& D, unsigned long long K) {
+    unsigned m;
+    asm("sub.cc.u64 %0, %0, %2;\n\tsubc.u32 %1, 0, 0;" : "+l"(D), "=r"(m) : "l"(K));
+    return m;
+}
+
 // Distance from coordinate c (mirrored so that it increases along the ray) to the next
 // plane in 2^-64 voxel units, and the cell the walk starts in.  A point exactly on a plane
 // with a non-zero slope starts in the cell below with distance 0 (a zero-length segment,
@@ -508,18 +545,35 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     const int sy = (b[1] > 0.0) ? 1 : -1;
     const double ainv1 = fabs(inv[1]);
     const double TWO64 = 18446744073709551616.0;
+    // The warp walks the slices of each direction group (sy > 0, then sy < 0) in lockstep
+    // from the group's first slice jstart.  Every lane's stepping state is set up AT jstart's
+    // entry plane by extending its ray (cells outside the block are never dereferenced:
+    // loads / reductions are predicated on the lane's own slice range [k0, k0 + nk]), so the
+    // loop needs no per-lane freezing of state before the lane's first slice.
     int j0 = 0, j1 = -1;
-    unsigned long long DX = 0ull, DZ = 0ull, KX = 0ull, KZ = 0ull;
-    float ikx = 0.f, ikz = 0.f, slo = 0.f, shi_last = 1.f, Ls = 0.f;
-    int o = 0, sxo = 1, pstep = plane;
     if (hit) {
         j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
         j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
         if (sy * (j1 - j0) < 0) j1 = j0;              // rounding on a sub-slice chord
-        const double yin0 = (double)(sy > 0 ? j0 : j0 + 1);   // entry plane of slice j0
+    }
+    const bool pos = hit && sy > 0, neg = hit && sy < 0;
+    const int jlo_p = __reduce_min_sync(0xffffffffu, pos ? j0 : INT_MAX);
+    const int jhi_p = __reduce_max_sync(0xffffffffu, pos ? j1 : INT_MIN);
+    const int jlo_n = __reduce_min_sync(0xffffffffu, neg ? j1 : INT_MAX);
+    const int jhi_n = __reduce_max_sync(0xffffffffu, neg ? j0 : INT_MIN);
+    unsigned long long DX = 0ull, DZ = 0ull, KX = 0ull, KZ = 0ull;
+    float ikx = 0.f, ikz = 0.f, slo = 0.f, shi_last = 1.f, Ls = 0.f;
+    unsigned o = 0u;   // wraps freely outside the lane's range; exact inside it
+    int sxo = 1, pstep = plane, k0 = INT_MAX, nk = 0;
+    if (hit) {
+        const int jstart = sy > 0 ? jlo_p : jhi_n;
+        k0 = sy * (j0 - jstart);
+        nk = sy * (j1 - j0);
+        const double ys = (double)(sy > 0 ? jstart : jstart + 1);   // entry plane of jstart
+        const double yin0 = (double)(sy > 0 ? j0 : j0 + 1);         // entry plane of slice j0
         const double yin1 = (double)(sy > 0 ? j1 : j1 + 1);
-        const double ap = (yin0 - a[1]) * inv[1];           // alpha at that plane
-        const double kx = b[0] * ainv1, kz = b[2] * ainv1;  // per unit of main-axis travel
+        const double ap = (ys - a[1]) * inv[1];                     // alpha at plane ys
+        const double kx = b[0] * ainv1, kz = b[2] * ainv1;          // per unit of main-axis travel
         const bool mx = kx < 0.0, mz = kz < 0.0;
         const double xr = a[0] + ap * b[0] - lo[0], zr = a[2] + ap * b[2] - lo[2];
         const double xm = mx ? -xr : xr, zm = mz ? -zr : zr;
@@ -528,79 +582,79 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         int cxm, czm;
         DX = plane_dist(xm, KX, cxm);
         DZ = plane_dist(zm, KZ, czm);
-        const int ix = mx ? -cxm - 1 : cxm;                   // frame cell relative to lo
+        const int ix = mx ? -cxm - 1 : cxm;                         // frame cell relative to lo
         const int iz = mz ? -czm - 1 : czm;
+        // K = 0 (ray parallel to that axis' planes): an infinite distance, never crossed
+        if (!KX) DX = ~0ull;
+        if (!KZ) DZ = ~0ull;
         ikx = KX ? (float)(1.0 / (double)KX) : 0.f;
         ikz = KZ ? (float)(1.0 / (double)KZ) : 0.f;
         sxo = mx ? -1 : 1;
         pstep = mz ? -plane : plane;
-        o = iz * plane + (j0 - lo[1]) * bdx + ix;
-        slo = (float)fmin(fmax((amin - ap) * fabs(b[1]), 0.0), 1.0);
-        const double aq = (yin1 - a[1]) * inv[1];
-        shi_last = (float)fmin(fmax((amax - aq) * fabs(b[1]), 0.0), 1.0);
+        o = (unsigned)iz * (unsigned)plane + (unsigned)(jstart - lo[1]) * (unsigned)bdx + (unsigned)ix;
+        slo = (float)fmin(fmax((amin - (yin0 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
+        shi_last = (float)fmin(fmax((amax - (yin1 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
         if (j1 == j0) shi_last = fmaxf(shi_last, slo);
         Ls = (float)(blen * ainv1);
     }
     const int rowstep = sy * bdx;
-    const float* pfb = src + (L.pf_rows - 1) * rowstep;   // FP: L1 prefetch lead (slack covers it)
     const float wbp = Ls * rs;   // BP weight per unit of main-axis travel
     double acc = 0.0;
     float acc32 = 0.f;
+    float pv0 = 0.f, pv1 = 0.f, pv2 = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f;   // FP: previous slice
     unsigned int nvis = 0;
 
     for (int pass = 0; pass < 2; ++pass) {
-        const int dir = pass == 0 ? 1 : -1;
-        const bool mine = hit && (pass == 0 ? sy > 0 : sy < 0);
-        if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
-        int jl = mine ? min(j0, j1) : INT_MAX;
-        int jh = mine ? max(j0, j1) : INT_MIN;
-        jl = __reduce_min_sync(0xffffffffu, jl);
-        jh = __reduce_max_sync(0xffffffffu, jh);
-        const int jstart = dir > 0 ? jl : jh;
+        const int jl = pass == 0 ? jlo_p : jlo_n, jh = pass == 0 ? jhi_p : jhi_n;
+        if (jl > jh) continue;                                      // warp-uniform
         const int nsl = jh - jl + 1;
-        const int k0 = mine ? dir * (j0 - jstart) : INT_MAX;   // this lane's slices [k0, k1]
-        const int nk = mine ? dir * (j1 - j0) : 0;
+        const int kb = (pass == 0 ? pos : neg) ? k0 : INT_MAX;      // this lane's slices [kb, kb + nk]
         for (int k = 0; k < nsl; ++k) {
-            if ((unsigned)(k - k0) <= (unsigned)nk) {
-                const float shi = (k - k0 == nk) ? shi_last : 1.f;
-                const bool cx = DX < KX, cz = DZ < KZ;              // borrows = plane crossings
-                const float ux = __ull2float_rn(DX) * ikx;          // crossing point in the slice
-                const float uz = __ull2float_rn(DZ) * ikz;
-                const float ex = cx ? ux : 2.f, ez = cz ? uz : 2.f;
-                const bool xfirst = ex <= ez;
-                const float m1 = fminf(ex, ez), m2 = fmaxf(ex, ez);
-                const float c1 = fminf(fmaxf(m1, slo), shi), c2 = fminf(fmaxf(m2, slo), shi);
-                const float l0 = c1 - slo, l1 = c2 - c1, l2 = shi - c2;
-                const int dox = cx ? sxo : 0, doz = cz ? pstep : 0;
-                const int o1 = o + (xfirst ? dox : doz);
-                const int o2 = o + dox + doz;
-                const bool p1 = cx || cz, p2 = cx && cz;
-                if (MODE == PROJ_FP) {
-                    const float x0 = __ldg(src + o);
-                    const float x1 = p1 ? __ldg(src + o1) : 0.f;
-                    const float x2 = p2 ? __ldg(src + o2) : 0.f;
-                    acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
-                }
-                if (MODE == PROJ_BP) {
-                    red_add(dst + o, l0 * wbp);
-                    red_add_if(p1, dst + o1, l1 * wbp);
-                    red_add_if(p2, dst + o2, l2 * wbp);
-                }
-                if (MODE == PROJ_COUNT)
-                    nvis += (unsigned)(l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
-                o = o2 + rowstep;
-                DX -= KX;                                           // wraps past a plane
-                DZ -= KZ;
-                slo = 0.f;
-                if (MODE == PROJ_FP) asm volatile("prefetch.global.L1 [%0];" ::"l"(pfb + o));
+            const int rel = k - kb;
+            const bool in = (unsigned)rel <= (unsigned)nk;
+            const float sl = rel == 0 ? slo : 0.f;
+            const float sh = rel == nk ? shi_last : 1.f;
+            // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
+            // plane distance borrows; u = 2 (beyond sh) otherwise
+            const float fx = __ull2float_rn(DX) * ikx;
+            const unsigned bx = sub_borrow(DX, KX);                 // ~0u on a plane crossing
+            const float ux = bx ? fx : 2.f;
+            const float fz = __ull2float_rn(DZ) * ikz;
+            const unsigned bz = sub_borrow(DZ, KZ);
+            const float uz = bz ? fz : 2.f;
+            const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
+            const float c1 = fminf(fmaxf(m1, sl), sh), c2 = fminf(fmaxf(m2, sl), sh);
+            const float l0 = c1 - sl, l1 = c2 - c1, l2 = sh - c2;
+            const unsigned dox = bx & (unsigned)sxo, doz = bz & (unsigned)pstep;
+            const unsigned o1 = o + (ux <= uz ? dox : doz);
+            const unsigned o2 = o + dox + doz;
+            const unsigned mor = bx | bz, mand = bx & bz;
+            if (MODE == PROJ_FP) {
+                // software pipeline: this slice's gathers are issued before the previous
+                // slice's values are consumed (two slices of loads in flight per warp)
+                float v0, v1, v2;
+                gather3((unsigned)rel, (unsigned)nk, mor, mand, src + (int)o, src + (int)o1,
+                        src + (int)o2, v0, v1, v2);
+                acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
+                pv0 = v0; pv1 = v1; pv2 = v2;
+                pl0 = l0; pl1 = l1; pl2 = l2;
             }
-            if (MODE == PROJ_FP && (k & 15) == 15) {   // warp-uniform
+            if (MODE == PROJ_BP)
+                scatter3((unsigned)rel, (unsigned)nk, mor, mand, dst + (int)o, dst + (int)o1,
+                         dst + (int)o2, l0 * wbp, l1 * wbp, l2 * wbp);
+            if (MODE == PROJ_COUNT) {
+                const bool p1 = in && mor != 0u, p2 = in && mand != 0u;
+                nvis += (unsigned)(in && l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
+            }
+            o = o2 + (unsigned)rowstep;
+            if (MODE == PROJ_FP && (k & 15) == 15) {               // warp-uniform
                 acc += (double)acc32;
                 acc32 = 0.f;
             }
         }
     }
     if (MODE == PROJ_FP && inrect) {
+        acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
         acc += (double)acc32;
         acc *= (double)Ls;                  // main-axis units -> voxel lengths
         float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;

@@ -13,11 +13,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k "
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/launches_${TAG}.log 2>&1
 # FP (full set) and BP (sections that replay reliably with the atomics)
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:k_project2 -s 6 -c 1 -o gpurun_out/prof_fp_${TAG} -f \
+  -k regex:k_project3 -s 6 -c 1 -o gpurun_out/prof_fp_${TAG} -f \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_fp_${TAG}.log 2>&1
 timeout 900 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section ComputeWorkloadAnalysis \
   --section WarpStateStats --section SchedulerStats --section Occupancy --section LaunchStats \
   --metrics lts__t_sectors_op_red.sum,lts__t_requests_op_red.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \
-  --clock-control none -k regex:k_project2 -s 7 -c 1 -o gpurun_out/prof_bp_${TAG} -f \
+  --clock-control none -k regex:k_project3 -s 7 -c 1 -o gpurun_out/prof_bp_${TAG} -f \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_bp_${TAG}.log 2>&1
 ls -la gpurun_out
