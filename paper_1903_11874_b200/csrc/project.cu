@@ -54,10 +54,21 @@ __device__ __forceinline__ void red_add_if(bool pred, float* p, float v) {
 }
 
 __device__ __forceinline__ bool lane_steep(const double b[3]) {
-    // K = |b_c / b_1| * 2^32 must round below 2^32 (a 32-bit increment without carry into
-    // the integer part); the tiny margin keeps the rounded increment < 2^32 - 1
+    // |b_c / b_1| < 1 with a margin (the v3 increments K = |b_c / b_1| 2^64 stay < 2^64)
     const double lim = fabs(b[1]) * (1.0 - 1.0 / 1073741824.0);
     return b[1] == 0.0 || !(fabs(b[0]) < lim) || !(fabs(b[2]) < lim);
+}
+// v3 main axis, chosen per WARP (majority of its rays; the lanes must share one layout for
+// coalescing): fewer steep lanes than a per-view choice where the fan/cone spans 45 deg.
+__device__ __forceinline__ bool warp_main_x(const double b[3], bool inrect) {
+    const unsigned vx = __ballot_sync(0xffffffffu, inrect && fabs(b[0]) > fabs(b[1]));
+    const unsigned n = __ballot_sync(0xffffffffu, inrect);
+    return 2 * __popc(vx) > __popc(n);
+}
+// lane_steep evaluated in the v3 frame of a world-frame direction b
+__device__ __forceinline__ bool lane_steep_v3(const double b[3], bool mainX) {
+    const double f[3] = {mainX ? b[1] : b[0], mainX ? b[0] : b[1], b[2]};
+    return lane_steep(f);
 }
 
 // Ray (view, iv, iu) in grid coordinates, exactly as the problem defines it.
@@ -254,6 +265,8 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     double a[3], b[3];
     make_ray(L.g, vec, iu, iv, a, b);
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
+    bool steep3 = false;   // STEEP_ONLY: the v3 kernel's predicate, in the v3 kernel's frame
+    if (STEEP_ONLY) steep3 = lane_steep_v3(b, warp_main_x(b, inrect));
     int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
     if (mainX) {
         double t = a[0]; a[0] = a[1]; a[1] = t;
@@ -269,7 +282,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     double amin, amax;
     bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
     // v3 companion mode: only the warps k_project3 leaves (a lane with a steep ray)
-    if (STEEP_ONLY && !__any_sync(0xffffffffu, hit && lane_steep(b))) return;
+    if (STEEP_ONLY && !__any_sync(0xffffffffu, hit && steep3)) return;
     float rs = 0.f;
     if (MODE == PROJ_BP) {
         if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
@@ -512,12 +525,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     const int iv = r0 + (inrect ? tid / w : 0);
     const int view = L.views[slot];
     const double* vec = L.g.vecs + 12 * (size_t)view;
-    const double cxv = (L.g.beam == BSGD_PARALLEL) ? vec[0] : vec[3] - vec[0];
-    const double cyv = (L.g.beam == BSGD_PARALLEL) ? vec[1] : vec[4] - vec[1];
-    const bool mainX = fabs(cxv) > fabs(cyv);
 
     double a[3], b[3];
     make_ray(L.g, vec, iu, iv, a, b);
+    const bool mainX = warp_main_x(b, inrect);
     int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
     if (mainX) {
         double t = a[0]; a[0] = a[1]; a[1] = t;
