@@ -299,7 +299,8 @@ def run_ours(args, rank, world, local_rank):
             "vs_gbs": 900.0,
             "note": "residual phase time includes the partial-sum and residual kernels, so this is a lower bound "
                     "on the collective's own bus bandwidth"},
-        "roofline": {"bound": "hbm", "kernel": "k_project<FP>" if dom == "fp" else "k_project<BP>",
+        "roofline": {"bound": "hbm", "kernel": ("k_project3<FP> (+ k_project2<FP, steep-only>)" if dom == "fp"
+                                else "k_project3<BP> (+ k_project2<BP, steep-only>)"),
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes": f"{'4' if dom == 'fp' else '8'} B x {vis_ep:.4g} visits per launch",

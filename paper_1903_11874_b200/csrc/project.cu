@@ -2,21 +2,22 @@
 // PAPER.md:139), matched BP g = s (A_I^J)^T r (Algo 1 line 9),
 // and the ones-pass block masses of BSGD-IM.
 //
-// Design (DESIGN.md §"Projector"):
+// Design:
 //  * a2 ray setup in fp64 (IEEE round-to-nearest, no FMA contraction, the same
 //    parametrisation p(alpha) = a + alpha b, alpha in [0,1], as the problem
 //    definition) and slab clipping against the block box;
-//  * traversal "slice by slice" along the view's main in-plane axis: every warp
-//    (32 adjacent detector columns of one detector row) walks the planes of the
-//    main axis in LOCKSTEP, so at every step the 32 lanes touch 32 neighbouring
-//    voxels of one image row -> coalesced 128-byte gathers (FP) and coalesced
-//    reductions (BP).  Inside a slice the exact Siddon segments are produced by
-//    the crossings of the other two axes: the t of the next plane crossing of each
-//    axis is kept in fp64 and advanced by |1/b| (drift ~1e-13 over a whole ray),
-//    every in-slice decision runs in fp32 on t-differences (lengths ~1e-7 relative).
-//  * views whose central ray is x-major use a transposed copy of the block
-//    ([z][x][y]) with x<->y swapped in the ray, so the lockstep axis is always
-//    the slow in-plane axis of the layout that is read.
+//  * traversal "slice by slice" along a main in-plane axis: every warp (32 adjacent
+//    detector columns of one detector row) walks the planes of that axis in LOCKSTEP, so
+//    at every step the 32 lanes touch 32 neighbouring voxels of one image row ->
+//    coalesced 128-byte gathers (FP) and coalesced reductions (BP).  Inside a slice the
+//    exact Siddon segments are cut by the crossings of the other two axes.
+//      k_project3 (default, v3): crossings from 64-bit fixed-point plane distances (no
+//        fp64 in the loop); warps with a "steep" ray are left to
+//      k_project2 (v2): crossing t kept in fp64, advanced by |1/b|; decisions in fp32 on
+//        t-differences.  k_project (v1): per-segment DDA, kept for A/B.
+//  * warps whose main axis is x read a transposed copy of the block ([z][x][y]) with
+//    x<->y swapped in the ray, so the lockstep axis is always the slow in-plane axis of
+//    the layout that is read.
 //  * no tensor cores: this is a sparse gather/scatter.
 #include <climits>
 #include <cstdlib>
