@@ -610,6 +610,8 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         Ls = (float)(blen * ainv1);
     }
     const int rowstep = sy * bdx;
+    const unsigned nsxo = (unsigned)(-sxo), npstep = (unsigned)(-pstep);
+    const float shm1 = shi_last - 1.f;
     const float wbp = Ls * rs;   // BP weight per unit of main-axis travel
     double acc = 0.0;
     float acc32 = 0.f;
@@ -621,11 +623,23 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         if (jl > jh) continue;                                      // warp-uniform
         const int nsl = jh - jl + 1;
         const int kb = (pass == 0 ? pos : neg) ? k0 : INT_MAX;      // this lane's slices [kb, kb + nk]
+        // float copies of rel = k - kb and rel - nk (exact integers): the first / last slice
+        // flags come from FFMA.SAT on the FMA pipe (sat(1 - r^2) = [r == 0]) instead of
+        // compare + select on the ALU pipe, which binds this loop
+        float fr = (float)max(-kb, -(1 << 23)), fe = fr - (float)nk;
         for (int k = 0; k < nsl; ++k) {
             const int rel = k - kb;
             const bool in = (unsigned)rel <= (unsigned)nk;
-            const float sl = rel == 0 ? slo : 0.f;
-            const float sh = rel == nk ? shi_last : 1.f;
+            float sl, sh;
+            if (MODE == PROJ_BP) {   // BP is ALU-bound: flags on the FMA pipe
+                sl = slo * __saturatef(fmaf(-fr, fr, 1.f));
+                sh = fmaf(__saturatef(fmaf(-fe, fe, 1.f)), shm1, 1.f);
+                fr += 1.f;
+                fe += 1.f;
+            } else {                 // FP is issue-bound: fewer instructions
+                sl = rel == 0 ? slo : 0.f;
+                sh = rel == nk ? shi_last : 1.f;
+            }
             // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
             // plane distance borrows; u = 2 (beyond sh) otherwise
             const float fx = __ull2float_rn(DX) * ikx;
@@ -637,9 +651,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
             const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
             const float c1 = fminf(fmaxf(m1, sl), sh), c2 = fminf(fmaxf(m2, sl), sh);
             const float l0 = c1 - sl, l1 = c2 - c1, l2 = sh - c2;
-            const unsigned dox = bx & (unsigned)sxo, doz = bz & (unsigned)pstep;
+            // bx, bz are 0 or ~0u (= -1): the steps as multiply-adds (FMA pipe)
+            const unsigned dox = bx * nsxo, doz = bz * npstep;
             const unsigned o1 = o + (ux <= uz ? dox : doz);
-            const unsigned o2 = o + dox + doz;
+            const unsigned o2 = bz * npstep + (bx * nsxo + o);
             const unsigned mor = bx | bz, mand = bx & bz;
             if (MODE == PROJ_FP) {
                 // software pipeline: this slice's gathers are issued before the previous
