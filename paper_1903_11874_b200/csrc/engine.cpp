@@ -166,7 +166,7 @@ struct bsgd_ctx_s {
     // Detector pixels (u0,u1,v0,v1) whose rays can meet the box [lo,hi) (grid coords):
     // bounding box of the projected corners + 1 pixel margin, u aligned to warps.
     // Falls back to the whole detector when a corner is not in front of the source.
-    int band_rows = 4;
+    int band_rows = 8;   // BSGD_BAND_ROWS (measured: 1: 3.31, 2: 3.46, 4: 3.54, 8: 3.56, 16: 3.54 epochs/s)
     int pf_rows = 0;   // BSGD_PF_ROWS (FP L1 prefetch lead; 0 = off, measured faster for v3)
     int4 footprint(const int lo[3], const int hi[3], int view) const {
         const int4 full = make_int4(0, nu, 0, nv);

@@ -659,8 +659,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
             if (MODE == PROJ_FP) {
                 // software pipeline: this slice's gathers are issued before the previous
                 // slice's values are consumed (two slices of loads in flight per warp)
+                // all three gathers predicated on the slice range only: without a crossing
+                // o1 = o2 = o (an L1 hit) and l1 = l2 = 0 exactly, so no crossing masks
                 float v0, v1, v2;
-                gather3((unsigned)rel, (unsigned)nk, mor, mand, src + (int)o, src + (int)o1,
+                gather3((unsigned)rel, (unsigned)nk, ~0u, ~0u, src + (int)o, src + (int)o1,
                         src + (int)o2, v0, v1, v2);
                 acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
                 pv0 = v0; pv1 = v1; pv2 = v2;
