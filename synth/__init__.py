@@ -90,6 +90,25 @@ def circular(beam: str | int, n_views: int, arc_deg: float, OP: float, OD: float
     return out
 
 
+def laminography(n_views: int, tilt_deg: float, OP: float, OD: float, det_u: int, det_v: int,
+                 pitch_u: float, pitch_v: float) -> np.ndarray:
+    """Cone-beam laminography vectors (PAPER.md:75 motivates arbitrary
+    trajectories): the rotation axis is z, the beam is inclined by `tilt_deg` out of the
+    xy-plane.  Source OP*(cos a cos t, cos a sin t, sin a), detector centre opposite at
+    -OD*(same), u = pitch_u*(-sin t, cos t, 0), v = pitch_v*(-sin a cos t, -sin a sin t,
+    cos a) (orthogonal to u and to the central ray).  Shape (n_views, 12), float64."""
+    ca, sa = cos_sin_deg(tilt_deg)
+    out = np.zeros((n_views, 12), dtype=np.float64)
+    for vi in range(n_views):
+        c, s = cos_sin_deg(vi * 360.0 / n_views)
+        d = np.array([ca * c, ca * s, sa])
+        out[vi, 0:3] = OP * d
+        out[vi, 3:6] = -OD * d
+        out[vi, 6:9] = (pitch_u * -s, pitch_u * c, 0.0)
+        out[vi, 9:12] = (pitch_v * -sa * c, pitch_v * -sa * s, pitch_v * ca)
+    return out
+
+
 @dataclass(frozen=True)
 class Geometry:
     beam: int

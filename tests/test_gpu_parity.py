@@ -129,6 +129,16 @@ def test_operator_parity_rects_and_ragged(bs):
     _fp_bp_check(bs, g2, (2, 1, 2), 1, np.arange(6), range(4))
 
 
+@pytest.mark.parametrize("tilt", [20.0, 40.0])
+def test_operator_parity_laminography_octants(bs, tilt):
+    """N4: an arbitrary trajectory through the per-view vectors — cone-beam
+    laminography with the beam inclined by `tilt` — over a 2x2x2 octant block grid (N3's
+    cubic blocks).  At 40 deg many rays have |k_z| >= 1 (the steep v2 path)."""
+    vecs = synth.laminography(16, tilt, 90.0, 60.0, 48, 40, 1.4, 1.3)
+    g = synth.Geometry(synth.CONE, vecs, 48, 40, (40, 36, 24))
+    _fp_bp_check(bs, g, (2, 2, 2), 4, np.arange(16), range(8))
+
+
 def test_im_table(bs):
     """Ones-pass block masses vs the oracle's traced masses; integer table bit-exact."""
     for name, kw in [("cfg2", {}), ("cfg3", dict(K=64, n_views=40))]:
