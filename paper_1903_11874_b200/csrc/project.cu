@@ -14,7 +14,7 @@
 //      k_project3 (default, v3): crossings from 64-bit fixed-point plane distances (no
 //        fp64 in the loop); warps with a "steep" ray are left to
 //      k_project2 (v2): crossing t kept in fp64, advanced by |1/b|; decisions in fp32 on
-//        t-differences.  k_project (v1): per-segment DDA, kept for A/B.
+//        t-differences (also the whole path under BSGD_PROJECTOR=2, for A/B).
 //  * warps whose main axis is x read a transposed copy of the block ([z][x][y]) with
 //    x<->y swapped in the ray, so the lockstep axis is always the slow in-plane axis of
 //    the layout that is read.
@@ -109,128 +109,6 @@ __device__ __forceinline__ bool clip(const double a[3], const double b[3], const
     return ok && amin < amax;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_project(const ProjLaunch L) {
-    const int slot = blockIdx.y;
-    const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
-    const int w = rc.y - rc.x, h = rc.w - rc.z;
-    const long long nrect = (long long)w * h;
-    const long long base = (long long)blockIdx.x * blockDim.x;
-    if (base >= nrect) return;                       // uniform over the CTA
-    const long long tid = base + threadIdx.x;
-    const bool inrect = tid < nrect;
-    const int iu = rc.x + (inrect ? (int)(tid % w) : 0);
-    const int iv = rc.z + (inrect ? (int)(tid / w) : 0);
-    const int view = L.views[slot];
-    const double* vec = L.g.vecs + 12 * (size_t)view;
-    const BlockDesc& B = L.blocks[blockIdx.z];
-
-    // main in-plane axis of the view (uniform over the CTA)
-    double cx = (L.g.beam == BSGD_PARALLEL) ? vec[0] : vec[3] - vec[0];
-    double cy = (L.g.beam == BSGD_PARALLEL) ? vec[1] : vec[4] - vec[1];
-    const bool mainX = fabs(cx) > fabs(cy);
-
-    double a[3], b[3];
-    make_ray(L.g, vec, iu, iv, a, b);
-    const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
-    int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
-    if (mainX) {   // work in the frame (y, x, z): the lockstep axis is frame-y
-        double t = a[0]; a[0] = a[1]; a[1] = t;
-        t = b[0]; b[0] = b[1]; b[1] = t;
-        int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
-        q = hi[0]; hi[0] = hi[1]; hi[1] = q;
-    }
-    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1], bdz = hi[2] - lo[2];
-    const long long plane = (long long)bdx * bdy;
-    double inv[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
-
-    double amin, amax;
-    bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
-    float rs = 0.f;
-    if (MODE == PROJ_BP) {
-        if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
-        hit = hit && (rs != 0.f);
-    }
-    const float* src = mainX ? B.xT : B.xN;
-    float* dst = mainX ? B.outT : B.outN;
-
-    const int sx = sgn(b[0]), sy = sgn(b[1]), sz = sgn(b[2]);
-    int j0 = 0, j1 = -1, ix = 0, iz = 0;
-    double t = 0.0, tx = 0.0, tz = 0.0;
-    const double INF = __longlong_as_double(0x7ff0000000000000ll);
-    if (hit) {
-        j0 = cell_enter(a[1] + amin * b[1], sy, lo[1], hi[1]);
-        j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
-        if (sy == 0) j1 = j0;
-        ix = cell_enter(a[0] + amin * b[0], sx, lo[0], hi[0]);
-        iz = cell_enter(a[2] + amin * b[2], sz, lo[2], hi[2]);
-        tx = sx ? ((double)(ix + (sx > 0)) - a[0]) * inv[0] : INF;
-        tz = sz ? ((double)(iz + (sz > 0)) - a[2]) * inv[2] : INF;
-        t = amin;
-    }
-    double acc = 0.0;
-    unsigned int nvis = 0;
-    const double a1 = a[1], inv1 = inv[1];
-
-    for (int pass = 0; pass < 2; ++pass) {
-        const int dir = pass == 0 ? 1 : -1;
-        const bool mine = hit && (pass == 0 ? sy >= 0 : sy < 0);
-        if (__ballot_sync(0xffffffffu, mine) == 0u) continue;
-        int jl = mine ? min(j0, j1) : INT_MAX;
-        int jh = mine ? max(j0, j1) : INT_MIN;
-        jl = __reduce_min_sync(0xffffffffu, jl);
-        jh = __reduce_max_sync(0xffffffffu, jh);
-        const int jstart = dir > 0 ? jl : jh;
-        const int nsl = jh - jl + 1;
-        for (int k = 0; k < nsl; ++k) {
-            const int j = jstart + dir * k;
-            const bool in = mine && (dir > 0 ? (j >= j0 && j <= j1) : (j <= j0 && j >= j1));
-            if (in) {
-                double thi = amax;
-                if (sy != 0) thi = fmin(amax, ((double)(sy > 0 ? j + 1 : j) - a1) * inv1);
-                const long long rowoff = (long long)(j - lo[1]) * bdx;
-                for (;;) {
-                    const double tn = fmin(fmin(tx, tz), thi);
-                    if (tn > t) {
-                        const unsigned ux = (unsigned)(ix - lo[0]), uz = (unsigned)(iz - lo[2]);
-                        if (ux < (unsigned)bdx && uz < (unsigned)bdz) {
-                            const long long addr = (long long)uz * plane + rowoff + ux;
-                            const double len = (tn - t) * blen;
-                            if (MODE == PROJ_FP) acc += len * (double)__ldg(src + addr);
-                            if (MODE == PROJ_BP) red_add(dst + addr, (float)(len * (double)rs));
-                            ++nvis;
-                        }
-                        t = tn;
-                    }
-                    if (tx <= tz) {
-                        if (tx < thi) {
-                            ix += sx;
-                            tx = ((double)(ix + (sx > 0)) - a[0]) * inv[0];
-                            continue;
-                        }
-                    } else if (tz < thi) {
-                        iz += sz;
-                        tz = ((double)(iz + (sz > 0)) - a[2]) * inv[2];
-                        continue;
-                    }
-                    break;
-                }
-                t = thi;
-            }
-        }
-    }
-    if (MODE == PROJ_FP && inrect) {
-        float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
-        *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
-    }
-    if (L.visits) {
-        unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
-        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits, (unsigned long long)s);
-    }
-}
-
 // v2 traversal: the same slice-lockstep Siddon, with a straight-line slice body for the
 // common case (at most one x and one z plane crossing inside the slice: up to three
 // segments, their loads issued together), a rare general loop for further crossings,
@@ -275,7 +153,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
         int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
         q = hi[0]; hi[0] = hi[1]; hi[1] = q;
     }
-    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1], bdz = hi[2] - lo[2];
+    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1];
     const unsigned plane = (unsigned)bdx * (unsigned)bdy;
     double inv[3];
 #pragma unroll
@@ -736,39 +614,30 @@ __global__ void __launch_bounds__(256) k_im_weights(const ImLaunch I) {
 
 void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
     if (L.n_slots == 0 || L.n_blocks == 0 || L.max_rect_rays == 0) return;
-    dim3 grid((unsigned)((L.max_rect_rays + 255) / 256), (unsigned)L.n_slots, (unsigned)L.n_blocks);
     static const int version = [] {
         const char* e = getenv("BSGD_PROJECTOR");
         return e ? atoi(e) : 3;
     }();
-    if (version == 1) {
-        if (mode == PROJ_FP) k_project<PROJ_FP><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_BP) k_project<PROJ_BP><<<grid, 256, 0, st>>>(L);
-        else k_project<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
-    } else if (version == 2) {
-        dim3 g2((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
-        if (g2.x == 0) return;
-        if (mode == PROJ_FP) k_project2<PROJ_FP><<<g2, 256, 0, st>>>(L);
-        else if (mode == PROJ_BP) k_project2<PROJ_BP><<<g2, 256, 0, st>>>(L);
-        else k_project2<PROJ_COUNT><<<g2, 256, 0, st>>>(L);
-    } else {
-        // v3 (fixed-point slice stepping) for every warp without steep rays, then the v2
-        // traversal for the warps v3 skipped (same launch geometry, same predicate)
-        dim3 g2((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
-        if (g2.x == 0) return;
-        if (mode == PROJ_FP) {
-            k_project3<PROJ_FP><<<g2, 256, 0, st>>>(L);
-            k_project2<PROJ_FP, true><<<g2, 256, 0, st>>>(L);
-        } else if (mode == PROJ_BP) {
-            k_project3<PROJ_BP><<<g2, 256, 0, st>>>(L);
-            k_project2<PROJ_BP, true><<<g2, 256, 0, st>>>(L);
-        } else {
-            k_project3<PROJ_COUNT><<<g2, 256, 0, st>>>(L);
-            k_project2<PROJ_COUNT, true><<<g2, 256, 0, st>>>(L);
-        }
+    const dim3 grid((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
+    if (grid.x == 0) return;
+    if (version == 2) {   // v2 alone (A/B reference)
+        if (mode == PROJ_FP) k_project2<PROJ_FP><<<grid, 256, 0, st>>>(L);
+        else if (mode == PROJ_BP) k_project2<PROJ_BP><<<grid, 256, 0, st>>>(L);
+        else k_project2<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
         BSGD_CUDA(cudaGetLastError());
         note_launch();
+        return;
     }
+    // v3 (fixed-point slice stepping) for every warp without steep rays, then the v2
+    // traversal for the warps v3 skipped (same launch geometry, same predicate)
+    if (mode == PROJ_FP) k_project3<PROJ_FP><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BP) k_project3<PROJ_BP><<<grid, 256, 0, st>>>(L);
+    else k_project3<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+    if (mode == PROJ_FP) k_project2<PROJ_FP, true><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BP) k_project2<PROJ_BP, true><<<grid, 256, 0, st>>>(L);
+    else k_project2<PROJ_COUNT, true><<<grid, 256, 0, st>>>(L);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
