@@ -13,6 +13,8 @@ Contents
   bsgd.py      sampler, partitions, Algo 1 (BSGD), Algo 2 (BSGD-IM/RAN),
                Algo 3 (auto-mu), Algo 4 (BSGD-TV), Eq. 4 SGD, Eq. 8, FGP TV
                prox, metrics
+  solvers.py   comparison solvers GD, GD-BB, ISTA, FISTA, SVRG
+                                                            PAPER.md:70, 229, 398, 506
 
 Parity status of every function is listed in DESIGN.md §"Oracle pins".
 """
