@@ -221,6 +221,41 @@ bsgd_status bsgd_set_state(bsgd_ctx ctx, int32_t what, int32_t index, const void
 bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, double* sigma_max_sq,
                                  void* stream);
 
+/* Comparison solvers on the same operators (the methods the paper
+ * compares against in Figs. 12 and 18, cited but not listed
+ * there; the textbook forms are in oracle/solvers.py).  With g(x) = 2 A^T (y - A x)
+ * (reading A1) and the full operator A (all M row blocks, all N column blocks):
+ *   GD     x+ = x + mu g(x)
+ *   GD_BB  GD with the Barzilai-Borwein step mu_k = <s,s>/<s,w>, s = x_k - x_{k-1},
+ *          w = g(x_{k-1}) - g(x_k); mu_0 = mu0; mu kept when <s,w> <= 0
+ *   ISTA   x+ = prox_{mu lambda TV}(x + mu g(x))
+ *   FISTA  z+ = prox_{mu lambda TV}(v + mu g(v)), t+ = (1 + sqrt(1 + 4t^2))/2,
+ *          v+ = z+ + ((t - 1)/t+)(z+ - z), v_0 = x_0, t_0 = 1
+ *   SVRG   per outer iteration x~ = x, G~ = g(x~); then svrg_m (0 = M) inner steps
+ *          drawing one row block i (sampler stream 1, counter = global inner step):
+ *          x <- x - mu M 2 A_I^T A_I (x - x~) + mu G~
+ * The prox is Algo 4's FGP prox (tv_iters iterations; lambda = 0: none).
+ * y (replicated, full length) and x_owned (owned blocks, block-major) are DEVICE
+ * buffers; x_owned holds x_0 on entry and the result on return.  obj[k] (host,
+ * nullable) = 1/2 ||y - A p_k||^2 at the point p_k whose full gradient iteration k
+ * evaluates (x_k; v_k for FISTA; x~ for SVRG outer iteration k); mu[k] the step.
+ * The BSGD state of the ctx is reset afterwards (as after bsgd_run without
+ * BSGD_RESUME).  Synchronises the stream.  Collective (world > 1).            */
+typedef enum {
+    BSGD_SOLVER_GD = 0, BSGD_SOLVER_GD_BB = 1, BSGD_SOLVER_ISTA = 2, BSGD_SOLVER_FISTA = 3, BSGD_SOLVER_SVRG = 4
+} bsgd_solver;
+typedef struct {
+    int32_t solver;
+    int32_t iters;          /* outer iterations (SVRG) / iterations                      */
+    double mu0;             /* step (GD_BB: initial step)                                 */
+    double lambda;          /* TV weight of ISTA / FISTA (0 = plain)                      */
+    int32_t tv_iters;       /* FGP iterations of the prox (20)                            */
+    int32_t svrg_m;         /* SVRG inner steps per outer iteration (0 = M)               */
+    uint64_t seed;          /* SVRG row-block draws                                       */
+} bsgd_solve_params;
+bsgd_status bsgd_solve(bsgd_ctx ctx, const float* y, float* x_owned, const bsgd_solve_params* params,
+                       double* obj, double* mu, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,13 @@ class RunLog(C.Structure):
                 ("visits", C.POINTER(C.c_uint64)), ("t_ms", C.POINTER(C.c_double))]
 
 
+class SolveParams(C.Structure):
+    _fields_ = [("solver", C.c_int32), ("iters", C.c_int32), ("mu0", C.c_double), ("lambda_", C.c_double),
+                ("tv_iters", C.c_int32), ("svrg_m", C.c_int32), ("seed", C.c_uint64)]
+
+
+SOLVERS = {"gd": 0, "gd_bb": 1, "ista": 2, "fista": 3, "svrg": 4}
+
 P = C.POINTER
 _ctx = C.c_void_p
 SIGS = {
@@ -124,6 +131,8 @@ SIGS = {
     "bsgd_get_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
+    "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
+                   C.c_int),
 }
 for _name, (_args, _res) in SIGS.items():
     _f = getattr(_lib, _name)
@@ -378,6 +387,16 @@ class Context:
         return RunResult(obj[:epochs], rmse[:epochs], mu[:epochs], sr.reshape(E, aM)[:epochs],
                          sc.reshape(E, gN)[:epochs], vis[:epochs],
                          tms.reshape(E, 6)[:epochs] if tms is not None else None)
+
+    def solve(self, solver, y, x, iters, mu0, lam=0.0, tv_iters=20, svrg_m=0, seed=1, stream=None):
+        """Comparison solver `solver` in {"gd", "gd_bb", "ista", "fista", "svrg"} (bsgd_solve;
+        SURVEY §8f N1).  y, x: device tensors; x holds x_0 and receives the result.
+        Returns (obj, mu) per iteration."""
+        prm = SolveParams(SOLVERS[solver], iters, mu0, lam, tv_iters, svrg_m, seed)
+        obj, mu = np.zeros(max(iters, 1)), np.zeros(max(iters, 1))
+        self._c(_lib.bsgd_solve(self.h, _ptr(y), _ptr(x), C.byref(prm), obj.ctypes.data_as(P(C.c_double)),
+                                mu.ctypes.data_as(P(C.c_double)), _stream(stream)))
+        return obj[:iters], mu[:iters]
 
     def get_state(self, what, index=0):
         sizes = {0: (self.n_rays, np.float32), 1: (self.block_voxels, np.float32), 2: (self.block_voxels, np.float32),

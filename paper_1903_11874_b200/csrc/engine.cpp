@@ -79,6 +79,7 @@ struct bsgd_ctx_s {
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
     float *y_dev = nullptr, *x_dev = nullptr, *xt_dev = nullptr;
+    float *sv_a = nullptr, *sv_b = nullptr, *sv_c = nullptr, *sv_d = nullptr, *y_zero = nullptr;   // solvers
     double* d_normsq = nullptr;
     double* d_red = nullptr;           // 8 doubles scratch
     double* d_log = nullptr;           // per-epoch [obj, rmse] scratch
@@ -537,6 +538,157 @@ struct bsgd_ctx_s {
     }
 
     // FGP TV prox (Algo 4 line 16) on the owned volume: x <- argmin 1/2|t-x|^2 + w TV(t)
+    // ------------------------------------------------------------ comparison solvers
+    // (oracle/solvers.py).  gout = 2 A_I^T (yv - A_I p) over the views of the
+    // row blocks `rsel` and all owned column blocks (+ the residual allreduce when world > 1);
+    // ||yv_I - A_I p||^2 lands in d_normsq[i] for i in rsel.  Clobbers z, r and the BP
+    // accumulators (the BSGD state is reset after a solve).
+    void row_grad(const float* yv, float* p, float* gout, const std::vector<int>& rsel, cudaStream_t st) {
+        std::vector<int> vsel, slot_row, slots(s);
+        for (int i : rsel)
+            for (int v : rows[i]) {
+                vsel.push_back(v);
+                slot_row.push_back(i);
+            }
+        for (int b = 0; b < s; ++b) slots[b] = b;
+        const int V = (int)vsel.size();
+        refresh_xT(p, slots, st);
+        std::vector<int4> rc((size_t)s * V, make_int4(0, nu, 0, nv));
+        {
+            std::vector<const float*> xs, xts;
+            std::vector<float*> zs;
+            for (int b = 0; b < s; ++b) {
+                xs.push_back(xN + b * bsize);
+                xts.push_back(xT + b * bsize);
+                zs.push_back(z + b * n_rays);
+            }
+            project(PROJ_FP, vsel, slots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
+        }
+        {
+            std::vector<char> staging(tab_bytes / 2);
+            size_t off = tab_bytes / 2;
+            staging.resize(off);
+            ResLaunch Rl;
+            Rl.n_slots = V;
+            Rl.views = tab_put(off, vsel, staging);
+            Rl.slot_row = tab_put(off, slot_row, staging);
+            int* drows = tab_put(off, rsel, staging);
+            if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
+            BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_bytes / 2, staging.data() + tab_bytes / 2,
+                                      off - tab_bytes / 2, cudaMemcpyHostToDevice, st));
+            Rl.per = (int)per;
+            Rl.z = z;
+            Rl.n_rays = n_rays;
+            Rl.s = s;
+            Rl.y = yv;
+            Rl.r = r;
+            Rl.pc = pc;
+            Rl.normsq = d_normsq;
+            launch_zero_rows(d_normsq, drows, (int)rsel.size(), st);
+            Rl.mode = coll ? 1 : 0;
+            launch_residual(Rl, st);
+            if (coll) {
+                allreduce_f(pc, (size_t)V * per, st);
+                Rl.mode = 2;
+                launch_residual(Rl, st);
+            }
+        }
+        std::vector<float*> oN, oT;
+        std::vector<const float*> none;
+        for (int b = 0; b < s; ++b) {
+            oN.push_back(accN + b * bsize);
+            oT.push_back(accT + b * bsize);
+        }
+        project(PROJ_BP, vsel, slots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
+        for (int b = 0; b < s; ++b) update(UPD_OUT, b, p + b * bsize, 0.f, 1, gout + b * bsize, 0, st);
+    }
+
+    // host copy of 1/2 sum_i d_normsq[i] (the objective after a full row_grad)
+    double half_normsq(cudaStream_t st) {
+        BSGD_CUDA(cudaMemcpyAsync(h_normsq.data(), d_normsq, sizeof(double) * M, cudaMemcpyDeviceToHost, st));
+        BSGD_CUDA(cudaStreamSynchronize(st));
+        double s2 = 0;
+        for (double v : h_normsq) s2 += v;
+        return 0.5 * s2;
+    }
+
+    void solve(int solver, const float* y, float* x, int iters, double mu0, double lam, int tv_iters, int m,
+               uint64_t seed, double* obj_log, double* mu_log, cudaStream_t st) {
+        const long long n = (long long)s * bsize;
+        auto need = [&](float*& b) { if (!b) b = dnew<float>(n, false); };
+        std::vector<int> all(M);
+        for (int i = 0; i < M; ++i) all[i] = i;
+        double mu = mu0;
+        if (solver == BSGD_SOLVER_GD || solver == BSGD_SOLVER_ISTA) {
+            need(sv_a);                                       // g
+            for (int k = 0; k < iters; ++k) {
+                row_grad(y, x, sv_a, all, st);
+                if (obj_log) obj_log[k] = half_normsq(st);
+                if (mu_log) mu_log[k] = mu;
+                launch_lincomb(x, 1.f, x, (float)mu, sv_a, 0.f, nullptr, n, st);   // x + mu g
+                if (solver == BSGD_SOLVER_ISTA) tv_prox(x, mu * lam, tv_iters, st);
+            }
+        } else if (solver == BSGD_SOLVER_GD_BB) {
+            need(sv_a); need(sv_b); need(sv_c);               // g, x_prev, g_prev
+            for (int k = 0; k < iters; ++k) {
+                row_grad(y, x, sv_a, all, st);
+                if (obj_log) obj_log[k] = half_normsq(st);
+                if (k > 0) {                                  // BB1: <s,s> / <s,w>
+                    BSGD_CUDA(cudaMemsetAsync(d_red, 0, 2 * sizeof(double), st));
+                    launch_bb_dots(x, sv_b, sv_c, sv_a, n, d_red, st);
+                    allreduce_d(d_red, 2, st);
+                    double h2[2];
+                    BSGD_CUDA(cudaMemcpyAsync(h2, d_red, sizeof(h2), cudaMemcpyDeviceToHost, st));
+                    BSGD_CUDA(cudaStreamSynchronize(st));
+                    if (h2[1] > 0.0) mu = h2[0] / h2[1];
+                }
+                if (mu_log) mu_log[k] = mu;
+                BSGD_CUDA(cudaMemcpyAsync(sv_b, x, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+                std::swap(sv_a, sv_c);                        // g_prev <- g
+                launch_lincomb(x, 1.f, x, (float)mu, sv_c, 0.f, nullptr, n, st);
+            }
+        } else if (solver == BSGD_SOLVER_FISTA) {
+            need(sv_a); need(sv_b); need(sv_c);               // g, v, z_new
+            BSGD_CUDA(cudaMemcpyAsync(sv_b, x, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));   // v_0 = x_0
+            double t = 1.0;
+            for (int k = 0; k < iters; ++k) {
+                row_grad(y, sv_b, sv_a, all, st);             // g(v)
+                if (obj_log) obj_log[k] = half_normsq(st);
+                if (mu_log) mu_log[k] = mu;
+                launch_lincomb(sv_c, 1.f, sv_b, (float)mu, sv_a, 0.f, nullptr, n, st);   // v + mu g(v)
+                tv_prox(sv_c, mu * lam, tv_iters, st);        // z+ (lam = 0: identity)
+                const double t1 = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0, beta = (t - 1.0) / t1;
+                // v+ = z+ + beta (z+ - z)   (z = x)
+                launch_lincomb(sv_b, (float)(1.0 + beta), sv_c, (float)(-beta), x, 0.f, nullptr, n, st);
+                BSGD_CUDA(cudaMemcpyAsync(x, sv_c, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+                t = t1;
+            }
+        } else if (solver == BSGD_SOLVER_SVRG) {
+            need(sv_a); need(sv_b); need(sv_c); need(sv_d);   // G~, x~, d = x - x~, g_I(d)
+            if (!y_zero) y_zero = dnew<float>(n_rays, true);
+            const int inner = m > 0 ? m : M;
+            long long step = 0;
+            for (int k = 0; k < iters; ++k) {
+                BSGD_CUDA(cudaMemcpyAsync(sv_b, x, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+                row_grad(y, sv_b, sv_a, all, st);             // G~ = g(x~)
+                if (obj_log) obj_log[k] = half_normsq(st);
+                if (mu_log) mu_log[k] = mu;
+                for (int t = 0; t < inner; ++t, ++step) {
+                    int i = 0;
+                    host::select(seed, 1, (int)step, M, 1, &i);
+                    launch_lincomb(sv_c, 1.f, x, -1.f, sv_b, 0.f, nullptr, n, st);   // d = x - x~
+                    row_grad(y_zero, sv_c, sv_d, std::vector<int>{i}, st);          // 2 A_I^T (0 - A_I d) = -h
+                    // x <- x - mu M h + mu G~ = x + mu M (-h) + mu G~
+                    launch_lincomb(x, 1.f, x, (float)(mu * M), sv_d, (float)mu, sv_a, n, st);
+                }
+            }
+        } else {
+            fail(BSGD_E_CONTRACT, "unknown solver");
+        }
+        reset(y, st);                                         // back to the initial BSGD state
+        epoch = 0;
+    }
+
     void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st) {
         const long long n = (long long)s * bsize;
         if (!tv_u) {
@@ -964,6 +1116,24 @@ bsgd_status bsgd_step(bsgd_ctx c, const float* y, float* x_owned, const bsgd_sel
         }
         c->epoch_step(y, x_owned, rows, cols, tiles, mu, sgd, S(stream), nullptr);
         c->epoch += 1;
+    });
+}
+
+bsgd_status bsgd_solve(bsgd_ctx c, const float* y, float* x_owned, const bsgd_solve_params* P, double* obj,
+                       double* mu, void* stream) {
+    return guard(c, [&] {
+        if (!c || !y || !x_owned || !P) fail(BSGD_E_CONTRACT, "NULL");
+        if (!is_device_ptr(y) || !is_device_ptr(x_owned)) fail(BSGD_E_CONTRACT, "bsgd_solve takes device buffers");
+        if (P->solver < BSGD_SOLVER_GD || P->solver > BSGD_SOLVER_SVRG) fail(BSGD_E_CONTRACT, "unknown solver");
+        if (P->iters < 0 || !isfinite(P->mu0) || P->mu0 <= 0.0) fail(BSGD_E_CONTRACT, "iters < 0 or bad mu0");
+        if (!isfinite(P->lambda) || P->lambda < 0.0 || P->tv_iters < 0 || P->svrg_m < 0)
+            fail(BSGD_E_CONTRACT, "bad lambda / tv_iters / svrg_m");
+        const bool tv = (P->solver == BSGD_SOLVER_ISTA || P->solver == BSGD_SOLVER_FISTA) && P->lambda > 0.0;
+        if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
+            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        c->solve(P->solver, y, x_owned, P->iters, P->mu0, tv ? P->lambda : 0.0, P->tv_iters, P->svrg_m, P->seed,
+                 obj, mu, S(stream));
+        BSGD_CUDA(cudaStreamSynchronize(S(stream)));
     });
 }
 

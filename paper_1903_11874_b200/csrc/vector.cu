@@ -299,6 +299,34 @@ __global__ void __launch_bounds__(256) k_sqdiff(const float* a, const float* b, 
     if (threadIdx.x == 0) atomicAdd(out, s);
 }
 
+// out = a x + b y (+ c z): the comparison solvers' vector updates.
+// Plain fp32 streaming (HBM-bound: 12-16 B per element).
+__global__ void __launch_bounds__(256) k_lincomb(float* out, float a, const float* x, float b,
+                                                 const float* y, float c, const float* z, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        float v = fmaf(a, x[i], b * y[i]);
+        if (z) v = fmaf(c, z[i], v);
+        out[i] = v;
+    }
+}
+
+// Barzilai-Borwein dots: s = x - xp, w = gp - g  ->  out[0] += <s,s>, out[1] += <s,w> (fp64).
+__global__ void __launch_bounds__(256) k_bb_dots(const float* x, const float* xp, const float* gp,
+                                                 const float* g, long long n, double* out) {
+    double ss = 0, sw = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double s = (double)x[i] - (double)xp[i], w = (double)gp[i] - (double)g[i];
+        ss += s * s;
+        sw += s * w;
+    }
+    ss = block_sum(ss);
+    if (threadIdx.x == 0) atomicAdd(out, ss);
+    sw = block_sum(sw);
+    if (threadIdx.x == 0) atomicAdd(out + 1, sw);
+}
+
 __device__ __forceinline__ uint64_t dmix(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -476,6 +504,20 @@ void launch_dot3(const float* a, const float* b, long long n, double* out3, cuda
 
 void launch_sqdiff(const float* a, const float* b, long long n, double* out, cudaStream_t st) {
     k_sqdiff<<<grid_for(n, 8), 256, 0, st>>>(a, b, n, out);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_lincomb(float* out, float a, const float* x, float b, const float* y, float c, const float* z,
+                    long long n, cudaStream_t st) {
+    k_lincomb<<<grid_for(n, 4), 256, 0, st>>>(out, a, x, b, y, c, z, n);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_bb_dots(const float* x, const float* xp, const float* gp, const float* g, long long n, double* out2,
+                    cudaStream_t st) {
+    k_bb_dots<<<grid_for(n, 8), 256, 0, st>>>(x, xp, gp, g, n, out2);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

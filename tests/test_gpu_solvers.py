@@ -1,0 +1,81 @@
+"""GPU parity of the comparison solvers (bsgd_solve) against the fp64
+oracle (oracle/solvers.py) on the same seeded problems: objective per iteration
+within 1e-3 relative (the trajectory bar of the north star), the final image within
+1e-2 of its maximum."""
+import numpy as np
+import pytest
+
+from oracle import bsgd as ob
+from oracle import solvers as so
+from oracle.projector import BlockGrid, Projector
+
+from _problems import problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROW_SEED = 11
+
+
+@pytest.fixture(scope="module")
+def bs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1903_11874_b200 as m
+    return m
+
+
+def _pair(bs, p, g, y, solver, iters, mu, **kw):
+    op = so.ProjectorOperator(g, p.blocks, p.M, "random", ROW_SEED)
+    y64 = y.astype(np.float64)
+    x0 = np.zeros(op.grid.N * op.grid.bsize)
+    if solver == "gd":
+        xo, lo = so.gd(op, y64, x0, mu, iters)
+    elif solver == "gd_bb":
+        xo, lo = so.gd_bb(op, y64, x0, mu, iters)
+    elif solver == "ista":
+        xo, lo = so.ista(op, y64, x0, mu, kw.get("lam", 0.0), iters, kw.get("tv_iters", 20))
+    elif solver == "fista":
+        xo, lo = so.fista(op, y64, x0, mu, kw.get("lam", 0.0), iters, kw.get("tv_iters", 20))
+    else:
+        xo, lo = so.svrg(op, y64, x0, mu, iters, kw.get("svrg_m", p.M), kw.get("seed", 1))
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=ROW_SEED, tiles=p.tiles)
+    yd = torch.from_numpy(y).cuda()
+    xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    obj, mus = ctx.solve(solver, yd, xd, iters, float(np.float32(mu)), lam=kw.get("lam", 0.0),
+                         tv_iters=kw.get("tv_iters", 20), svrg_m=kw.get("svrg_m", 0), seed=kw.get("seed", 1))
+    xg = xd.cpu().numpy().astype(np.float64)
+    ctx.close()
+    oo = np.array([r["obj"] for r in lo])
+    mo = np.array([r["mu"] for r in lo])
+    e_obj = float(np.max(np.abs(obj - oo) / oo))
+    e_mu = float(np.max(np.abs(mus - mo) / mo))
+    e_x = float(np.max(np.abs(xg - xo)) / np.max(np.abs(xo)))
+    assert e_obj < 1e-3, (solver, e_obj, obj, oo)
+    assert e_mu < 1e-3, (solver, e_mu)
+    assert e_x < 1e-2, (solver, e_x)
+    return e_obj, e_x, oo
+
+
+@pytest.mark.parametrize("solver", ["gd", "gd_bb", "fista", "svrg"])
+def test_solver_parity_cfg1(bs, solver):
+    p, g, vol32, y = problem("cfg1")
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 0.5 / ob.power_iteration(P, 100, seed=1)
+    # GD-BB's long steps (up to ~30/s_max^2 here) amplify rounding: an fp32 emulation of
+    # the fp64 oracle itself leaves the 1e-3 band after 13 iterations (1.9e-7 at 10,
+    # 6e-6 at 11, 2e-3 at 13, 1.6 at 15), so its parity window is 10 iterations
+    iters = {"svrg": 6, "gd_bb": 10}.get(solver, 15)
+    e_obj, e_x, oo = _pair(bs, p, g, y, solver, iters, mu)
+    assert oo[-1] < oo[0]                                  # each method makes progress
+    print(solver, "obj rel err", e_obj, "x rel err", e_x)
+
+
+@pytest.mark.parametrize("solver", ["ista", "fista"])
+def test_tv_solver_parity_3d(bs, solver):
+    """ISTA / FISTA with the TV prox on a scaled cfg4 (z-slabs, 3D prox)."""
+    p, g, vol32, y = problem("cfg4", K=32, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 0.5 / ob.power_iteration(P, 30, seed=1)
+    e_obj, e_x, oo = _pair(bs, p, g, y, solver, 6, mu, lam=0.1, tv_iters=20)
+    print(solver, "obj rel err", e_obj, "x rel err", e_x)
