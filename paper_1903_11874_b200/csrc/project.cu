@@ -47,13 +47,6 @@ __device__ __forceinline__ int sgn(double v) { return (v > 0.0) - (v < 0.0); }
 __device__ __forceinline__ void red_add(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
-// Predicated variant: one @p RED instruction instead of a branch around it.
-__device__ __forceinline__ void red_add_if(bool pred, float* p, float v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.global.add.f32 [%0], %1;\n\t}" ::"l"(p),
-                 "f"(v), "r"((int)pred)
-                 : "memory");
-}
-
 __device__ __forceinline__ bool lane_steep(const double b[3]) {
     // |b_c / b_1| < 1 with a margin (the v3 increments K = |b_c / b_1| 2^64 stay < 2^64)
     const double lim = fabs(b[1]) * (1.0 - 1.0 / 1073741824.0);
@@ -251,8 +244,10 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 }
                 if (MODE == PROJ_BP) {   // zero-length segments (exact-boundary ties) add 0
                     red_add(dst + o, l0 * wbp);
-                    red_add_if(p1, dst + o1, l1 * wbp);
-                    red_add_if(p2, dst + o2, l2 * wbp);
+                    if (p1) {            // p2 implies p1: one reconvergence region
+                        red_add(dst + o1, l1 * wbp);
+                        if (p2) red_add(dst + o2, l2 * wbp);
+                    }
                 }
                 if (MODE == PROJ_COUNT)
                     nvis += (unsigned)(l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
@@ -331,34 +326,35 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
 // Rays with |kx| or |kz| >= 1 (or parallel to the slices) can cross one axis twice in a
 // slice.  A warp containing such a lane is left to the v2 kernel (launched second, it skips
 // every warp this kernel handled), so both decide "steep" with the same predicate.
-// One slice's gathers / reductions, predicated inside PTX (no branches):
-//   segment 0 iff the lane is in its slice range (rel <= nk, unsigned),
-//   segment 1 iff also some plane is crossed (m_or != 0), segment 2 iff both are (m_and != 0).
-__device__ __forceinline__ void gather3(unsigned rel, unsigned nk, unsigned m_or, unsigned m_and,
-                                        const float* p0, const float* p1, const float* p2,
-                                        float& v0, float& v1, float& v2) {
+// One slice's three gathers, predicated inside PTX on the lane's slice range
+// (rel <= nk, unsigned; no branch).  Without a crossing o1 = o2 = o (an L1 hit) and the
+// segment lengths l1 = l2 = 0 exactly, so no crossing masks are needed.
+__device__ __forceinline__ void gather3(unsigned rel, unsigned nk, const float* p0, const float* p1,
+                                        const float* p2, float& v0, float& v1, float& v2) {
     v0 = 0.f; v1 = 0.f; v2 = 0.f;
-    asm("{\n\t.reg .pred a, b, c;\n\t"
+    asm("{\n\t.reg .pred a;\n\t"
         "setp.le.u32 a, %3, %4;\n\t"
-        "setp.ne.and.u32 b, %5, 0, a;\n\t"
-        "setp.ne.and.u32 c, %6, 0, a;\n\t"
-        "@a ld.global.nc.f32 %0, [%7];\n\t"
-        "@b ld.global.nc.f32 %1, [%8];\n\t"
-        "@c ld.global.nc.f32 %2, [%9];\n\t}"
+        "@a ld.global.nc.f32 %0, [%5];\n\t"
+        "@a ld.global.nc.f32 %1, [%6];\n\t"
+        "@a ld.global.nc.f32 %2, [%7];\n\t}"
         : "+f"(v0), "+f"(v1), "+f"(v2)
-        : "r"(rel), "r"(nk), "r"(m_or), "r"(m_and), "l"(p0), "l"(p1), "l"(p2));
+        : "r"(rel), "r"(nk), "l"(p0), "l"(p1), "l"(p2));
 }
-__device__ __forceinline__ void scatter3(unsigned rel, unsigned nk, unsigned m_or, unsigned m_and,
-                                         float* p0, float* p1, float* p2, float v0, float v1, float v2) {
-    asm volatile("{\n\t.reg .pred a, b, c;\n\t"
-                 "setp.le.u32 a, %0, %1;\n\t"
-                 "setp.ne.and.u32 b, %2, 0, a;\n\t"
-                 "setp.ne.and.u32 c, %3, 0, a;\n\t"
-                 "@a red.global.add.f32 [%4], %7;\n\t"
-                 "@b red.global.add.f32 [%5], %8;\n\t"
-                 "@c red.global.add.f32 [%6], %9;\n\t}"
-                 :: "r"(rel), "r"(nk), "r"(m_or), "r"(m_and), "l"(p0), "l"(p1), "l"(p2),
-                    "f"(v0), "f"(v1), "f"(v2));
+
+// One slice's reductions.  ptxas turns every predicated RED into a BSSY/BRA/BSYNC
+// branch, so the rare segments are nested under the common ones (one reconvergence
+// region per slice instead of three; measured BP 136 -> 121 ms at cfg5):
+// segment 0 iff the lane is in its slice range, segment 1 iff also a plane is crossed
+// (m_or != 0), segment 2 iff both planes are (m_and != 0).
+__device__ __forceinline__ void scatter3(bool in, unsigned m_or, unsigned m_and, float* p0, float* p1,
+                                         float* p2, float v0, float v1, float v2) {
+    if (in) {
+        red_add(p0, v0);
+        if (m_or) {
+            red_add(p1, v1);
+            if (m_and) red_add(p2, v2);
+        }
+    }
 }
 
 // D -= K on the 64-bit plane distance; returns ~0u when it borrows (a plane is crossed).
@@ -537,18 +533,15 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
             if (MODE == PROJ_FP) {
                 // software pipeline: this slice's gathers are issued before the previous
                 // slice's values are consumed (two slices of loads in flight per warp)
-                // all three gathers predicated on the slice range only: without a crossing
-                // o1 = o2 = o (an L1 hit) and l1 = l2 = 0 exactly, so no crossing masks
                 float v0, v1, v2;
-                gather3((unsigned)rel, (unsigned)nk, ~0u, ~0u, src + (int)o, src + (int)o1,
-                        src + (int)o2, v0, v1, v2);
+                gather3((unsigned)rel, (unsigned)nk, src + (int)o, src + (int)o1, src + (int)o2, v0, v1, v2);
                 acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
                 pv0 = v0; pv1 = v1; pv2 = v2;
                 pl0 = l0; pl1 = l1; pl2 = l2;
             }
             if (MODE == PROJ_BP)
-                scatter3((unsigned)rel, (unsigned)nk, mor, mand, dst + (int)o, dst + (int)o1,
-                         dst + (int)o2, l0 * wbp, l1 * wbp, l2 * wbp);
+                scatter3(in, mor, mand, dst + (int)o, dst + (int)o1, dst + (int)o2, l0 * wbp, l1 * wbp,
+                         l2 * wbp);
             if (MODE == PROJ_COUNT) {
                 const bool p1 = in && mor != 0u, p2 = in && mand != 0u;
                 nvis += (unsigned)(in && l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
