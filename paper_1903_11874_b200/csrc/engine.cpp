@@ -130,14 +130,20 @@ struct bsgd_ctx_s {
         if (zero) BSGD_CUDA(cudaMemset(p, 0, sizeof(T) * (size_t)count));
         return p;
     }
-    // Image buffers the projector reads or scatters into carry `slack` zeroed floats on both
-    // sides: a ray leaving the box can take one rounding-induced step past a face with a
-    // ~1e-9-voxel segment; the kernel does not test for it, the slack keeps it in memory.
-    long long slack = 0;
-    float* dnew_slack(long long count) {
-        float* p = dnew<float>(count + 2 * slack);
+    // Image buffers the projector reads or scatters into are PADDED copies (BlockDesc):
+    // per block, rows carry PAD_X zero floats on each side and PAD_Z zero planes bound the
+    // block, so a traversal step up to one cell past a row / plane face reads 0 (FP) or lands
+    // in the ignored border (BP).  That lets the FP/BP slice loop skip entry/exit clamping.
+    // Each whole buffer also carries `slack` zeroed floats on both sides (v2's L1 prefetch
+    // lead).  pN / pT give the interior origin of owned block b.
+    int rowN = 0, planeN = 0, rowT = 0, planeT = 0;
+    long long padN = 0, padT = 0, orgN = 0, orgT = 0, slack = 0;
+    float* dnew_pad(int nblocks, bool transposed) {
+        float* p = dnew<float>((long long)nblocks * (transposed ? padT : padN) + 2 * slack);
         return p + slack;
     }
+    float* pN(float* base, long long b) const { return base + b * padN + orgN; }
+    float* pT(float* base, long long b) const { return base + b * padT + orgT; }
     void release() {
         for (auto& b : bufs) {
             if (alloc.free) alloc.free(b.p, b.bytes, nullptr, alloc.user);
@@ -249,6 +255,7 @@ struct bsgd_ctx_s {
             d.outN = oN.empty() ? nullptr : oN[b];
             d.outT = oT.empty() ? nullptr : oT[b];
             d.z = zout.empty() ? nullptr : zout[b];
+            d.rowN = rowN; d.planeN = planeN; d.rowT = rowT; d.planeT = planeT;
         }
         std::vector<int4> rc = rects;
         int maxr = 0;
@@ -305,13 +312,14 @@ struct bsgd_ctx_s {
                 int ghat_i = 0, float* xN_ = nullptr) {
         UpdLaunch U;
         U.bd[0] = bd[0]; U.bd[1] = bd[1]; U.bd[2] = bd[2];
-        U.accN = accN_ ? accN_ : accN + b * bsize;
-        U.accT = accT_ ? accT_ : accT + b * bsize;
+        U.rowN = rowN; U.planeN = planeN; U.rowT = rowT; U.planeT = planeT;
+        U.accN = accN_ ? accN_ : pN(accN, b);
+        U.accT = accT_ ? accT_ : pT(accT, b);
         U.ghat = ghat ? ghat_of(ghat_i, b) : nullptr;
         U.g = g + b * bsize;
         U.x = x;
-        U.xT = xT_ ? xT_ : xT + b * bsize;
-        U.xN = xN_ ? xN_ : (xT_ ? nullptr : xN + b * bsize);
+        U.xT = xT_ ? xT_ : pT(xT, b);
+        U.xN = xN_ ? xN_ : (xT_ ? nullptr : pN(xN, b));
         U.out = out;
         U.mu = mu_;
         U.final_ = final_;
@@ -370,8 +378,8 @@ struct bsgd_ctx_s {
             std::vector<float*> zs;
             for (int b = 0; b < nb; ++b) {
                 for (int vs = 0; vs < V; ++vs) rc[(size_t)b * V + vs] = rect_for(b, vs);
-                xs.push_back(xN + oslots[b] * bsize);
-                xts.push_back(xT + oslots[b] * bsize);
+                xs.push_back(pN(xN, oslots[b]));
+                xts.push_back(pT(xT, oslots[b]));
                 zs.push_back(z + oslots[b] * n_rays);
             }
             project(PROJ_FP, vsel, oslots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
@@ -414,8 +422,8 @@ struct bsgd_ctx_s {
         std::vector<float*> oN, oT;
         std::vector<const float*> none;
         for (int b = 0; b < nb; ++b) {
-            oN.push_back(accN + oslots[b] * bsize);
-            oT.push_back(accT + oslots[b] * bsize);
+            oN.push_back(pN(accN, oslots[b]));
+            oT.push_back(pT(accT, oslots[b]));
         }
         if (sgd) {   // Eq. 4: g = 2 A_I^T r_I over all selected rows, no memory
             std::vector<int4> rc((size_t)nb * V, make_int4(0, nu, 0, nv));
@@ -558,8 +566,8 @@ struct bsgd_ctx_s {
             std::vector<const float*> xs, xts;
             std::vector<float*> zs;
             for (int b = 0; b < s; ++b) {
-                xs.push_back(xN + b * bsize);
-                xts.push_back(xT + b * bsize);
+                xs.push_back(pN(xN, b));
+                xts.push_back(pT(xT, b));
                 zs.push_back(z + b * n_rays);
             }
             project(PROJ_FP, vsel, slots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
@@ -596,8 +604,8 @@ struct bsgd_ctx_s {
         std::vector<float*> oN, oT;
         std::vector<const float*> none;
         for (int b = 0; b < s; ++b) {
-            oN.push_back(accN + b * bsize);
-            oT.push_back(accT + b * bsize);
+            oN.push_back(pN(accN, b));
+            oT.push_back(pT(accT, b));
         }
         project(PROJ_BP, vsel, slots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
         for (int b = 0; b < s; ++b) update(UPD_OUT, b, p + b * bsize, 0.f, 1, gout + b * bsize, 0, st);
@@ -952,15 +960,25 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         const long long sb = (long long)c->s * c->bsize;
         c->d_vecs = c->dnew<double>(12LL * c->n_views, false);
         BSGD_CUDA(cudaMemcpy(c->d_vecs, c->vecs.data(), sizeof(double) * c->vecs.size(), cudaMemcpyHostToDevice));
-        c->slack = (((long long)c->bd[0] * c->bd[1] + 64 + 63) / 64) * 64;
-        c->xT = c->dnew_slack(sb);
-        c->xN = c->dnew_slack(sb);
+        c->rowN = c->bd[0] + 2 * PAD_X;
+        c->planeN = c->rowN * c->bd[1];
+        c->rowT = c->bd[1] + 2 * PAD_X;
+        c->planeT = c->rowT * c->bd[0];
+        c->padN = (long long)c->planeN * (c->bd[2] + 2 * PAD_Z);
+        c->padT = (long long)c->planeT * (c->bd[2] + 2 * PAD_Z);
+        c->orgN = (long long)PAD_Z * c->planeN + PAD_X;
+        c->orgT = (long long)PAD_Z * c->planeT + PAD_X;
+        if (c->padN >= (1LL << 31) || c->padT >= (1LL << 31))
+            fail(BSGD_E_PARTITION, "a padded block must hold < 2^31 voxels (32-bit offsets)");
+        c->slack = (((long long)std::max(c->planeN, c->planeT) + 64 + 63) / 64) * 64;
+        c->xT = c->dnew_pad(c->s, true);
+        c->xN = c->dnew_pad(c->s, false);
         c->g = c->dnew<float>(sb);
         c->ghat = c->dnew<float>((long long)c->M * sb);
         c->z = c->dnew<float>((long long)c->s * c->n_rays);
         c->r = c->dnew<float>(c->n_rays);
-        c->accN = c->dnew_slack(sb);
-        c->accT = c->dnew_slack(sb);
+        c->accN = c->dnew_pad(c->s, false);
+        c->accT = c->dnew_pad(c->s, true);
         if (const char* e = getenv("BSGD_FORCE_NCCL")) c->coll = atoi(e) != 0;   // test hook
         if (c->world > 1) c->coll = true;
         c->pc = c->coll ? c->dnew<float>(c->n_rays) : nullptr;
@@ -1026,8 +1044,8 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
         if (!c->owned(col_block)) fail(BSGD_E_DIMENSION, "column block not owned by this rank");
         if (n == 0) return;
         if (!c->fp_scratchT) {
-            c->fp_scratchT = c->dnew_slack(c->bsize);
-            c->fp_scratchN = c->dnew_slack(c->bsize);
+            c->fp_scratchT = c->pT(c->dnew_pad(1, true), 0);
+            c->fp_scratchN = c->pN(c->dnew_pad(1, false), 0);
         }
         const int b = col_block - c->first;
         cudaStream_t st = S(stream);
@@ -1067,8 +1085,8 @@ bsgd_status bsgd_back(bsgd_ctx c, int32_t n, const int32_t* views, const int32_t
         std::vector<int4> rc;
         if (rects)
             for (int k = 0; k < n; ++k) rc.push_back(make_int4(rects[4 * k], rects[4 * k + 1], rects[4 * k + 2], rects[4 * k + 3]));
-        float* aN = c->accN + b * c->bsize;
-        float* aT = c->accT + b * c->bsize;
+        float* aN = c->pN(c->accN, b);
+        float* aT = c->pT(c->accT, b);
         if (n > 0) c->project(PROJ_BP, vv, {b}, rc, {}, {}, {aN}, {aT}, {}, proj, scale, 0, st, 0);
         c->update(UPD_OUT, b, nullptr, 0.f, 0, g_block, accumulate, st);
     });
@@ -1395,8 +1413,8 @@ bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, doubl
         const long long sb = (long long)c->s * c->bsize;
         if (!c->pw_v) {
             c->pw_v = c->dnew<float>(sb, false);
-            c->pw_vT = c->dnew_slack(sb);
-            c->pw_vN = c->dnew_slack(sb);
+            c->pw_vT = c->dnew_pad(c->s, true);
+            c->pw_vN = c->dnew_pad(c->s, false);
             c->pw_proj = c->dnew<float>(c->n_rays, false);
         }
         launch_fill_random(c->pw_v, sb, seed + 1000003ull * (uint64_t)c->rank, st);
@@ -1411,13 +1429,13 @@ bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, doubl
             BSGD_CUDA(cudaMemsetAsync(c->pw_proj, 0, sizeof(float) * c->n_rays, st));
             for (int b = 0; b < c->s; ++b) {
                 c->update(UPD_XT, b, c->pw_v + b * c->bsize, 0.f, 1, nullptr, 0, st, nullptr, nullptr,
-                          c->pw_vT + b * c->bsize, 0, c->pw_vN + b * c->bsize);
-                c->project(PROJ_FP, all, {b}, {}, {c->pw_vN + b * c->bsize}, {c->pw_vT + b * c->bsize}, {}, {},
+                          c->pT(c->pw_vT, b), 0, c->pN(c->pw_vN, b));
+                c->project(PROJ_FP, all, {b}, {}, {c->pN(c->pw_vN, b)}, {c->pT(c->pw_vT, b)}, {}, {},
                            {c->pw_proj}, nullptr, 0.f, 1, st, 0);
             }
             c->allreduce_f(c->pw_proj, c->n_rays, st);
             for (int b = 0; b < c->s; ++b) {
-                c->project(PROJ_BP, all, {b}, {}, {}, {}, {c->accN + b * c->bsize}, {c->accT + b * c->bsize}, {},
+                c->project(PROJ_BP, all, {b}, {}, {}, {}, {c->pN(c->accN, b)}, {c->pT(c->accT, b)}, {},
                            c->pw_proj, 1.f, 0, st, 0);
                 c->update(UPD_OUT, b, nullptr, 0.f, 0, c->pw_v + b * c->bsize, 0, st);
             }

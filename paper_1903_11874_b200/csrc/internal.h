@@ -52,7 +52,16 @@ struct BlockDesc {
     float* z;            // FP target, full-length projection vector
     int lo[3], hi[3];    // box in grid coordinates
     int band_lo;         // first detector-row band with work for this block
+    // Strides of the library's PADDED image copies (xN/xT, outN/outT point at voxel (0,0,0)
+    // of the block interior): every row carries PAD_X zero floats on each side and every
+    // block PAD_Z zero planes below and above, so a traversal step up to one cell outside
+    // the block in the row or plane direction reads 0 (FP) / lands in the ignored border
+    // (BP).  Normal layout [z][y][x]: row = bx + 2 PAD_X, plane = row * by; transposed
+    // [z][x][y]: row = by + 2 PAD_X, plane = row * bx.
+    int rowN, planeN, rowT, planeT;
 };
+constexpr int PAD_X = 4;   // keeps float4 alignment of the interior rows
+constexpr int PAD_Z = 1;
 
 struct ProjLaunch {
     KGeom g;
@@ -79,13 +88,14 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st);
 enum { UPD_BSGD = 0, UPD_SGD = 1, UPD_OUT = 2, UPD_XT = 3, UPD_SGD_ACC = 4 };
 struct UpdLaunch {
     int bd[3];            // block dims (x, y, z)
-    float* accN;          // normal-layout BP accumulator (zeroed after reading)
-    float* accT;          // transposed-layout BP accumulator (zeroed after reading)
+    int rowN, planeN, rowT, planeT;   // padded strides of accN / xN and accT / xT (see BlockDesc)
+    float* accN;          // normal-layout BP accumulator, padded (interior zeroed after reading)
+    float* accT;          // transposed-layout BP accumulator, padded (interior zeroed after reading)
     float* ghat;          // g_hat^i_J (UPD_BSGD)
     float* g;             // g_J
     float* x;             // x_J (normal layout)
-    float* xT;            // x_J transposed (written when x changes / UPD_XT)
-    float* xN;            // x_J copy in the library's slack-padded buffer (FP source)
+    float* xT;            // x_J transposed, padded (written when x changes / UPD_XT)
+    float* xN;            // x_J copy, padded (FP source)
     float* out;           // UPD_OUT target
     float mu;
     int final_;           // apply x += mu g and refresh xT

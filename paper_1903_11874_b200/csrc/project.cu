@@ -146,8 +146,9 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
         int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
         q = hi[0]; hi[0] = hi[1]; hi[1] = q;
     }
-    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1];
-    const unsigned plane = (unsigned)bdx * (unsigned)bdy;
+    // strides of the padded copy of the frame's layout (BlockDesc)
+    const int bdx = mainX ? B.rowT : B.rowN;
+    const unsigned plane = (unsigned)(mainX ? B.planeT : B.planeN);
     double inv[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
@@ -426,8 +427,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     const float* __restrict__ src = mainX ? B.xT : B.xN;
     float* dst = mainX ? B.outT : B.outN;
 
-    const int bdx = hi[0] - lo[0], bdy = hi[1] - lo[1];
-    const int plane = bdx * bdy;
+    // strides of the padded copy of the frame's layout (BlockDesc): rows carry PAD_X and
+    // the block PAD_Z zero cells beyond every face the slice walk can step through
+    const int bdx = mainX ? B.rowT : B.rowN;
+    const int plane = mainX ? B.planeT : B.planeN;
     const int sy = (b[1] > 0.0) ? 1 : -1;
     const double ainv1 = fabs(inv[1]);
     const double TWO64 = 18446744073709551616.0;
@@ -485,7 +488,6 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     }
     const int rowstep = sy * bdx;
     const unsigned nsxo = (unsigned)(-sxo), npstep = (unsigned)(-pstep);
-    const float shm1 = shi_last - 1.f;
     const float wbp = Ls * rs;   // BP weight per unit of main-axis travel
     double acc = 0.0;
     float acc32 = 0.f;
@@ -497,34 +499,40 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         if (jl > jh) continue;                                      // warp-uniform
         const int nsl = jh - jl + 1;
         const int kb = (pass == 0 ? pos : neg) ? k0 : INT_MAX;      // this lane's slices [kb, kb + nk]
-        // float copies of rel = k - kb and rel - nk (exact integers): the first / last slice
-        // flags come from FFMA.SAT on the FMA pipe (sat(1 - r^2) = [r == 0]) instead of
-        // compare + select on the ALU pipe, which binds this loop
-        float fr = (float)max(-kb, -(1 << 23)), fe = fr - (float)nk;
         for (int k = 0; k < nsl; ++k) {
             const int rel = k - kb;
             const bool in = (unsigned)rel <= (unsigned)nk;
-            float sl, sh;
-            if (MODE == PROJ_BP) {   // BP is ALU-bound: flags on the FMA pipe
-                sl = slo * __saturatef(fmaf(-fr, fr, 1.f));
-                sh = fmaf(__saturatef(fmaf(-fe, fe, 1.f)), shm1, 1.f);
-                fr += 1.f;
-                fe += 1.f;
-            } else {                 // FP is issue-bound: fewer instructions
-                sl = rel == 0 ? slo : 0.f;
-                sh = rel == nk ? shi_last : 1.f;
-            }
             // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
-            // plane distance borrows; u = 2 (beyond sh) otherwise
+            // plane distance borrows
             const float fx = __ull2float_rn(DX) * ikx;
             const unsigned bx = sub_borrow(DX, KX);                 // ~0u on a plane crossing
-            const float ux = bx ? fx : 2.f;
             const float fz = __ull2float_rn(DZ) * ikz;
             const unsigned bz = sub_borrow(DZ, KZ);
-            const float uz = bz ? fz : 2.f;
-            const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
-            const float c1 = fminf(fmaxf(m1, sl), sh), c2 = fminf(fmaxf(m2, sl), sh);
-            const float l0 = c1 - sl, l1 = c2 - c1, l2 = sh - c2;
+            float l0, l1, l2, ux, uz;
+            if (MODE == PROJ_COUNT) {
+                // exact in-block segments: the slice clamped to [s_lo, s_hi] at the lane's
+                // first / last slice (entry / exit through an x or z face or the far face)
+                const float sl = rel == 0 ? slo : 0.f;
+                const float sh = rel == nk ? shi_last : 1.f;
+                ux = bx ? fx : 2.f;
+                uz = bz ? fz : 2.f;
+                const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
+                const float c1 = fminf(fmaxf(m1, sl), sh), c2 = fminf(fmaxf(m2, sl), sh);
+                l0 = c1 - sl;
+                l1 = c2 - c1;
+                l2 = sh - c2;
+            } else {
+                // FP / BP take the whole slice: where the ray enters or leaves inside a slice
+                // (through an x or z face) the part outside the block lies in the cell just
+                // beyond that face, i.e. in the padded copy's zero border (FP reads 0, BP's
+                // reduction lands in the ignored border), so no entry/exit clamping
+                ux = bx ? __saturatef(fx) : 1.f;
+                uz = bz ? __saturatef(fz) : 1.f;
+                const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
+                l0 = m1;
+                l1 = m2 - m1;
+                l2 = 1.f - m2;
+            }
             // bx, bz are 0 or ~0u (= -1): the steps as multiply-adds (FMA pipe)
             const unsigned dox = bx * nsxo, doz = bz * npstep;
             const unsigned o1 = o + (ux <= uz ? dox : doz);

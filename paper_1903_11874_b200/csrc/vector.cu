@@ -48,12 +48,14 @@ __global__ void __launch_bounds__(256) k_block_update4(const UpdLaunch U) {
     const bool writes_x = (MODE == UPD_XT) || ((MODE == UPD_BSGD || MODE == UPD_SGD) && final_);
     const bool needs_x = (MODE == UPD_BSGD && final_) || MODE == UPD_SGD || MODE == UPD_XT;
     const long long in_ = zoff + (long long)(y0 + r) * bdx + x0 + 4 * q;     // normal layout
-    const long long it_ = zoff + (long long)(x0 + r) * bdy + y0 + 4 * q;     // transposed layout
+    // the padded copies (accN / xN normal, accT / xT transposed; see BlockDesc)
+    const long long inP = (long long)blockIdx.z * U.planeN + (long long)(y0 + r) * U.rowN + x0 + 4 * q;
+    const long long itP = (long long)blockIdx.z * U.planeT + (long long)(x0 + r) * U.rowT + y0 + 4 * q;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 vT = z4, vN = z4, vgh = z4, vg = z4, vx = z4, vo = z4;
     if (use_acc) {
-        vT = *reinterpret_cast<const float4*>(U.accT + it_);
-        vN = *reinterpret_cast<const float4*>(U.accN + in_);
+        vT = *reinterpret_cast<const float4*>(U.accT + itP);
+        vN = *reinterpret_cast<const float4*>(U.accN + inP);
     }
     if (MODE == UPD_BSGD) {
         vgh = *reinterpret_cast<const float4*>(U.ghat + in_);
@@ -63,8 +65,8 @@ __global__ void __launch_bounds__(256) k_block_update4(const UpdLaunch U) {
     if (MODE == UPD_OUT && U.accumulate) vo = *reinterpret_cast<const float4*>(U.out + in_);
     if (use_acc) {
         tT[r][4 * q + 0] = vT.x; tT[r][4 * q + 1] = vT.y; tT[r][4 * q + 2] = vT.z; tT[r][4 * q + 3] = vT.w;
-        *reinterpret_cast<float4*>(U.accT + it_) = z4;
-        *reinterpret_cast<float4*>(U.accN + in_) = z4;
+        *reinterpret_cast<float4*>(U.accT + itP) = z4;
+        *reinterpret_cast<float4*>(U.accN + inP) = z4;
     }
     __syncthreads();
     float nv[4] = {vN.x, vN.y, vN.z, vN.w};
@@ -103,9 +105,9 @@ __global__ void __launch_bounds__(256) k_block_update4(const UpdLaunch U) {
         *reinterpret_cast<float4*>(U.out + in_) = make_float4(ng[0], ng[1], ng[2], ng[3]);
     }
     if (!writes_x) return;
-    if (U.xN) *reinterpret_cast<float4*>(U.xN + in_) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+    if (U.xN) *reinterpret_cast<float4*>(U.xN + inP) = make_float4(nx[0], nx[1], nx[2], nx[3]);
     __syncthreads();
-    *reinterpret_cast<float4*>(U.xT + it_) =
+    *reinterpret_cast<float4*>(U.xT + itP) =
         make_float4(tX[r][4 * q + 0], tX[r][4 * q + 1], tX[r][4 * q + 2], tX[r][4 * q + 3]);
 }
 
@@ -132,20 +134,21 @@ __global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U) {
     float* __restrict__ out = U.out;
     float vT[4], vN[4], vgh[4], vg[4], vx[4], vo[4];
     bool okT[4], ok[4];
-    long long iT[4], idx[4];
+    long long iT[4], idx[4], iP[4];   // iT: padded transposed; idx: plain normal; iP: padded normal
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int xxT = x0 + ty + 8 * k, yyT = y0 + tx;
         okT[k] = xxT < bdx && yyT < bdy;
-        iT[k] = zoff + (long long)xxT * bdy + yyT;
+        iT[k] = (long long)blockIdx.z * U.planeT + (long long)xxT * U.rowT + yyT;
         const int xx = x0 + tx, yy = y0 + ty + 8 * k;
         ok[k] = xx < bdx && yy < bdy;
         idx[k] = zoff + (long long)yy * bdx + xx;
+        iP[k] = (long long)blockIdx.z * U.planeN + (long long)yy * U.rowN + xx;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         vT[k] = (use_acc && okT[k]) ? accT[iT[k]] : 0.f;
-        vN[k] = (use_acc && ok[k]) ? accN[idx[k]] : 0.f;
+        vN[k] = (use_acc && ok[k]) ? accN[iP[k]] : 0.f;
         vgh[k] = (MODE == UPD_BSGD && ok[k]) ? ghat[idx[k]] : 0.f;
         vg[k] = (MODE == UPD_BSGD && ok[k]) ? g[idx[k]] : 0.f;
         vx[k] = (((MODE == UPD_BSGD && final_) || MODE == UPD_SGD || MODE == UPD_XT) && ok[k]) ? x[idx[k]] : 0.f;
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U) {
         if (ok[k]) {
             const long long i = idx[k];
             const float nv = use_acc ? vN[k] + tT[tx][ty + 8 * k] : 0.f;
-            if (use_acc) accN[i] = 0.f;
+            if (use_acc) accN[iP[k]] = 0.f;
             if (MODE == UPD_BSGD) {
                 ghat[i] = nv;
                 const float gv = vg[k] + (nv - vgh[k]);
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U) {
             } else if (MODE == UPD_XT) {
                 xv = vx[k];
             }
-            if (writes_x && U.xN) U.xN[i] = xv;
+            if (writes_x && U.xN) U.xN[iP[k]] = xv;
         }
         tX[ty + 8 * k][tx] = xv;
     }
