@@ -330,15 +330,16 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
 // One slice's three gathers, predicated inside PTX on the lane's slice range
 // (rel <= nk, unsigned; no branch).  Without a crossing o1 = o2 = o (an L1 hit) and the
 // segment lengths l1 = l2 = 0 exactly, so no crossing masks are needed.
+// Outside the range the outputs are left unwritten (undefined): the caller discards the
+// slice's contribution with a select on the same predicate (no zero-initialisation).
 __device__ __forceinline__ void gather3(unsigned rel, unsigned nk, const float* p0, const float* p1,
                                         const float* p2, float& v0, float& v1, float& v2) {
-    v0 = 0.f; v1 = 0.f; v2 = 0.f;
     asm("{\n\t.reg .pred a;\n\t"
         "setp.le.u32 a, %3, %4;\n\t"
         "@a ld.global.nc.f32 %0, [%5];\n\t"
         "@a ld.global.nc.f32 %1, [%6];\n\t"
         "@a ld.global.nc.f32 %2, [%7];\n\t}"
-        : "+f"(v0), "+f"(v1), "+f"(v2)
+        : "=f"(v0), "=f"(v1), "=f"(v2)
         : "r"(rel), "r"(nk), "l"(p0), "l"(p1), "l"(p2));
 }
 
@@ -492,6 +493,7 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     double acc = 0.0;
     float acc32 = 0.f;
     float pv0 = 0.f, pv1 = 0.f, pv2 = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f;   // FP: previous slice
+    bool pin = false;                                                          // ... and its range flag
     unsigned int nvis = 0;
 
     for (int pass = 0; pass < 2; ++pass) {
@@ -543,9 +545,11 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
                 // slice's values are consumed (two slices of loads in flight per warp)
                 float v0, v1, v2;
                 gather3((unsigned)rel, (unsigned)nk, src + (int)o, src + (int)o1, src + (int)o2, v0, v1, v2);
-                acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
+                const float an = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
+                acc32 = pin ? an : acc32;            // the previous slice was in range
                 pv0 = v0; pv1 = v1; pv2 = v2;
                 pl0 = l0; pl1 = l1; pl2 = l2;
+                pin = in;
             }
             if (MODE == PROJ_BP)
                 scatter3(in, mor, mand, dst + (int)o, dst + (int)o1, dst + (int)o2, l0 * wbp, l1 * wbp,
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         }
     }
     if (MODE == PROJ_FP && inrect) {
-        acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
+        if (pin) acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
         acc += (double)acc32;
         acc *= (double)Ls;                  // main-axis units -> voxel lengths
         float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
