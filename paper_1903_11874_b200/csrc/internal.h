@@ -60,7 +60,7 @@ struct BlockDesc {
     // [z][x][y]: row = by + 2 PAD_X, plane = row * bx.
     int rowN, planeN, rowT, planeT;
 };
-constexpr int PAD_X = 4;   // keeps float4 alignment of the interior rows
+constexpr int PAD_X = 32;  // keeps padded rows and their interiors 128-byte aligned (bx % 32 == 0)
 constexpr int PAD_Z = 1;
 
 struct ProjLaunch {
