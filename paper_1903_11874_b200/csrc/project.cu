@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     const int rowstep = sy * bdx;
     const int pf_off = (L.pf_rows - 1) * rowstep;   // FP prefetch lead (rows beyond the next slice)
     const float wbp = (float)blen * rs;   // BP weight per unit t: |b| * scale * r_ray
+    const float cthr = (float)(1e-6 / blen);   // COUNT: segments above 1e-6 voxel (see v3)
     double acc = 0.0;
     float acc32 = 0.f;
     unsigned int nvis = 0;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                     }
                 }
                 if (MODE == PROJ_COUNT)
-                    nvis += (unsigned)(l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
+                    nvis += (unsigned)(l0 > cthr) + (unsigned)(p1 && l1 > cthr) + (unsigned)(p2 && l2 > cthr);
                 if (!more) {
                     o = o2;
                     if (cx) tx = ntx;
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                             const float len = (float)(tn - tt);   // t units (see above)
                             if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
                             if (MODE == PROJ_BP) red_add(dst + o, len * wbp);
-                            if (MODE == PROJ_COUNT) ++nvis;
+                            if (MODE == PROJ_COUNT && len > cthr) ++nvis;
                             tt = tn;
                         }
                         if (tx <= tz) {
@@ -556,7 +557,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
                          l2 * wbp);
             if (MODE == PROJ_COUNT) {
                 const bool p1 = in && mor != 0u, p2 = in && mand != 0u;
-                nvis += (unsigned)(in && l0 > 0.f) + (unsigned)(p1 && l1 > 0.f) + (unsigned)(p2 && l2 > 0.f);
+                // a segment counts when longer than 1e-6 of the slice: exact ties (a ray through
+                // a voxel edge) leave rounding slivers of ~1e-7 that the oracle's exact
+                // arithmetic gives as 0 (its zero-length gaps are dropped, reading A18)
+                nvis += (unsigned)(in && l0 > 1e-6f) + (unsigned)(p1 && l1 > 1e-6f) + (unsigned)(p2 && l2 > 1e-6f);
             }
             o = o2 + (unsigned)rowstep;
             if (MODE == PROJ_FP && (k & 15) == 15) {               // warp-uniform

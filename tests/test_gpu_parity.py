@@ -139,6 +139,32 @@ def test_operator_parity_laminography_octants(bs, tilt):
     _fp_bp_check(bs, g, (2, 2, 2), 4, np.arange(16), range(8))
 
 
+@pytest.mark.parametrize("name,kw", [("cfg1", {}), ("cfg3", dict(K=64, n_views=40))])
+def test_visit_counts(bs, name, kw):
+    """The visit table behind the intersections/s metric (COUNT traversal: in-block
+    segments longer than 1e-6 of a slice) against the oracle's a_ij over the epoch's
+    selected (row block, column block) pairs.  At exact ties (rays through voxel edges)
+    both sides produce rounding slivers (~1e-7 in fp32, ~1e-15 in fp64) whose count is
+    arbitrary, so the unique quantity compared is the number of entries longer than
+    1.2e-6 voxel (1e-6 slice x |b|/|b_main| in [1, 1.73] is the GPU's cut): |d| <= 2."""
+    p = synth.PRESETS[name]
+    if kw:
+        p = synth.scaled(p, **kw)
+    g = p.geometry()
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=5)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    y = torch.zeros(g.n_rays, device="cuda")
+    x = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    res = ctx.run(y, x, epochs=3, mu0=1e-6, seed=9, rows_per_epoch=1, cols_per_epoch=2)
+    parts = ob.view_partition(g.n_views, p.M, "random", 5)
+    for e in range(3):
+        views = [v for i in res.sel_rows[e] for v in parts[i]]
+        want = sum(int(np.count_nonzero(P.csr(views, int(j)).data > 1.2e-6)) for j in res.sel_cols[e])
+        got = int(res.visits[e])
+        assert abs(got - want) <= 2, (e, got, want)
+    ctx.close()
+
+
 def test_im_table(bs):
     """Ones-pass block masses vs the oracle's traced masses; integer table bit-exact."""
     for name, kw in [("cfg2", {}), ("cfg3", dict(K=64, n_views=40))]:
