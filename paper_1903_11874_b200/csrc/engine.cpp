@@ -81,6 +81,17 @@ struct bsgd_ctx_s {
     float *y_dev = nullptr, *x_dev = nullptr, *xt_dev = nullptr;
     float *sv_a = nullptr, *sv_b = nullptr, *sv_c = nullptr, *sv_d = nullptr, *y_zero = nullptr;   // solvers
     double* d_normsq = nullptr;
+    double* d_normsq0 = nullptr;         // ||y_I||^2 of a deferred reset (host-buffer runs)
+    cudaStream_t copy_st = nullptr;      // H2D uploads of host-buffer runs
+    std::vector<cudaEvent_t> x_events;
+    std::vector<cudaEvent_t> up_ev;      // [s] x blocks, [s] y, [s + 1] start
+    void ensure_copy_stream() {
+        if (copy_st) return;
+        BSGD_CUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+        up_ev.resize(s + 2);
+        for (auto& e : up_ev) BSGD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        d_normsq0 = dnew<double>(M);
+    }
     double* d_red = nullptr;           // 8 doubles scratch
     double* d_log = nullptr;           // per-epoch [obj, rmse] scratch
     long long d_log_cap = 0;
@@ -145,6 +156,10 @@ struct bsgd_ctx_s {
     float* pN(float* base, long long b) const { return base + b * padN + orgN; }
     float* pT(float* base, long long b) const { return base + b * padT + orgT; }
     void release() {
+        for (auto& e : up_ev) cudaEventDestroy(e);
+        up_ev.clear();
+        if (copy_st) cudaStreamDestroy(copy_st);
+        copy_st = nullptr;
         for (auto& b : bufs) {
             if (alloc.free) alloc.free(b.p, b.bytes, nullptr, alloc.user);
             else cudaFree(b.p);
@@ -340,9 +355,20 @@ struct bsgd_ctx_s {
 
     // ------------------------------------------------------------ one epoch
     // Algo 1 / Algo 2 / Eq. 4 with an explicit selection.  tiles: [n_cols][V_sel] or empty.
+    // Host-buffer runs (bsgd_run with y / x in host memory) overlap the uploads with the
+    // first epoch: xev (per owned block) makes the FP wait block by block for its x
+    // upload (refreshing the projector copies of every owned block), yev makes the
+    // residual wait for y, and y_reset runs the deferred r = y of Algo 1 line 1 there
+    // (its ||y_I||^2 are kept in d_normsq0 for Algo 3's ||r||^0).
+    struct Upload {
+        const std::vector<cudaEvent_t>* xev = nullptr;
+        cudaEvent_t yev = nullptr;
+        bool y_reset = false;
+    };
     void epoch_step(const float* y, float* x_owned, const std::vector<int>& sel_rows,
                     const std::vector<int>& sel_cols, const std::vector<int>& tiles, float mu_,
-                    bool sgd, cudaStream_t st, cudaEvent_t* ev, bool refresh = true) {
+                    bool sgd, cudaStream_t st, cudaEvent_t* ev, bool refresh = true,
+                    const Upload* up = nullptr) {
         std::vector<int> vsel, slot_row;
         for (int i : sel_rows)
             for (int v : rows[i]) {
@@ -362,7 +388,7 @@ struct bsgd_ctx_s {
         const int nb = (int)oslots.size();
         // x^T of the selected blocks must match x (the caller may have changed x);
         // bsgd_run keeps it in sync itself (refresh = false)
-        if (refresh) refresh_xT(x_owned, oslots, st);
+        if (refresh && !(up && up->xev)) refresh_xT(x_owned, oslots, st);
         auto rect_for = [&](int b, int vs) -> int4 {
             if (tiles.empty()) return make_int4(0, nu, 0, nv);
             int t = tiles[(size_t)ocs[b] * V + vs];
@@ -372,7 +398,19 @@ struct bsgd_ctx_s {
         };
         if (ev) BSGD_CUDA(cudaEventRecord(ev[0], st));
         // ---- lines 4-6: z^j_{I_i} = A_{I_i}^{J_j} x_{J_j}  (IM: tile rows only)
-        {
+        if (up && up->xev) {   // block by block as the x upload lands
+            for (int b = 0; b < s; ++b) {
+                BSGD_CUDA(cudaStreamWaitEvent(st, (*up->xev)[b], 0));
+                refresh_xT(x_owned, {b}, st);
+                for (int q = 0; q < nb; ++q) {
+                    if (oslots[q] != b) continue;
+                    std::vector<int4> rc(V);
+                    for (int vs = 0; vs < V; ++vs) rc[vs] = rect_for(q, vs);
+                    project(PROJ_FP, vsel, {b}, rc, {pN(xN, b)}, {pT(xT, b)}, {}, {}, {z + b * n_rays},
+                            nullptr, 0.f, 0, st, 0);
+                }
+            }
+        } else {
             std::vector<int4> rc((size_t)nb * V);
             std::vector<const float*> xs, xts;
             std::vector<float*> zs;
@@ -383,6 +421,13 @@ struct bsgd_ctx_s {
                 zs.push_back(z + oslots[b] * n_rays);
             }
             project(PROJ_FP, vsel, oslots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
+        }
+        if (up && up->yev) {
+            BSGD_CUDA(cudaStreamWaitEvent(st, up->yev, 0));
+            if (up->y_reset) {
+                reset_r(y, st);
+                BSGD_CUDA(cudaMemcpyAsync(d_normsq0, d_normsq, sizeof(double) * M, cudaMemcpyDeviceToDevice, st));
+            }
         }
         if (ev) BSGD_CUDA(cudaEventRecord(ev[1], st));
         // ---- line 7: r = y - sum_j z^j on the selected rows (+ allreduce of the partials)
@@ -453,9 +498,22 @@ struct bsgd_ctx_s {
     }
 
     void reset(const float* y, cudaStream_t st) {
+        reset_state(st);
+        reset_r(y, st);
+    }
+    // Algo 1 line 1 without y: z = 0, g_hat = 0, g = 0 and the host-side schedule state
+    void reset_state(cudaStream_t st) {
         BSGD_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)s * n_rays, st));
         BSGD_CUDA(cudaMemsetAsync(ghat, 0, sizeof(float) * (size_t)M * s * bsize, st));
         BSGD_CUDA(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)s * bsize, st));
+        if (eud_cur) BSGD_CUDA(cudaMemsetAsync(eud_cur, 0, sizeof(float) * (size_t)s * bsize, st));
+        epoch = 0;
+        have_prev_eud = false;
+        have_theta_prev = false;
+        rnorm_hist.clear();
+    }
+    // ... and r = y on every row block with ||r_I||^2 (needs y on the device)
+    void reset_r(const float* y, cudaStream_t st) {
         BSGD_CUDA(cudaMemsetAsync(d_normsq, 0, sizeof(double) * M, st));
         // r = y - sum z = y on every row block, with ||r_I||^2 (Algo 1 line 1)
         std::vector<int> all(n_views), srow(n_views);
@@ -482,11 +540,6 @@ struct bsgd_ctx_s {
         Rl.normsq = d_normsq;
         Rl.mode = 0;
         launch_residual(Rl, st);   // z = 0 here, so r = y (no allreduce needed)
-        if (eud_cur) BSGD_CUDA(cudaMemsetAsync(eud_cur, 0, sizeof(float) * (size_t)s * bsize, st));
-        epoch = 0;
-        have_prev_eud = false;
-        have_theta_prev = false;
-        rnorm_hist.clear();
     }
 
     // Exact ray-voxel intersection counts (positive-length Siddon segments) per
@@ -1178,20 +1231,37 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (tv && (P->tv_iters < 0 || !isfinite(P->lambda))) fail(BSGD_E_CONTRACT, "bad TV parameters");
         cudaStream_t st = S(stream);
         const long long sb = (long long)c->s * c->bsize;
-        // host or device buffers
+        // host or device buffers.  Host y / x are uploaded on a copy stream that overlaps the
+        // first epoch: x block by block ahead of that block's FP, then y ahead of the first
+        // residual (epoch_step's Upload hooks); the D2H of x at the end stays in order.
         const float* y = y_in;
         float* x = x_in;
         const float* xt = xt_in;
-        if (!is_device_ptr(y_in)) {
-            if (!c->y_dev) c->y_dev = c->dnew<float>(c->n_rays, false);
-            BSGD_CUDA(cudaMemcpyAsync(c->y_dev, y_in, sizeof(float) * c->n_rays, cudaMemcpyHostToDevice, st));
-            y = c->y_dev;
+        const bool y_host = !is_device_ptr(y_in), x_host = !is_device_ptr(x_in);
+        bsgd_ctx_s::Upload up;
+        if (y_host || x_host) {
+            c->ensure_copy_stream();
+            BSGD_CUDA(cudaEventRecord(c->up_ev[c->s + 1], st));            // after prior work
+            BSGD_CUDA(cudaStreamWaitEvent(c->copy_st, c->up_ev[c->s + 1], 0));
         }
-        const bool x_host = !is_device_ptr(x_in);
         if (x_host) {
             if (!c->x_dev) c->x_dev = c->dnew<float>(sb, false);
-            BSGD_CUDA(cudaMemcpyAsync(c->x_dev, x_in, sizeof(float) * sb, cudaMemcpyHostToDevice, st));
+            for (int b = 0; b < c->s; ++b) {
+                BSGD_CUDA(cudaMemcpyAsync(c->x_dev + (size_t)b * c->bsize, x_in + (size_t)b * c->bsize,
+                                          sizeof(float) * c->bsize, cudaMemcpyHostToDevice, c->copy_st));
+                BSGD_CUDA(cudaEventRecord(c->up_ev[b], c->copy_st));
+            }
             x = c->x_dev;
+            c->x_events.assign(c->up_ev.begin(), c->up_ev.begin() + c->s);
+            up.xev = &c->x_events;
+        }
+        if (y_host) {
+            if (!c->y_dev) c->y_dev = c->dnew<float>(c->n_rays, false);
+            BSGD_CUDA(cudaMemcpyAsync(c->y_dev, y_in, sizeof(float) * c->n_rays, cudaMemcpyHostToDevice,
+                                      c->copy_st));
+            BSGD_CUDA(cudaEventRecord(c->up_ev[c->s], c->copy_st));
+            y = c->y_dev;
+            up.yev = c->up_ev[c->s];
         }
         if (xt_in && !is_device_ptr(xt_in)) {
             if (!c->xt_dev) c->xt_dev = c->dnew<float>(sb, false);
@@ -1202,25 +1272,39 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             c->eud_cur = c->dnew<float>(sb);
             c->eud_prev = c->dnew<float>(sb);
         }
+        bool defer_r0 = false;
         if (!(P->flags & BSGD_RESUME)) {
-            c->reset(y, st);
+            if (y_host && P->epochs > 0) {   // r = y after the y upload, inside epoch 0
+                c->reset_state(st);
+                up.y_reset = true;
+                defer_r0 = true;
+            } else {
+                if (y_host) BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
+                c->reset(y, st);
+            }
             c->mu = P->mu0;
             c->rnorm_hist.clear();
         } else if (c->epoch == 0) {
             c->mu = P->mu0;
         }
-        if (c->rnorm_hist.empty()) {   // ||r||^0 = ||y|| (reading A13/A14): r = y after reset
-            BSGD_CUDA(cudaMemcpyAsync(c->h_normsq.data(), c->d_normsq, sizeof(double) * c->M,
-                                      cudaMemcpyDeviceToHost, st));
+        auto push_r0 = [&](const double* d_src) {   // ||r||^0 = ||y|| (reading A13/A14)
+            BSGD_CUDA(cudaMemcpyAsync(c->h_normsq.data(), d_src, sizeof(double) * c->M, cudaMemcpyDeviceToHost, st));
             BSGD_CUDA(cudaStreamSynchronize(st));
             double s2 = 0;
             for (double v : c->h_normsq) s2 += v;
             c->rnorm_hist.push_back(sqrt(s2));
+        };
+        if (c->rnorm_hist.empty() && !defer_r0) {
+            if (y_host && up.yev) BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
+            push_r0(c->d_normsq);
         }
         if (im && !uni) c->ensure_im_table(st);
         std::vector<int> all_slots(c->s);
         for (int b = 0; b < c->s; ++b) all_slots[b] = b;
-        c->refresh_xT(x, all_slots, st);
+        if (x_host && P->epochs == 0) {   // no epoch to hide the upload behind
+            for (int b = 0; b < c->s; ++b) BSGD_CUDA(cudaStreamWaitEvent(st, c->up_ev[b], 0));
+        }
+        if (!x_host || P->epochs == 0) c->refresh_xT(x, all_slots, st);
         const int E = P->epochs;
         if (c->d_log_cap < 2LL * E + 2) {
             c->d_log = c->dnew<double>(2LL * E + 2);
@@ -1266,7 +1350,9 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 }
             }
             cudaEvent_t* evp = timing ? &ev[(size_t)e * 7] : nullptr;
-            c->epoch_step(y, x, rows, sgd ? std::vector<int>() : cols, tiles, (float)c->mu, sgd, st, evp, false);
+            c->epoch_step(y, x, rows, sgd ? std::vector<int>() : cols, tiles, (float)c->mu, sgd, st, evp, false,
+                          e == 0 ? &up : nullptr);
+            if (e == 0 && defer_r0) push_r0(c->d_normsq0);
             if (want_visits) {   // FP visits of this epoch on this rank (BP visits are the same segments)
                 unsigned long long nvt = 0;
                 int V = 0;

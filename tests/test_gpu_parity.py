@@ -358,3 +358,39 @@ def test_collective_path_one_rank(bs, monkeypatch):
     assert np.array_equal(out[0][2], out[1][2])                     # auto-mu decisions
     for k in (1, 3):
         assert np.allclose(out[0][k], out[1][k], rtol=1e-5, atol=0)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_buffer_run_matches_device_run(bs, pinned):
+    """bsgd_run with y / x in host memory (uploads overlapped with the first epoch on a
+    copy stream, the r = y reset deferred into epoch 0) reproduces the device-buffer run:
+    selections and auto-mu decisions identical, objective / x to the run-to-run spread of
+    the order-nondeterministic BP reductions."""
+    p, g, vol32, y = problem("cfg4", K=32, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 1.5 / ob.power_iteration(P, 20, seed=1)
+    rng = np.random.default_rng(3)
+    outs = []
+    for host in (False, True):
+        ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=2, tiles=p.tiles)
+        x0 = (0.01 * rng.random(ctx.owned_count * ctx.block_voxels)).astype(np.float32) if not outs else outs[0][3]
+        if host:
+            yh = torch.from_numpy(y.copy())
+            xh = torch.from_numpy(x0.copy())
+            if pinned:
+                yh, xh = yh.pin_memory(), xh.pin_memory()
+            res = ctx.run(yh, xh, epochs=25, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=3, flags=bs.AUTO_MU)
+            xr = xh.numpy().copy()
+        else:
+            yd = torch.from_numpy(y).cuda()
+            xd = torch.from_numpy(x0.copy()).cuda()
+            res = ctx.run(yd, xd, epochs=25, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=3, flags=bs.AUTO_MU)
+            xr = xd.cpu().numpy()
+        outs.append((res, xr, res.mu.copy(), x0))
+        ctx.close()
+    (r0, x0r, m0, _), (r1, x1r, m1, _) = outs
+    assert np.array_equal(r0.sel_rows, r1.sel_rows) and np.array_equal(r0.sel_cols, r1.sel_cols)
+    assert np.array_equal(m0, m1)
+    assert np.allclose(r0.obj, r1.obj, rtol=1e-5, atol=0)
+    assert np.max(np.abs(x0r - x1r)) <= 1e-5 * np.max(np.abs(x0r))
+
