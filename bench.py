@@ -273,7 +273,8 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": args.steps / (float(te.item()) / 1e3), "unit": "epochs/s",
                "h2d_bytes_per_step": int(4 * g.n_rays / args.steps) + int(4 * n_owned / args.steps),
                "d2h_bytes_per_step": int(4 * n_owned / args.steps),
-               "what": "bsgd_run(y, x on pinned host memory): y and x copied in, K epochs, x copied back"}
+               "what": ("bsgd_run(y, x on pinned host memory): y and x uploaded (on a copy stream, "
+                        "overlapped with the first epoch), K epochs, x copied back")}
         del yh, xh
     ctx.close()
     if rank != 0:
