@@ -35,6 +35,15 @@ WORKLOAD = ("cfg5: 3D cone-beam 1024^3 volume, 720 projections of 1024x1024, M=1
             "(72 views), N=8 z-slab blocks, alpha*M=1, gamma*N=8 per epoch")
 
 
+def workload(p) -> str:
+    """The `config.workload` string of a preset (cfg5 is the headline workload)."""
+    if p.name == "cfg5":
+        return WORKLOAD
+    d = "x".join(str(v) for v in p.dims if v > 1)
+    return (f"{p.name}: {p.beam} {d} volume, {p.n_views} projections of {p.det[0]}x{p.det[1]}, M={p.M} row "
+            f"blocks, N={p.N} blocks {p.blocks}, alpha*M={p.rows_per_epoch}, gamma*N={p.cols_per_epoch} per epoch")
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -192,7 +201,7 @@ def run_ours(args, rank, world, local_rank):
     import paper_1903_11874_b200 as bs
 
     torch.cuda.set_device(local_rank)
-    p = synth.PRESETS["cfg5"]
+    p = synth.PRESETS[args.config]
     g = p.geometry()
     if world > 1:
         r, w, nid = bs.dist_from_process_group()
@@ -207,10 +216,11 @@ def run_ours(args, rank, world, local_rank):
     if args.cheap_data:   # profiling runs: seeded uniform data (Siddon work does not depend on values)
         y.uniform_(0.0, 100.0, generator=torch.Generator(device="cuda").manual_seed(7))
     else:
-        ells = synth.ellipsoids_world("random", g.dims)
+        ells = synth.ellipsoids_world("random" if p.dims[2] > 1 else "shepp2d", g.dims)
         synth.analytic_projection(g, ells, device="cuda", out_torch=y, chunk_rays=1 << 23)
     x = torch.zeros(n_owned, dtype=torch.float32, device="cuda")
-    mu0 = 0.25 / 7.35e5          # below 1/sigma_max^2 (sigma_max^2 >= 7.35e5)
+    # below 1/sigma_max^2 (Rayleigh lower bounds of sigma_max^2)
+    mu0 = 0.25 / {"cfg1": 5451.0, "cfg2": 9.09e4, "cfg3": 8.93e4, "cfg4": 3.59e5}.get(args.config, 7.35e5)
     aM, gN = p.rows_per_epoch, p.cols_per_epoch
     stream = torch.cuda.current_stream()
 
@@ -280,7 +290,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return 0
     cpu = None
-    if world == 1 and not args.no_cpu:
+    if world == 1 and not args.no_cpu and args.config == "cfg5":
         vps, cores, sample, _, _ = oracle_sample(target_s=args.cpu_seconds)
         cpu = {"value": vps / (2 * vis_ep), "unit": "epochs/s", "cores": cores, "kind": "oracle",
                "sample": sample, "intersections_per_s": vps}
@@ -289,8 +299,10 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "intersections_per_s": visits_all / (t_ms / 1e3),
-        "config": {"workload": WORKLOAD, "global_batch": 72, "parallelism": f"z-slab{world}",
-                   "l2": "inputs larger than L2 (537 MB slabs, 3.0 GB y); no flush needed",
+        "config": {"workload": workload(p), "global_batch": int(res.sel_rows.shape[1]) * (g.n_views // p.M),
+                   "parallelism": f"z-slab{world}" if p.blocks[:2] == (1, 1) else f"blocks{world}",
+                   "l2": ("inputs larger than L2 (537 MB slabs, 3.0 GB y); no flush needed" if p.name == "cfg5"
+                          else "auxiliary workload: inputs may be L2-resident, no flush (not the headline)"),
                    "visits_per_epoch_fp": vis_ep * world if world == 1 else None,
                    "fp64": "ray parameters fp64, values fp32"},
         "phase_ms": {"fp": fp_ms, "residual_allreduce": res_ms, "bp": bp_ms, "step": st_ms},
@@ -327,6 +339,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cheap-data", action="store_true", help="uniform random y instead of analytic projections")
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="workload (cfg5 = the BASELINE.json headline; the others for DESIGN tables)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
