@@ -533,13 +533,14 @@ struct bsgd_ctx_s {
         Rl.per = (int)per;
         Rl.z = z;
         Rl.n_rays = n_rays;
-        Rl.s = s;
+        Rl.s = 0;                  // no z terms: r = y exactly (Algo 1 line 1, z = 0), even when a
+                                   // deferred reset runs after the first FP has filled some z
         Rl.y = y;
         Rl.r = r;
         Rl.pc = pc;
         Rl.normsq = d_normsq;
         Rl.mode = 0;
-        launch_residual(Rl, st);   // z = 0 here, so r = y (no allreduce needed)
+        launch_residual(Rl, st);   // no allreduce needed
     }
 
     // Exact ray-voxel intersection counts (positive-length Siddon segments) per
