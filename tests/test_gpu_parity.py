@@ -334,6 +334,35 @@ def test_full_size_engine_step_cfg5(bs):
     ctx.close()
 
 
+def test_full_size_trajectory_cfg4(bs):
+    """cfg4 at full size (512^3, 720 x 512^2, M = 10, N = 8 z-slabs), 4 BSGD epochs with
+    alpha M = 1, gamma N = 2 against the oracle (fp64, ~25 GB of host state): selections
+    bit-exact, objective and x within the trajectory bar."""
+    p = synth.PRESETS["cfg4"]
+    g = p.geometry()
+    ells = synth.ellipsoids_world(p.phantom, g.dims)
+    y = synth.analytic_projection(g, ells, device="cuda").astype(np.float32).ravel()
+    mu = 0.25 / 3.59e5          # below 1/sigma_max^2 (sigma_max^2 >= 3.59e5, SURVEY App. A)
+    prm = ob.Params(seed=3, mu=float(np.float32(mu)), rows_per_epoch=1, cols_per_epoch=2)
+    o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11)
+    for _ in range(4):
+        o.epoch()
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11)
+    yd = torch.from_numpy(y).cuda()
+    xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    res = ctx.run(yd, xd, epochs=4, mu0=float(np.float32(mu)), seed=3, rows_per_epoch=1, cols_per_epoch=2)
+    xg = xd.cpu().numpy().astype(np.float64)
+    ctx.close()
+    assert [r["rows"] for r in o.log] == res.sel_rows.tolist()
+    assert [r["cols"] for r in o.log] == res.sel_cols.tolist()
+    obj = np.array([r["obj"] for r in o.log])
+    e_obj = np.max(np.abs(res.obj - obj) / obj)
+    xo = o.x.ravel()
+    e_x = np.max(np.abs(xg - xo)) / np.max(np.abs(xo))
+    print("cfg4 full-size trajectory: obj rel err", e_obj, "x rel err", e_x)
+    assert e_obj < 1e-3 and e_x < 1e-2, (e_obj, e_x)
+
+
 def test_collective_path_one_rank(bs, monkeypatch):
     """The world > 1 code path (partial sums -> ncclAllReduce -> residual; fp64
     allreduces of Algo 3 and RMSE) run through a one-rank NCCL communicator
