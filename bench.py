@@ -67,29 +67,63 @@ def load_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled during the timed region: NVML
+    every 20 ms (pynvml, from nvidia_ml_py), else nvidia-smi every 0.2 s."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap,utilization.gpu")
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []            # (sm_mhz, max_mhz, reasons set, util %)
         self._stop = threading.Event()
         self._t = None
+        self.source = "none"
 
-    def _run(self):
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = [(name, getattr(nv, attr)) for name, attr in self.REASONS if hasattr(nv, attr)]
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                ev = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                util = nv.nvmlDeviceGetUtilizationRates(h).gpu
+                self.rows.append((float(sm), float(mx), {n for n, b in bits if ev & b}, util))
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def _run_smi(self):
+        names = [n for n, _ in self.REASONS[:4]]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                r = [c.strip() for c in out.split(",")] if out else []
+                if len(r) >= 7 and r[0].replace(".", "").isdigit():
+                    act = {names[k] for k in range(4) if "Active" in r[2 + k] and "Not" not in r[2 + k]}
+                    self.rows.append((float(r[0]), float(r[1]), act, int(r[6]) if r[6].isdigit() else 100))
             except Exception:
                 pass
             self._stop.wait(0.2)
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.source = "nvml"
+            self._run_nvml(nv)
+        except Exception:
+            self.source = "nvidia-smi"
+            self._run_smi()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -102,15 +136,14 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        busy = [float(r[0]) for r in self.rows if len(r) > 6 and r[6].isdigit() and int(r[6]) > 50]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 2 + k and "Active" in r[2 + k]
-                          and "Not" not in r[2 + k]})
-        return {"sm_mhz": float(np.median(busy or sm)) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"]}
+        sm = [r[0] for r in self.rows]
+        busy = [r[0] for r in self.rows if r[3] > 50]
+        reasons = sorted(set().union(*(r[2] for r in self.rows)))
+        frac = {n: round(sum(1 for r in self.rows if n in r[2]) / len(self.rows), 3) for n in reasons}
+        return {"sm_mhz": float(np.median(busy or sm)), "sm_max_mhz": self.rows[0][1], "reasons": reasons,
+                "reason_sample_fraction": frac, "sm_mhz_min": float(min(sm)), "samples": len(self.rows),
+                "source": self.source}
 
 
 # --------------------------------------------------------------------------- oracle (CPU) timing
@@ -259,13 +292,16 @@ def run_ours(args, rank, world, local_rank):
     vis_ep = float(np.mean(res.visits))
     peak, peak_src = load_peaks()
     prof = load_traffic()
-    kern = {"fp": (fp_ms, 4.0 * vis_ep), "bp": (bp_ms, 8.0 * vis_ep)}
-    dom = max(kern, key=lambda k: kern[k][0])
-    dms, dbytes = kern[dom]
+    # The dominant kernel is the projector pair: the FP and the BP launches are one and the
+    # same Siddon traversal (each ~48 % of the step) and SURVEY §8d's unit of work is the
+    # FP+BP visit pair (4 B gathered + 8 B reduced = 12 B).  Reporting the pair keeps the
+    # line stable when the two are within noise of each other; fp_frac / bp_frac below.
+    dms = fp_ms + bp_ms
+    dbytes = 12.0 * vis_ep
     achieved = dbytes / (dms / 1e3) / 1e9
     traffic = None
-    if prof.get(dom, {}).get("dram_bytes_per_visit") is not None:
-        traffic = prof[dom]["dram_bytes_per_visit"] * vis_ep
+    if all(prof.get(k, {}).get("dram_bytes_per_visit") is not None for k in ("fp", "bp")):
+        traffic = (prof["fp"]["dram_bytes_per_visit"] + prof["bp"]["dram_bytes_per_visit"]) * vis_ep
     # e2e: the same metric through the C ABI with HOST buffers (pinned), copies inside
     e2e = None
     if not args.no_e2e:
@@ -312,11 +348,12 @@ def run_ours(args, rank, world, local_rank):
             "vs_gbs": 900.0,
             "note": "residual phase time includes the partial-sum and residual kernels, so this is a lower bound "
                     "on the collective's own bus bandwidth"},
-        "roofline": {"bound": "hbm", "kernel": ("k_project3<FP> (+ k_project2<FP, steep-only>)" if dom == "fp"
-                                else "k_project3<BP> (+ k_project2<BP, steep-only>)"),
+        "roofline": {"bound": "hbm",
+                     "kernel": "projector pair k_project3<FP> + k_project3<BP> (+ k_project2 steep-only companions)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes": f"{'4' if dom == 'fp' else '8'} B x {vis_ep:.4g} visits per launch",
+                     "algorithmic_bytes": f"12 B x {vis_ep:.4g} visit pairs per FP+BP launch pair",
+                     "time_ms": dms,
                      "fp_frac": (4.0 * vis_ep / (fp_ms / 1e3) / 1e9) / peak,
                      "bp_frac": (8.0 * vis_ep / (bp_ms / 1e3) / 1e9) / peak,
                      "fp_plus_bp_frac": (12.0 * vis_ep / ((fp_ms + bp_ms) / 1e3) / 1e9) / peak},
