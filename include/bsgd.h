@@ -208,7 +208,9 @@ bsgd_status bsgd_run(bsgd_ctx ctx, const float* y, float* x_owned, const float* 
                      const bsgd_run_params* params, bsgd_run_log* log, void* stream);
 
 /* Inspection (tests): copy internal state to / from host memory.
- * what: 0 = z^j of owned block slot `index` (n_rays floats);
+ * what: 0 = z^j of owned block slot `index` (n_rays floats, full length; the library stores
+ *           only each view's detector footprint of the block, zero elsewhere, so set_state
+ *           keeps just the footprint part of the given vector);
  *       1 = g_hat^i of (i = index / owned_count, owned slot = index % owned_count);
  *       2 = g of owned slot `index`;  3 = r (n_rays floats);
  *       4 = per-row-block ||r_I||^2 (M doubles);  5 = current mu (1 double).

@@ -81,6 +81,10 @@ struct bsgd_ctx_s {
     float *y_dev = nullptr, *x_dev = nullptr, *xt_dev = nullptr;
     float *sv_a = nullptr, *sv_b = nullptr, *sv_c = nullptr, *sv_d = nullptr, *y_zero = nullptr;   // solvers
     double* d_normsq = nullptr;
+    // footprint-restricted z^j storage: ZRect per (owned block, view)
+    std::vector<ZRect> h_zr;
+    ZRect* d_zr = nullptr;
+    long long z_size = 0;
     double* d_normsq0 = nullptr;         // ||y_I||^2 of a deferred reset (host-buffer runs)
     cudaStream_t copy_st = nullptr;      // H2D uploads of host-buffer runs
     std::vector<cudaEvent_t> x_events;
@@ -270,6 +274,7 @@ struct bsgd_ctx_s {
             d.outN = oN.empty() ? nullptr : oN[b];
             d.outT = oT.empty() ? nullptr : oT[b];
             d.z = zout.empty() ? nullptr : zout[b];
+            d.zr = (!zout.empty() && zout[b] == z) ? d_zr + (size_t)slots[b] * n_views : nullptr;
             d.rowN = rowN; d.planeN = planeN; d.rowT = rowT; d.planeT = planeT;
         }
         std::vector<int4> rc = rects;
@@ -406,7 +411,7 @@ struct bsgd_ctx_s {
                     if (oslots[q] != b) continue;
                     std::vector<int4> rc(V);
                     for (int vs = 0; vs < V; ++vs) rc[vs] = rect_for(q, vs);
-                    project(PROJ_FP, vsel, {b}, rc, {pN(xN, b)}, {pT(xT, b)}, {}, {}, {z + b * n_rays},
+                    project(PROJ_FP, vsel, {b}, rc, {pN(xN, b)}, {pT(xT, b)}, {}, {}, {z},
                             nullptr, 0.f, 0, st, 0);
                 }
             }
@@ -418,7 +423,7 @@ struct bsgd_ctx_s {
                 for (int vs = 0; vs < V; ++vs) rc[(size_t)b * V + vs] = rect_for(b, vs);
                 xs.push_back(pN(xN, oslots[b]));
                 xts.push_back(pT(xT, oslots[b]));
-                zs.push_back(z + oslots[b] * n_rays);
+                zs.push_back(z);   // packed footprint storage (ZRect table of the slot)
             }
             project(PROJ_FP, vsel, oslots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
         }
@@ -444,6 +449,9 @@ struct bsgd_ctx_s {
                                       off - tab_bytes / 2, cudaMemcpyHostToDevice, st));
             Rl.per = (int)per;
             Rl.z = z;
+            Rl.zr = d_zr;
+            Rl.n_views = n_views;
+            Rl.nu = nu;
             Rl.n_rays = n_rays;
             Rl.s = s;
             Rl.y = y;
@@ -503,7 +511,7 @@ struct bsgd_ctx_s {
     }
     // Algo 1 line 1 without y: z = 0, g_hat = 0, g = 0 and the host-side schedule state
     void reset_state(cudaStream_t st) {
-        BSGD_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)s * n_rays, st));
+        BSGD_CUDA(cudaMemsetAsync(z, 0, sizeof(float) * (size_t)z_size, st));
         BSGD_CUDA(cudaMemsetAsync(ghat, 0, sizeof(float) * (size_t)M * s * bsize, st));
         BSGD_CUDA(cudaMemsetAsync(g, 0, sizeof(float) * (size_t)s * bsize, st));
         if (eud_cur) BSGD_CUDA(cudaMemsetAsync(eud_cur, 0, sizeof(float) * (size_t)s * bsize, st));
@@ -532,6 +540,9 @@ struct bsgd_ctx_s {
         tab_upload(staging, off, st);
         Rl.per = (int)per;
         Rl.z = z;
+        Rl.zr = d_zr;
+        Rl.n_views = n_views;
+        Rl.nu = nu;
         Rl.n_rays = n_rays;
         Rl.s = 0;                  // no z terms: r = y exactly (Algo 1 line 1, z = 0), even when a
                                    // deferred reset runs after the first FP has filled some z
@@ -622,7 +633,7 @@ struct bsgd_ctx_s {
             for (int b = 0; b < s; ++b) {
                 xs.push_back(pN(xN, b));
                 xts.push_back(pT(xT, b));
-                zs.push_back(z + b * n_rays);
+                zs.push_back(z);
             }
             project(PROJ_FP, vsel, slots, rc, xs, xts, {}, {}, zs, nullptr, 0.f, 0, st, 0);
         }
@@ -640,6 +651,9 @@ struct bsgd_ctx_s {
                                       off - tab_bytes / 2, cudaMemcpyHostToDevice, st));
             Rl.per = (int)per;
             Rl.z = z;
+            Rl.zr = d_zr;
+            Rl.n_views = n_views;
+            Rl.nu = nu;
             Rl.n_rays = n_rays;
             Rl.s = s;
             Rl.y = yv;
@@ -1029,7 +1043,28 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         c->xN = c->dnew_pad(c->s, false);
         c->g = c->dnew<float>(sb);
         c->ghat = c->dnew<float>((long long)c->M * sb);
-        c->z = c->dnew<float>((long long)c->s * c->n_rays);
+        {   // z^j only inside each block's detector footprint per view (the launch-culling
+            // rectangle): at cfg5 about 1.3 full-length vectors for 8 slabs instead of 8
+            c->h_zr.resize((size_t)c->s * c->n_views);
+            long long off = 0;
+            for (int b = 0; b < c->s; ++b) {
+                int lo[3], hi[3];
+                c->box(c->first + b, lo, hi);
+                for (int v = 0; v < c->n_views; ++v) {
+                    int4 f = c->footprint(lo, hi, v);
+                    if (f.x >= f.y || f.z >= f.w) f = make_int4(0, 0, 0, 0);
+                    ZRect& q = c->h_zr[(size_t)b * c->n_views + v];
+                    q.u0 = f.x; q.u1 = f.y; q.v0 = f.z; q.v1 = f.w;
+                    q.base = off;
+                    q.pad_ = 0;
+                    off += (long long)(f.y - f.x) * (f.w - f.z);
+                }
+            }
+            c->z_size = std::max(off, 1LL);
+            c->z = c->dnew<float>(c->z_size);
+            c->d_zr = c->dnew<ZRect>((long long)c->h_zr.size(), false);
+            BSGD_CUDA(cudaMemcpy(c->d_zr, c->h_zr.data(), sizeof(ZRect) * c->h_zr.size(), cudaMemcpyHostToDevice));
+        }
         c->r = c->dnew<float>(c->n_rays);
         c->accN = c->dnew_pad(c->s, false);
         c->accT = c->dnew_pad(c->s, true);
@@ -1458,8 +1493,23 @@ bsgd_status bsgd_get_state(bsgd_ctx c, int32_t what, int32_t index, void* dst, s
         if (!c || !dst) fail(BSGD_E_CONTRACT, "NULL");
         const void* src = nullptr;
         size_t need = 0;
+        if (what == 0) {   // z^j of owned slot `index`, expanded from the footprint storage
+            if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot");
+            if (bytes != 4 * (size_t)c->n_rays) fail(BSGD_E_DIMENSION, "size mismatch");
+            BSGD_CUDA(cudaDeviceSynchronize());
+            float* out = (float*)dst;
+            memset(out, 0, bytes);
+            for (int v = 0; v < c->n_views; ++v) {
+                const ZRect& q = c->h_zr[(size_t)index * c->n_views + v];
+                const int w = q.u1 - q.u0;
+                if (w <= 0 || q.v1 <= q.v0) continue;
+                BSGD_CUDA(cudaMemcpy2D(out + ((size_t)v * c->nv + q.v0) * c->nu + q.u0, sizeof(float) * c->nu,
+                                       c->z + q.base, sizeof(float) * w, sizeof(float) * w, q.v1 - q.v0,
+                                       cudaMemcpyDeviceToHost));
+            }
+            return;
+        }
         switch (what) {
-            case 0: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); src = c->z + index * c->n_rays; need = 4 * c->n_rays; break;
             case 1: if (index < 0 || index >= c->M * c->s) fail(BSGD_E_DIMENSION, "index"); src = c->ghat_of(index / c->s, index % c->s); need = 4 * c->bsize; break;
             case 2: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); src = c->g + index * c->bsize; need = 4 * c->bsize; break;
             case 3: src = c->r; need = 4 * c->n_rays; break;
@@ -1478,8 +1528,22 @@ bsgd_status bsgd_set_state(bsgd_ctx c, int32_t what, int32_t index, const void* 
         if (!c || !src) fail(BSGD_E_CONTRACT, "NULL");
         void* dst = nullptr;
         size_t need = 0;
+        if (what == 0) {   // z^j of owned slot `index`: only its footprint part is stored
+            if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot");
+            if (bytes != 4 * (size_t)c->n_rays) fail(BSGD_E_DIMENSION, "size mismatch");
+            BSGD_CUDA(cudaDeviceSynchronize());
+            const float* in = (const float*)src;
+            for (int v = 0; v < c->n_views; ++v) {
+                const ZRect& q = c->h_zr[(size_t)index * c->n_views + v];
+                const int w = q.u1 - q.u0;
+                if (w <= 0 || q.v1 <= q.v0) continue;
+                BSGD_CUDA(cudaMemcpy2D(c->z + q.base, sizeof(float) * w,
+                                       in + ((size_t)v * c->nv + q.v0) * c->nu + q.u0, sizeof(float) * c->nu,
+                                       sizeof(float) * w, q.v1 - q.v0, cudaMemcpyHostToDevice));
+            }
+            return;
+        }
         switch (what) {
-            case 0: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); dst = c->z + index * c->n_rays; need = 4 * c->n_rays; break;
             case 1: if (index < 0 || index >= c->M * c->s) fail(BSGD_E_DIMENSION, "index"); dst = c->ghat_of(index / c->s, index % c->s); need = 4 * c->bsize; break;
             case 2: if (index < 0 || index >= c->s) fail(BSGD_E_DIMENSION, "slot"); dst = c->g + index * c->bsize; need = 4 * c->bsize; break;
             case 3: dst = c->r; need = 4 * c->n_rays; break;

@@ -43,13 +43,25 @@ struct KGeom {
     double R;            // parallel-beam half length (|diag|/2 + 1)
 };
 
+// Footprint-restricted storage of z^j: per (owned block, view) the detector
+// rectangle [u0,u1) x [v0,v1) the block's box projects into (the launch-culling footprint,
+// u0/u1 multiples of 32 or nu) and the offset of its (u0, v0) element in the packed buffer;
+// rays outside it have z^j = 0 and are not stored.
+struct ZRect {
+    int u0, u1, v0, v1;
+    long long base;
+    long long pad_;
+};
+
 // One column block as seen by a projection launch.
 struct BlockDesc {
     const float* xN;     // FP source, block layout [z][y][x]
     const float* xT;     // FP source, transposed layout [z][x][y]
     float* outN;         // BP target (normal layout)
     float* outT;         // BP target (transposed layout)
-    float* z;            // FP target, full-length projection vector
+    float* z;            // FP target: full-length projection vector (zr == NULL) or the packed
+                         // footprint storage of the block's z (zr = its [n_views] ZRect table)
+    const ZRect* zr;
     int lo[3], hi[3];    // box in grid coordinates
     int band_lo;         // first detector-row band with work for this block
     // Strides of the library's PADDED image copies (xN/xT, outN/outT point at voxel (0,0,0)
@@ -108,7 +120,10 @@ struct ResLaunch {
     const int* views;       // device [n_slots]
     const int* slot_row;    // device [n_slots] row-block id of the slot
     int per;                // rays per view
-    const float* z;         // owned z vectors, stride n_rays
+    const float* z;         // owned z vectors: packed footprint storage (ZRect table zr)
+    const ZRect* zr;        // [s][n_views]
+    int n_views;
+    int nu;                 // detector columns (rays per view = per = nu * nv)
     long long n_rays;
     int s;                  // owned blocks
     const float* y;

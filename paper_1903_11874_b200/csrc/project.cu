@@ -65,6 +65,14 @@ __device__ __forceinline__ bool lane_steep_v3(const double b[3], bool mainX) {
     return lane_steep(f);
 }
 
+// FP output address of ray (view, iu, iv): the full-length vector, or the block's packed
+// footprint storage of z^j (the launch rectangles lie inside the footprint)
+__device__ __forceinline__ float* zaddr(const BlockDesc& B, const KGeom& g, int view, int iu, int iv) {
+    if (!B.zr) return B.z + ((long long)view * g.nv + iv) * g.nu + iu;
+    const ZRect q = B.zr[view];
+    return B.z + q.base + (long long)(iv - q.v0) * (q.u1 - q.u0) + (iu - q.u0);
+}
+
 // Ray (view, iv, iu) in grid coordinates, exactly as the problem defines it.
 __device__ __forceinline__ void make_ray(const KGeom& g, const double* vec, int iu, int iv,
                                          double a[3], double b[3]) {
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     if (MODE == PROJ_FP && inrect) {
         acc += (double)acc32;
         acc *= blen;                        // t units -> voxel lengths
-        float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
+        float* zp = zaddr(B, L.g, view, iu, iv);
         *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
     }
     if (MODE == PROJ_COUNT && L.visits) {   // per (block, slot) counters
@@ -573,7 +581,7 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         if (pin) acc32 = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
         acc += (double)acc32;
         acc *= (double)Ls;                  // main-axis units -> voxel lengths
-        float* zp = B.z + ((long long)view * L.g.nv + iv) * L.g.nu + iu;
+        float* zp = zaddr(B, L.g, view, iu, iv);
         *zp = L.accumulate ? (*zp + (float)acc) : (float)acc;
     }
     if (MODE == PROJ_COUNT && L.visits) {

@@ -197,24 +197,36 @@ __global__ void __launch_bounds__(256) k_block_update(const UpdLaunch U) {
         if (okT[k]) U.xT[iT[k]] = tX[tx][ty + 8 * k];
 }
 
+// sum_j z^j over the owned blocks whose footprint holds the ray (packed storage, ZRect)
+__device__ __forceinline__ const float* zrow(const ResLaunch& R, int j, int view, int iu, int iv) {
+    const ZRect q = R.zr[(size_t)j * R.n_views + view];
+    if (iu < q.u0 || iu >= q.u1 || iv < q.v0 || iv >= q.v1) return nullptr;
+    return R.z + q.base + (long long)(iv - q.v0) * (q.u1 - q.u0) + (iu - q.u0);
+}
+
 __global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
     const int slot = blockIdx.y;
-    const long long base = (long long)R.views[slot] * R.per;
+    const int view = R.views[slot];
+    const long long base = (long long)view * R.per;
     const long long cbase = (long long)slot * R.per;
     double ss = 0.0;
-    const bool v4 = (R.per & 3) == 0;
+    // float4 along u: footprint rectangles start and end on multiples of 32 columns (or nu)
+    const bool v4 = (R.per & 3) == 0 && (R.nu & 3) == 0;
     const long long nvec = v4 ? R.per / 4 : R.per;
     for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nvec;
          q += (long long)gridDim.x * blockDim.x) {
         if (v4) {
             const long long e = base + 4 * q;
+            const int iv = (int)((4 * q) / R.nu), iu = (int)((4 * q) % R.nu);
             float4 acc;
             if (R.mode == 2) {
                 acc = *reinterpret_cast<const float4*>(R.pc + cbase + 4 * q);
             } else {
                 acc = make_float4(0.f, 0.f, 0.f, 0.f);
                 for (int j = 0; j < R.s; ++j) {   // sum over owned blocks in ascending order
-                    const float4 zz = __ldg(reinterpret_cast<const float4*>(R.z + (long long)j * R.n_rays + e));
+                    const float* zp = zrow(R, j, view, iu, iv);
+                    if (!zp) continue;
+                    const float4 zz = __ldg(reinterpret_cast<const float4*>(zp));
                     acc.x += zz.x; acc.y += zz.y; acc.z += zz.z; acc.w += zz.w;
                 }
             }
@@ -228,10 +240,14 @@ __global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
             }
         } else {
             const long long e = base + q;
+            const int iv = (int)(q / R.nu), iu = (int)(q % R.nu);
             float acc = 0.f;
             if (R.mode == 2) acc = R.pc[cbase + q];
             else
-                for (int j = 0; j < R.s; ++j) acc += __ldg(R.z + (long long)j * R.n_rays + e);
+                for (int j = 0; j < R.s; ++j) {
+                    const float* zp = zrow(R, j, view, iu, iv);
+                    if (zp) acc += __ldg(zp);
+                }
             if (R.mode == 1) {
                 R.pc[cbase + q] = acc;
             } else {
