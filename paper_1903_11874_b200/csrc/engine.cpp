@@ -369,6 +369,10 @@ struct bsgd_ctx_s {
         const std::vector<cudaEvent_t>* xev = nullptr;
         cudaEvent_t yev = nullptr;
         bool y_reset = false;
+        // last epoch of a host-x run: each block's x goes to the host as soon as its final
+        // update is done (the BP of the final row block then runs block by block), so the
+        // download overlaps the remaining BP launches
+        float* x_host_out = nullptr;
     };
     void epoch_step(const float* y, float* x_owned, const std::vector<int>& sel_rows,
                     const std::vector<int>& sel_cols, const std::vector<int>& tiles, float mu_,
@@ -493,12 +497,34 @@ struct bsgd_ctx_s {
                 std::vector<int4> rc((size_t)nb * Vi);
                 for (int b = 0; b < nb; ++b)
                     for (int k = 0; k < Vi; ++k) rc[(size_t)b * Vi + k] = rect_for(b, vs0 + k);
-                project(PROJ_BP, vi, oslots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
-                if (ev && ii + 1 == sel_rows.size()) BSGD_CUDA(cudaEventRecord(ev[3], st));
                 const int fin = (ii + 1 == sel_rows.size());
-                for (int b = 0; b < nb; ++b)
-                    update(UPD_BSGD, oslots[b], x_owned + oslots[b] * bsize, mu_, fin, nullptr, 0, st,
-                           nullptr, nullptr, nullptr, i);
+                if (fin && up && up->x_host_out) {
+                    // blocks this epoch does not update are final already
+                    BSGD_CUDA(cudaEventRecord(up_ev[s + 1], st));
+                    BSGD_CUDA(cudaStreamWaitEvent(copy_st, up_ev[s + 1], 0));
+                    for (int q = 0; q < s; ++q)
+                        if (std::find(oslots.begin(), oslots.end(), q) == oslots.end())
+                            BSGD_CUDA(cudaMemcpyAsync(up->x_host_out + (size_t)q * bsize, x_owned + (size_t)q * bsize,
+                                                      sizeof(float) * bsize, cudaMemcpyDeviceToHost, copy_st));
+                    for (int b = 0; b < nb; ++b) {
+                        std::vector<int4> rcb(rc.begin() + (size_t)b * Vi, rc.begin() + (size_t)(b + 1) * Vi);
+                        project(PROJ_BP, vi, {oslots[b]}, rcb, none, none, {oN[b]}, {oT[b]}, {}, r, 2.f, 0, st, 0);
+                        update(UPD_BSGD, oslots[b], x_owned + oslots[b] * bsize, mu_, fin, nullptr, 0, st,
+                               nullptr, nullptr, nullptr, i);
+                        BSGD_CUDA(cudaEventRecord(up_ev[b], st));
+                        BSGD_CUDA(cudaStreamWaitEvent(copy_st, up_ev[b], 0));
+                        BSGD_CUDA(cudaMemcpyAsync(up->x_host_out + (size_t)oslots[b] * bsize,
+                                                  x_owned + (size_t)oslots[b] * bsize, sizeof(float) * bsize,
+                                                  cudaMemcpyDeviceToHost, copy_st));
+                    }
+                    if (ev) BSGD_CUDA(cudaEventRecord(ev[3], st));
+                } else {
+                    project(PROJ_BP, vi, oslots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
+                    if (ev && fin) BSGD_CUDA(cudaEventRecord(ev[3], st));
+                    for (int b = 0; b < nb; ++b)
+                        update(UPD_BSGD, oslots[b], x_owned + oslots[b] * bsize, mu_, fin, nullptr, 0, st,
+                               nullptr, nullptr, nullptr, i);
+                }
                 vs0 += Vi;
             }
         }
@@ -1360,6 +1386,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                                                   : std::max(1, (int)floor((double)c->M * c->N / ((double)aM * gN) + 0.5)))
                               : 0;
         std::vector<double> mu_log(E);
+        bool downloaded = false;
         std::vector<int> rows(aM), cols(gN);
         for (int e = 0; e < E; ++e) {
             const int eg = c->epoch;          // global 0-based epoch (RNG counter)
@@ -1386,8 +1413,19 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 }
             }
             cudaEvent_t* evp = timing ? &ev[(size_t)e * 7] : nullptr;
+            // last epoch of a host-x run: overlap the x download with the final BP launches
+            // (not when a TV prox follows: it changes x after the updates)
+            bsgd_ctx_s::Upload down;
+            const bool overlap_down = x_host && !sgd && e + 1 == E && !(tv && k % period == 0);
+            bsgd_ctx_s::Upload* hook = e == 0 ? &up : nullptr;
+            if (overlap_down) {
+                if (hook) down = up;
+                down.x_host_out = x_in;
+                hook = &down;
+                downloaded = true;
+            }
             c->epoch_step(y, x, rows, sgd ? std::vector<int>() : cols, tiles, (float)c->mu, sgd, st, evp, false,
-                          e == 0 ? &up : nullptr);
+                          hook);
             if (e == 0 && defer_r0) push_r0(c->d_normsq0);
             if (want_visits) {   // FP visits of this epoch on this rank (BP visits are the same segments)
                 unsigned long long nvt = 0;
@@ -1463,7 +1501,12 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             if (evp) BSGD_CUDA(cudaEventRecord(evp[6], st));
             c->epoch += 1;
         }
-        if (x_host) BSGD_CUDA(cudaMemcpyAsync(x_in, x, sizeof(float) * sb, cudaMemcpyDeviceToHost, st));
+        if (downloaded) {   // the per-block downloads on the copy stream
+            BSGD_CUDA(cudaEventRecord(c->up_ev[c->s + 1], c->copy_st));
+            BSGD_CUDA(cudaStreamWaitEvent(st, c->up_ev[c->s + 1], 0));
+        } else if (x_host) {
+            BSGD_CUDA(cudaMemcpyAsync(x_in, x, sizeof(float) * sb, cudaMemcpyDeviceToHost, st));
+        }
         std::vector<double> hl(2 * (size_t)E + 2);
         BSGD_CUDA(cudaMemcpyAsync(hl.data(), c->d_log, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, st));
         BSGD_CUDA(cudaStreamSynchronize(st));
