@@ -149,8 +149,8 @@ struct bsgd_ctx_s {
     // per block, rows carry PAD_X zero floats on each side and PAD_Z zero planes bound the
     // block, so a traversal step up to one cell past a row / plane face reads 0 (FP) or lands
     // in the ignored border (BP).  That lets the FP/BP slice loop skip entry/exit clamping.
-    // Each whole buffer also carries `slack` zeroed floats on both sides (v2's L1 prefetch
-    // lead).  pN / pT give the interior origin of owned block b.
+    // Each whole buffer also carries `slack` zeroed floats on both sides (a safety margin
+    // of one padded plane).  pN / pT give the interior origin of owned block b.
     int rowN = 0, planeN = 0, rowT = 0, planeT = 0;
     long long padN = 0, padT = 0, orgN = 0, orgT = 0, slack = 0;
     float* dnew_pad(int nblocks, bool transposed) {
@@ -193,7 +193,6 @@ struct bsgd_ctx_s {
     // bounding box of the projected corners + 1 pixel margin, u aligned to warps.
     // Falls back to the whole detector when a corner is not in front of the source.
     int band_rows = 8;   // BSGD_BAND_ROWS (measured: 1: 3.31, 2: 3.46, 4: 3.54, 8: 3.56, 16: 3.54 epochs/s)
-    int pf_rows = 0;   // BSGD_PF_ROWS (FP L1 prefetch lead; 0 = off, measured faster for v3)
     int4 footprint(const int lo[3], const int hi[3], int view) const {
         const int4 full = make_int4(0, nu, 0, nv);
         const double* q = &vecs[12 * (size_t)view];
@@ -314,7 +313,6 @@ struct bsgd_ctx_s {
         L.rows_per_band = R;
         L.n_chunks = (R * maxw + 255) / 256;
         L.n_bands = nbands;
-        L.pf_rows = std::min(pf_rows, std::max(1, bd[0] < bd[1] ? bd[0] : bd[1]) / 1);
         L.rproj = rproj;
         L.scale = scale;
         L.accumulate = accumulate;
@@ -1037,7 +1035,6 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         c->s = c->N / c->world;
         c->first = c->rank * c->s;
         if (const char* e = getenv("BSGD_BAND_ROWS")) c->band_rows = std::max(1, atoi(e));
-        if (const char* e = getenv("BSGD_PF_ROWS")) c->pf_rows = std::min(4, std::max(0, atoi(e)));
         if (c->bsize >= (1LL << 31)) fail(BSGD_E_PARTITION, "a column block must hold fewer than 2^31 voxels");
         // row blocks
         std::vector<int32_t> vv(c->n_views), off(c->M + 1);

@@ -86,7 +86,6 @@ struct ProjLaunch {
     int rows_per_band;         // R: detector rows per band (band-major CTA order)
     int n_chunks;              // CTAs per (band, slot)
     int n_bands;               // max bands per block (grid.x = n_bands * n_slots * n_chunks)
-    int pf_rows;               // FP: prefetch the line this many slices ahead (1..4; slack covers it)
     const float* rproj;        // BP input (full length)
     float scale;               // BP scale (2 in Algo 1)
     int accumulate;            // FP: add into z instead of overwriting

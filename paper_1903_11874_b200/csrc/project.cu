@@ -201,7 +201,6 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     }
     const int pstep = sz * (int)plane;
     const int rowstep = sy * bdx;
-    const int pf_off = (L.pf_rows - 1) * rowstep;   // FP prefetch lead (rows beyond the next slice)
     const float wbp = (float)blen * rs;   // BP weight per unit t: |b| * scale * r_ray
     const float cthr = (float)(1e-6 / blen);   // COUNT: segments above 1e-6 voxel (see v3)
     double acc = 0.0;
@@ -295,9 +294,6 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                 t = thi;
                 tpl += dty;
                 o += rowstep;
-                // FP: pull the next slice's line into L1 now (no register cost); the
-                // gather there then hits L1 instead of waiting on L2/HBM
-                if (MODE == PROJ_FP) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + o + pf_off));
             }
             if (MODE == PROJ_FP && (k & 15) == 15) {   // warp-uniform
                 acc += (double)acc32;
@@ -320,22 +316,22 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
 // ---------------------------------------------------------------------------------------
 // v3 traversal: the same slice-lockstep Siddon, parametrised by the distance s travelled
 // along the main axis instead of by the ray parameter t.  Inside the block the ray is the
-// line x(s) = x_p + kx s, z(s) = z_p + kz s (|kx|, |kz| < 1 for "non-steep" rays), so the
-// in-plane coordinates at consecutive slice planes form arithmetic sequences.  They are kept
-// as 32-bit fixed-point FRACTIONS (2^-32 voxel) of mirrored coordinates (mirroring makes
-// both slopes non-negative): a plane of an axis is crossed inside a slice iff the fraction
-// add carries, and the crossing lies at u = (2^32 - frac) / K of the slice.  The integer
-// parts never need storing: the voxel offset o advances by the axis stride on a carry.
-// Per slice this is two integer adds, two I2F + FMUL and ~20 fp32/int ops, with no fp64
-// (the fp64 ray setup fixes the fractions to ~1e-16; the increments add < 2^-33 voxel per
-// slice, < 1.2e-7 voxel over 1024 slices).  Entry and exit inside a slice (through the x
-// or z faces, or the far y face) clamp the slice to [s_lo, s_hi]; segments outside it get
-// zero length (their voxel may lie one cell outside the block: in the neighbouring row /
-// block or in the buffer slack, read or scattered with weight 0).
+// line x(s) = x_p + kx s, z(s) = z_p + kz s (|kx|, |kz| < 1 for "non-steep" rays), so each
+// slice holds at most one x- and one z-plane crossing.  Per lane and axis the distance to
+// the next plane (of the coordinate mirrored so that it increases) is a 64-bit fixed-point
+// integer D in 2^-64 voxel, decremented by K = |k| 2^64 per slice: the plane is crossed
+// inside the slice iff the subtraction borrows, at u = D / K of the slice (I2F.U64 + FMUL,
+// <= 1.5 ulp).  The integer cell is never stored: the voxel offset o advances by the axis
+// stride on a borrow.  No fp64 and no division in the loop; the fp64 ray setup fixes D and
+// K to ~1e-16 and the stepping drifts < 2^-54 voxel over 1024 slices.  (A 32-bit fraction
+// was too coarse: for a small slope k an error dx in position moves the crossing by dx/k.)
+// FP and BP take whole slices: the part of a slice outside the block (entry / exit through
+// an x or z face) lies in the padded copies' zero border (BlockDesc); COUNT clamps exactly.
 //
 // Rays with |kx| or |kz| >= 1 (or parallel to the slices) can cross one axis twice in a
 // slice.  A warp containing such a lane is left to the v2 kernel (launched second, it skips
 // every warp this kernel handled), so both decide "steep" with the same predicate.
+
 // One slice's three gathers, predicated inside PTX on the lane's slice range
 // (rel <= nk, unsigned; no branch).  Without a crossing o1 = o2 = o (an L1 hit) and the
 // segment lengths l1 = l2 = 0 exactly, so no crossing masks are needed.
