@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     double amin, amax;
     bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
     // v3 companion mode: only the warps k_project3 leaves (a lane with a steep ray)
-    if (STEEP_ONLY && !__any_sync(0xffffffffu, hit && steep3)) return;
+    if (STEEP_ONLY && !__any_sync(0xffffffffu, hit && (steep3 || amin == 0.0 || amax == 1.0))) return;
     float rs = 0.f;
     if (MODE == PROJ_BP) {
         if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
@@ -423,7 +423,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     for (int c = 0; c < 3; ++c) inv[c] = (b[c] != 0.0) ? 1.0 / b[c] : 0.0;
     double amin, amax;
     bool hit = inrect && clip(a, b, inv, lo, hi, amin, amax);
-    if (__any_sync(0xffffffffu, hit && lane_steep(b))) return;   // the v2 kernel takes this warp
+    // the v2 kernel takes this warp if a lane's ray is steep or starts / ends inside the box
+    // (source or detector within the block: no face to exit through, the zero border would
+    // not absorb the rest of the slice)
+    if (__any_sync(0xffffffffu, hit && (lane_steep(b) || amin == 0.0 || amax == 1.0))) return;
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     float rs = 0.f;
     if (MODE == PROJ_BP) {

@@ -140,6 +140,35 @@ def test_operator_parity_laminography_octants(bs, tilt):
 
 
 @pytest.mark.parametrize("name,kw", [("cfg1", {}), ("cfg3", dict(K=64, n_views=40))])
+def _divisors(n):
+    return [d for d in range(1, n + 1) if n % d == 0]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_operator_parity_fuzz(bs, seed):
+    """Random small problems: beam (parallel / fan / cone), volume and block grid (any
+    divisors, not only z-slabs), detector size and pitch, orbit arc and view count (with
+    axis-aligned and 45-degree views, where ties and steep rays occur) - FP and BP per ray /
+    voxel against the oracle on every block."""
+    rng = np.random.default_rng(1000 + seed)
+    beam = ["parallel", "fan", "cone"][seed % 3]
+    nx, ny = int(rng.integers(6, 33)), int(rng.integers(6, 33))
+    nz = 1 if beam == "fan" else int(rng.integers(2, 25))
+    nu = int(rng.integers(5, 48))
+    nv = 1 if beam == "fan" else int(rng.integers(2, 30))
+    nviews = int(rng.integers(3, 10))
+    arc = [180.0, 360.0, 90.0][int(rng.integers(0, 3))]
+    OP = float(rng.uniform(1.2, 4.0)) * max(nx, ny)
+    OD = float(rng.uniform(0.5, 2.0)) * max(nx, ny)
+    pu, pv = float(rng.uniform(0.6, 2.5)), float(rng.uniform(0.6, 2.5))
+    vecs = synth.circular(beam, nviews, arc, OP, OD, nu, nv, pu, pv)
+    if seed % 4 == 3:   # force a 45-degree view
+        vecs = np.concatenate([vecs, synth.circular(beam, 8, 360.0, OP, OD, nu, nv, pu, pv)[1:2]])
+    g = synth.Geometry(synth.BEAM_NAMES[beam], vecs, nu, nv, (nx, ny, nz))
+    blocks = tuple(int(rng.choice(_divisors(n)[:3])) for n in (nx, ny, nz))
+    _fp_bp_check(bs, g, blocks, 1, np.arange(g.n_views), range(blocks[0] * blocks[1] * blocks[2]), seed=seed)
+
+
 def test_visit_counts(bs, name, kw):
     """The visit table behind the intersections/s metric (COUNT traversal: in-block
     segments longer than 1e-6 of a slice) against the oracle's a_ij over the epoch's
