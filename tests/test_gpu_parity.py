@@ -166,7 +166,14 @@ def test_operator_parity_fuzz(bs, seed):
         vecs = np.concatenate([vecs, synth.circular(beam, 8, 360.0, OP, OD, nu, nv, pu, pv)[1:2]])
     g = synth.Geometry(synth.BEAM_NAMES[beam], vecs, nu, nv, (nx, ny, nz))
     blocks = tuple(int(rng.choice(_divisors(n)[:3])) for n in (nx, ny, nz))
-    _fp_bp_check(bs, g, blocks, 1, np.arange(g.n_views), range(blocks[0] * blocks[1] * blocks[2]), seed=seed)
+    rects = None
+    if seed % 2:   # IM-style detector rectangles (one per view)
+        rects = []
+        for _ in range(g.n_views):
+            u0 = int(rng.integers(0, nu)); v0 = int(rng.integers(0, nv))
+            rects.append((u0, int(rng.integers(u0 + 1, nu + 1)), v0, int(rng.integers(v0 + 1, nv + 1))))
+    _fp_bp_check(bs, g, blocks, 1, np.arange(g.n_views), range(blocks[0] * blocks[1] * blocks[2]), rects=rects,
+                 seed=seed)
 
 
 def test_visit_counts(bs, name, kw):
