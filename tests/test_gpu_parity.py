@@ -459,3 +459,56 @@ def test_host_buffer_run_matches_device_run(bs, pinned):
     assert np.allclose(r0.obj, r1.obj, rtol=1e-5, atol=0)
     assert np.max(np.abs(x0r - x1r)) <= 1e-5 * np.max(np.abs(x0r))
 
+
+@pytest.mark.parametrize("seed", range(8))
+def test_trajectory_fuzz(bs, seed):
+    """Random small BSGD runs through bsgd_run: geometry, block grid, M, alpha M, gamma N
+    and the flag set (IS / RAN / TV / AUTO_MU / SGD) drawn at random; selections, mu
+    decisions, objective and x against the oracle over 8 epochs."""
+    rng = np.random.default_rng(500 + seed)
+    cone = seed % 2 == 0
+    n = int(rng.choice([8, 12, 16]))
+    dims = (n, n, n if cone else 1)
+    nviews = int(rng.integers(8, 20))
+    nu = int(rng.integers(n, 2 * n))
+    nv = int(rng.integers(n // 2, n + 1)) if cone else 1
+    beam = "cone" if cone else "fan"
+    vecs = synth.circular(beam, nviews, 360.0, 3.0 * n, 2.0 * n, nu, nv, 1.5, 1.5)
+    g = synth.Geometry(synth.BEAM_NAMES[beam], vecs, nu, nv, dims)
+    blocks = (1, 1, int(rng.choice([2, 4]))) if cone else (int(rng.choice([1, 2])), int(rng.choice([2, 4])), 1)
+    N = blocks[0] * blocks[1] * blocks[2]
+    M = int(rng.integers(2, 5))
+    aM, gN = int(rng.integers(1, M + 1)), int(rng.integers(1, N + 1))
+    tiles = (1, 2) if cone else (2, 1)
+    flags, okw, rkw = 0, {}, {}
+    pick = int(rng.integers(0, 5))
+    if pick == 1:
+        flags, okw = bs.IS, dict(im=True)
+    elif pick == 2:
+        flags, okw = bs.IS | bs.IS_UNIFORM, dict(im=True, im_uniform=True)
+    elif pick == 3:
+        flags, okw, rkw = bs.TV | bs.AUTO_MU, dict(tv=True, auto_mu=True, lam=0.05), dict(lam=0.05, tv_iters=20)
+    elif pick == 4:
+        flags, okw = bs.SGD, dict(sgd=True)
+    vol = synth.rasterise(synth.ellipsoids_world("shepp3d" if cone else "shepp2d", dims), dims).astype(np.float32)
+    P = Projector(g, BlockGrid(dims, blocks))
+    xb = P.grid.to_blocks(vol.astype(np.float64))
+    y = np.zeros(g.n_rays)
+    for j in range(N):
+        P.fp(np.arange(g.n_views), j, xb[j], proj=y, accumulate=True)
+    y = y.astype(np.float32)
+    mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
+    prm = ob.Params(seed=seed + 1, mu=mu, rows_per_epoch=aM, cols_per_epoch=gN, total_epochs=8, **okw)
+    o = ob.OracleBSGD(g, blocks, M, y.astype(np.float64), prm, row_kind="random", row_seed=seed + 3, tiles=tiles,
+                      x_true=xb)
+    for _ in range(8):
+        o.epoch()
+    ctx = bs.Context.from_geometry(g, blocks, M, kind="random", row_seed=seed + 3, tiles=tiles)
+    xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    res = ctx.run(torch.from_numpy(y).cuda(), xd, epochs=8, mu0=mu, seed=seed + 1,
+                  x_true=torch.from_numpy(xb.ravel().astype(np.float32)).cuda(), rows_per_epoch=aM,
+                  cols_per_epoch=gN, flags=flags, **rkw)
+    xg = xd.cpu().numpy().astype(np.float64)
+    ctx.close()
+    print(seed, beam, dims, blocks, "M", M, "aM", aM, "gN", gN, "flags", flags, _compare(o, res, xg, sgd=bool(flags & bs.SGD)))
+
