@@ -139,7 +139,6 @@ def test_operator_parity_laminography_octants(bs, tilt):
     _fp_bp_check(bs, g, (2, 2, 2), 4, np.arange(16), range(8))
 
 
-@pytest.mark.parametrize("name,kw", [("cfg1", {}), ("cfg3", dict(K=64, n_views=40))])
 def _divisors(n):
     return [d for d in range(1, n + 1) if n % d == 0]
 
@@ -176,6 +175,7 @@ def test_operator_parity_fuzz(bs, seed):
                  seed=seed)
 
 
+@pytest.mark.parametrize("name,kw", [("cfg1", {}), ("cfg3", dict(K=64, n_views=40))])
 def test_visit_counts(bs, name, kw):
     """The visit table behind the intersections/s metric (COUNT traversal: in-block
     segments longer than 1e-6 of a slice) against the oracle's a_ij over the epoch's
