@@ -163,6 +163,8 @@ def test_operator_parity_fuzz(bs, seed):
     vecs = synth.circular(beam, nviews, arc, OP, OD, nu, nv, pu, pv)
     if seed % 4 == 3:   # force a 45-degree view
         vecs = np.concatenate([vecs, synth.circular(beam, 8, 360.0, OP, OD, nu, nv, pu, pv)[1:2]])
+    if seed % 5 == 4 and beam == "cone":   # a laminography orbit (tilted beam, steep rays)
+        vecs = synth.laminography(nviews, float(rng.uniform(10.0, 50.0)), OP, OD, nu, nv, pu, pv)
     g = synth.Geometry(synth.BEAM_NAMES[beam], vecs, nu, nv, (nx, ny, nz))
     blocks = tuple(int(rng.choice(_divisors(n)[:3])) for n in (nx, ny, nz))
     rects = None
