@@ -83,6 +83,7 @@ class ClockSampler:
         self.index = index
         self.rows = []            # (sm_mhz, max_mhz, reasons set, util %)
         self._stop = threading.Event()
+        self._ready = threading.Event()   # set once the sampler runs (short timed regions)
         self._t = None
         self.source = "none"
 
@@ -98,6 +99,7 @@ class ClockSampler:
                 self.rows.append((float(sm), float(mx), {n for n, b in bits if ev & b}, util))
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.02)
 
     def _run_smi(self):
@@ -113,6 +115,7 @@ class ClockSampler:
                     self.rows.append((float(r[0]), float(r[1]), act, int(r[6]) if r[6].isdigit() else 100))
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def _run(self):
@@ -128,6 +131,7 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(timeout=5.0)
         return self
 
     def __exit__(self, *a):
@@ -255,6 +259,10 @@ def run_ours(args, rank, world, local_rank):
     # below 1/sigma_max^2 (Rayleigh lower bounds of sigma_max^2)
     mu0 = 0.25 / {"cfg1": 5451.0, "cfg2": 9.09e4, "cfg3": 8.93e4, "cfg4": 3.59e5}.get(args.config, 7.35e5)
     aM, gN = p.rows_per_epoch, p.cols_per_epoch
+    # cfg4's schedule: BSGD-TV (Algo 4, lambda = 0.1; period
+    # round(1/(alpha gamma)) = 40 epochs) + automatic mu (Algo 3)
+    sched = (bs.TV | bs.AUTO_MU) if args.config == "cfg4" else 0
+    lam = 0.1
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -263,7 +271,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     # warm-up epochs (untimed; also builds/initialises everything)
-    ctx.run(y, x, epochs=args.warmup, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN)
+    ctx.run(y, x, epochs=args.warmup, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN, flags=sched, lam=lam)
     launches0 = bs.kernel_launches()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -271,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         ev0.record(stream)
         res = ctx.run(y, x, epochs=args.steps, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN,
-                      flags=bs.RESUME | bs.TIMING)
+                      flags=sched | bs.RESUME | bs.TIMING, lam=lam)
         ev1.record(stream)
         barrier()
     launches = bs.kernel_launches() - launches0
@@ -308,12 +316,13 @@ def run_ours(args, rank, world, local_rank):
         yh = y.cpu().pin_memory()
         xh = torch.zeros(n_owned, dtype=torch.float32).pin_memory()
         # untimed warm-up of the host-buffer path (one-time staging allocations, copy stream)
-        ctx.run(yh, xh, epochs=1, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN)
+        ctx.run(yh, xh, epochs=1, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN, flags=sched, lam=lam)
         xh.zero_()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ctx.run(yh, xh, epochs=args.steps, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN)
+        ctx.run(yh, xh, epochs=args.steps, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN, flags=sched,
+                lam=lam)
         e1.record(stream)
         barrier()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -325,6 +334,9 @@ def run_ours(args, rank, world, local_rank):
                "what": ("bsgd_run(y, x on pinned host memory): y and x uploaded (on a copy stream, "
                         "overlapped with the first epoch), K epochs, x copied back")}
         del yh, xh
+    tv = None
+    if not args.no_tv:
+        tv = time_tv(bs, ctx, x, mu0 * lam, p, aM, gN, world, stream, t_ms / args.steps, peak)
     ctx.close()
     if rank != 0:
         return 0
@@ -360,6 +372,7 @@ def run_ours(args, rank, world, local_rank):
                      "fp_frac": (4.0 * vis_ep / (fp_ms / 1e3) / 1e9) / peak,
                      "bp_frac": (8.0 * vis_ep / (bp_ms / 1e3) / 1e9) / peak,
                      "fp_plus_bp_frac": (12.0 * vis_ep / ((fp_ms + bp_ms) / 1e3) / 1e9) / peak},
+        "tv_prox": tv,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "e2e": e2e,
@@ -367,6 +380,44 @@ def run_ours(args, rank, world, local_rank):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def time_tv(bs, ctx, x, w, p, aM, gN, world, stream, epoch_ms, peak, iters=20, calls=3):
+    """The TV proximal call of Algo 4 line 16 on this rank's owned volume,
+    timed on its own (CUDA events on the launch stream, max over ranks): 20 FGP iterations.
+    Algorithmic HBM bytes per call: per iteration read q (3), p (3), b and write q, p
+    (13 floats = 52 B per voxel), plus the set-up (copy x -> b, zero p and q: 32 B) and the
+    final x = b - w grad^T p (read b, 3 p, write x: 20 B)."""
+    import torch
+    import torch.distributed as dist
+    xt = x.clone()
+    ctx.tv_prox(xt, w, iters)                  # untimed: allocates the dual fields
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = bs.kernel_launches()
+    e0.record(stream)
+    for _ in range(calls):
+        ctx.tv_prox(xt, w, iters)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = (bs.kernel_launches() - l0) // calls
+    t = torch.tensor([e0.elapsed_time(e1) / calls], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    n = x.numel()
+    nbytes = n * (52.0 * iters + 32.0 + 20.0)
+    period = max(1, round(p.M * p.N / (aM * gN)))
+    del xt
+    return {"ms_per_call": ms, "iters": iters, "w": w, "voxels_per_rank": n, "launches_per_call": int(launches),
+            "kernel": "k_tv_fgp4 (fused FGP iteration, float4) x iters + k_tv_out" if p.blocks[:2] == (1, 1)
+            else "k_tv_u + k_tv_pq per iteration + k_tv_u",
+            "algorithmic_bytes": f"{nbytes:.4g} B per call (52 B per voxel per FGP iteration + 52 B set-up/final)",
+            "achieved_gbs": nbytes / (ms / 1e3) / 1e9, "frac": nbytes / (ms / 1e3) / 1e9 / peak,
+            "period_epochs": period,
+            "epochs_per_s_tv_amortised": 1e3 / (epoch_ms + ms / period)}
 
 
 def main():
@@ -378,6 +429,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-tv", action="store_true", help="skip the separate TV-prox timing")
     ap.add_argument("--cheap-data", action="store_true", help="uniform random y instead of analytic projections")
     ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="workload (cfg5 = the BASELINE.json headline; the others for DESIGN tables)")

@@ -223,6 +223,16 @@ bsgd_status bsgd_set_state(bsgd_ctx ctx, int32_t what, int32_t index, const void
 bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, double* sigma_max_sq,
                                  void* stream);
 
+/* TV proximal step (Algo 4 line 16; TV of Eq. 5-6):
+ * x_owned <- argmin_t 1/2 ||t - x_owned||^2 + w TV(t), by `iters` cold-start FGP iterations
+ * on the dual (reading A16; the same call bsgd_run makes every tv_period epochs, with
+ * w = mu lambda).  TV is the isotropic backward-difference TV of Eq. 6 over the WHOLE volume
+ * (zero difference at index 0).  x_owned: device, this rank's owned blocks, block-major (the
+ * layout of bsgd_run's x_owned), modified in place; enqueued on `stream`.  Collective when
+ * world > 1 (z-slab halo planes by ncclSend/Recv; every rank calls it).  w = 0 or iters = 0
+ * leaves x unchanged.  Errors: BSGD_E_CONTRACT for NULL x, w < 0 or iters < 0.          */
+bsgd_status bsgd_tv_prox(bsgd_ctx ctx, float* x_owned, double w, int32_t iters, void* stream);
+
 /* Comparison solvers on the same operators (the methods the paper
  * compares against in Figs. 12 and 18, cited but not listed
  * there; the textbook forms are in oracle/solvers.py).  With g(x) = 2 A^T (y - A x)

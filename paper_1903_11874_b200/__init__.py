@@ -131,6 +131,7 @@ SIGS = {
     "bsgd_get_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
+    "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_void_p], C.c_int),
     "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
                    C.c_int),
 }
@@ -410,6 +411,12 @@ class Context:
         dt = np.float64 if what in (4, 5) else np.float32
         a = np.ascontiguousarray(arr, dtype=dt)
         self._c(_lib.bsgd_set_state(self.h, what, index, a.ctypes.data, a.nbytes))
+
+    def tv_prox(self, x, w, iters=20, stream=None):
+        """x (CUDA float32, the owned blocks block-major) <- prox_{w TV}(x) in place by
+        `iters` FGP iterations (bsgd_tv_prox; Algo 4 line 16)."""
+        self._c(_lib.bsgd_tv_prox(self.h, _ptr(x), float(w), int(iters), _stream(stream)))
+        return x
 
     def power_iteration(self, iters=30, seed=0, stream=None) -> float:
         out = C.c_double()

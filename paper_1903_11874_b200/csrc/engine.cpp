@@ -74,7 +74,7 @@ struct bsgd_ctx_s {
     float *accN = nullptr, *accT = nullptr, *pc = nullptr;
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
-          *tv_b = nullptr;
+          *tv_b = nullptr, *tv_q2 = nullptr, *tv_hp = nullptr;
     float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
@@ -791,14 +791,21 @@ struct bsgd_ctx_s {
 
     void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st) {
         const long long n = (long long)s * bsize;
-        if (!tv_u) {
-            tv_u = dnew<float>(n, false);
+        // z-slab layouts (the owned volume is one [z][y][x] array) take the fused iteration
+        const bool fused = bgrid[0] == 1 && bgrid[1] == 1;
+        const long long plane = (long long)dims[0] * dims[1];
+        if (!tv_p) {
             tv_p = dnew<float>(3 * n, false);
             tv_q = dnew<float>(3 * n, false);
             tv_b = dnew<float>(n, false);
-            long long plane = (long long)dims[0] * dims[1];
             tv_hq = dnew<float>(plane);
-            tv_hu = dnew<float>(plane);
+            if (fused) {
+                tv_q2 = dnew<float>(3 * n, false);
+                tv_hp = dnew<float>(4 * plane);
+            } else {
+                tv_u = dnew<float>(n, false);
+                tv_hu = dnew<float>(plane);
+            }
         }
         if (wgt == 0.0 || iters <= 0) return;
         BSGD_CUDA(cudaMemcpyAsync(tv_b, x_owned, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
@@ -824,8 +831,32 @@ struct bsgd_ctx_s {
         Tl.n = n;
         Tl.z0 = first * bd[2];
         Tl.z1 = (first + s) * bd[2];
-        const long long plane = (long long)dims[0] * dims[1];
         double sk = 1.0;
+        if (fused) {
+            Tl.halo_prev = tv_hp;
+            halo_exchange(tv_b + n - plane, tv_hp + 3 * plane, plane, false, st);   // b of plane z0-1
+            float *qa = tv_q, *qb = tv_q2;
+            for (int it = 0; it < iters; ++it) {
+                const double sk1 = (1.0 + sqrt(1.0 + 4.0 * sk * sk)) / 2.0;
+                Tl.beta = (sk - 1.0) / sk1;
+                for (int c = 0; c < 3; ++c)       // q of plane z0-1 from the previous rank
+                    halo_exchange(qa + c * n + n - plane, tv_hp + c * plane, plane, false, st);
+                halo_exchange(qa + 2 * n, tv_hq, plane, true, st);   // q_z of plane z1 from the next
+                Tl.q = qa;
+                Tl.q_out = qb;
+                Tl.wf = (float)wgt;
+                Tl.sf = (float)(1.0 / (Tl.L * wgt));
+                Tl.betaf = (float)Tl.beta;
+                launch_tv_fgp(Tl, st);
+                std::swap(qa, qb);
+                sk = sk1;
+            }
+            halo_exchange(tv_p + 2 * n, tv_hq, plane, true, st);
+            Tl.q = tv_p;
+            Tl.wf = (float)wgt;
+            launch_tv_out(Tl, x_owned, st);
+            return;
+        }
         for (int it = 0; it < iters; ++it) {
             const double sk1 = (1.0 + sqrt(1.0 + 4.0 * sk * sk)) / 2.0;
             Tl.beta = (sk - 1.0) / sk1;
@@ -1594,6 +1625,13 @@ bsgd_status bsgd_set_state(bsgd_ctx c, int32_t what, int32_t index, const void* 
         if (bytes != need) fail(BSGD_E_DIMENSION, "size mismatch");
         BSGD_CUDA(cudaDeviceSynchronize());
         BSGD_CUDA(cudaMemcpy(dst, src, need, cudaMemcpyHostToDevice));
+    });
+}
+
+bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, void* stream) {
+    return guard(c, [&] {
+        if (!c || !x_owned || !(w >= 0.0) || iters < 0) fail(BSGD_E_CONTRACT, "bad arguments");
+        c->tv_prox(x_owned, w, iters, S(stream));
     });
 }
 

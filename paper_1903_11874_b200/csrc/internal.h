@@ -169,6 +169,9 @@ struct TvLaunch {
     float* out;         // output image
     const float* halo_q_next;  // q plane z1 (3 comps) or NULL
     const float* halo_u_prev;  // u plane z0-1 or NULL
+    float* q_out;              // fused FGP: the next q (3 * owned; q is read-only then)
+    const float* halo_prev;    // fused FGP: qx, qy, qz, b of plane z0-1 (4 planes) or NULL
+    float wf, sf, betaf;       // fused FGP in fp32: w, 1/(L w), beta
     double w;           // weight mu*lambda
     double L;           // Lipschitz bound 4*(#axes > 1)
     double beta;        // FISTA momentum (s_k - 1)/s_{k+1}
@@ -176,5 +179,10 @@ struct TvLaunch {
 };
 void launch_tv_u(const TvLaunch& T, const float* src_q, float* dst, cudaStream_t st);
 void launch_tv_pq(const TvLaunch& T, cudaStream_t st);
+// One fused FGP iteration (u, projection, momentum) for z-slab layouts (bgrid = 1 x 1 x N):
+// reads q, p, b (+ halos), writes q_out, p.
+void launch_tv_fgp(const TvLaunch& T, cudaStream_t st);
+// x = b - w grad^T q (T.q = the final p) for z-slab layouts
+void launch_tv_out(const TvLaunch& T, float* out, cudaStream_t st);
 
 }  // namespace bsgd

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // HBM-streaming kernels of the hot path:
 //  * k_block_update: g_hat / g / x step of Algo 1 lines 11-14
 //    fused with the combination of the two BP accumulators (normal + transposed
@@ -448,6 +449,243 @@ __global__ void __launch_bounds__(256) k_tv_pq(const TvLaunch T) {
     }
 }
 
+// Fused FGP iteration for z-slab layouts (the owned volume is one [z][y][x] array of planes
+// z0..z1-1).  Same arithmetic as k_tv_u + k_tv_pq (Beck-Teboulle FGP):
+//   u = b - w grad^T q;  p1 = P(q + grad(u) / (L w));  q_out = p1 + beta (p1 - p);  p = p1
+// without storing u: one thread per voxel, a 32 x 8 CTA per plane tile; u of x-1 comes from
+// the neighbouring lane (shuffle), of y-1 from the row above (shared memory), and u of z-1 is
+// evaluated directly (its q / b planes are L2 hits: the CTAs of plane z-1 just read them);
+// tile-edge threads evaluate their halo u directly.  All loads of a thread are independent
+// and issued together (a z-marching variant with one barrier per plane was latency-bound at
+// 2.1 TB/s).  HBM per voxel: read q (3), p (3), b; write q_out (3), p (3) = 52 B.  q is
+// double-buffered (q -> q_out) because neighbouring tiles read q around their edges.
+constexpr int TV_TX = 32, TV_TY = 16;
+
+struct TvPlane {
+    const float *qx, *qy, *qz, *b;   // plane z (qx, qy, qz, b), indexed y * nx + x
+    const float* qz1;                // q_z of plane z + 1
+};
+
+__device__ __forceinline__ TvPlane tv_plane(const TvLaunch& T, int z) {
+    const long long plane = (long long)T.dims[0] * T.dims[1];
+    TvPlane P;
+    if (z < T.z0) {                  // previous rank's last plane (only read when z >= 0)
+        P.qx = T.halo_prev;
+        P.qy = T.halo_prev + plane;
+        P.qz = T.halo_prev + 2 * plane;
+        P.b = T.halo_prev + 3 * plane;
+        P.qz1 = T.q + 2 * T.n;       // own first plane (z + 1 = z0)
+    } else {
+        const long long off = (long long)(z - T.z0) * plane;
+        P.qx = T.q + off;
+        P.qy = T.q + T.n + off;
+        P.qz = T.q + 2 * T.n + off;
+        P.b = T.b + off;
+        P.qz1 = (z + 1 < T.z1) ? P.qz + plane : T.halo_q_next;   // next rank's first plane
+    }
+    return P;
+}
+
+// u at (x, y) of plane z: b - w grad^T q with the zero-boundary adjoint of Eq. 6 (fp32: the
+// dual fields are stored in fp32 anyway; the oracle parity margin is ~100x)
+__device__ __forceinline__ float tv_u_at(const TvLaunch& T, const TvPlane& P, int x, int y, int z, float w) {
+    const int i = y * T.dims[0] + x;
+    float t = 0.f;
+    if (x >= 1) t += P.qx[i];
+    if (x + 1 < T.dims[0]) t -= P.qx[i + 1];
+    if (y >= 1) t += P.qy[i];
+    if (y + 1 < T.dims[1]) t -= P.qy[i + T.dims[0]];
+    if (z >= 1) t += P.qz[i];
+    if (z + 1 < T.dims[2]) t -= P.qz1[i];
+    return fmaf(-w, t, P.b[i]);
+}
+
+// CTA = a TV_TX x TV_TY output tile of one plane plus helper threads for the u halo
+// (row y0-1 and column x0-1), so that no output warp diverges on a halo evaluation.
+constexpr int TV_OUT = TV_TX * TV_TY, TV_HALO = TV_TX + TV_TY;
+constexpr int TV_THREADS = (TV_OUT + TV_HALO + 31) / 32 * 32;
+
+template <int ZT>
+__global__ void __launch_bounds__(TV_THREADS, ZT == 1 ? 3 : (ZT == 2 ? 2 : 1)) k_tv_fgp(const TvLaunch T) {
+    __shared__ float su[ZT][TV_TY + 1][TV_TX + 1];
+    const int t = threadIdx.x;
+    int tx, ty;                              // slot in su: (ty + 1, tx + 1) <-> voxel (x0 + tx, y0 + ty)
+    if (t < TV_OUT) { tx = t % TV_TX; ty = t / TV_TX; }
+    else if (t < TV_OUT + TV_TX) { tx = t - TV_OUT; ty = -1; }
+    else if (t < TV_OUT + TV_HALO) { tx = -1; ty = t - TV_OUT - TV_TX; }
+    else { tx = TV_TX; ty = TV_TY; }         // idle padding thread (outside the tile, x or y invalid)
+    const int x = blockIdx.x * TV_TX + tx, y = blockIdx.y * TV_TY + ty, zb = T.z0 + blockIdx.z * ZT;
+    const bool inside = x >= 0 && y >= 0 && x < T.dims[0] && y < T.dims[1] && tx < TV_TX && ty < TV_TY;
+    const bool out = inside && t < TV_OUT;
+    const float w = T.wf;
+    const long long plane = (long long)T.dims[0] * T.dims[1];
+    const long long i0 = (long long)(zb - T.z0) * plane + (long long)y * T.dims[0] + x;
+    // every load of the thread is independent: issue all of them before the barrier
+    float u[ZT + 1], qx[ZT], qy[ZT], qz[ZT], ox[ZT], oy[ZT], oz[ZT];
+    u[0] = 0.f;
+    if (out && zb >= 1) u[0] = tv_u_at(T, tv_plane(T, zb - 1), x, y, zb - 1, w);
+#pragma unroll
+    for (int k = 0; k < ZT; ++k) {
+        const bool pin = zb + k < T.z1;
+        u[k + 1] = 0.f;
+        if (inside && pin) u[k + 1] = tv_u_at(T, tv_plane(T, zb + k), x, y, zb + k, w);
+        const long long i = i0 + k * plane;
+        if (out && pin) {
+            qx[k] = T.q[i];
+            qy[k] = T.q[T.n + i];
+            qz[k] = T.q[2 * T.n + i];
+            ox[k] = T.p[i];
+            oy[k] = T.p[T.n + i];
+            oz[k] = T.p[2 * T.n + i];
+        }
+        if (inside) su[k][ty + 1][tx + 1] = u[k + 1];
+    }
+    __syncthreads();
+    if (!out) return;
+    const float s = T.sf, beta = T.betaf;
+#pragma unroll
+    for (int k = 0; k < ZT; ++k) {
+        const int z = zb + k;
+        if (z >= T.z1) break;
+        const float uo = u[k + 1];
+        const float p0x = qx[k] + (x >= 1 ? uo - su[k][ty + 1][tx] : 0.f) * s;
+        const float p0y = qy[k] + (y >= 1 ? uo - su[k][ty][tx + 1] : 0.f) * s;
+        const float p0z = qz[k] + (z >= 1 ? uo - u[k] : 0.f) * s;
+        const float n2 = p0x * p0x + p0y * p0y + p0z * p0z;
+        const float inv = n2 > 1.f ? rsqrtf(n2) : 1.f;      // projection onto |p| <= 1
+        const float px = p0x * inv, py = p0y * inv, pz = p0z * inv;
+        const long long i = i0 + k * plane;
+        T.q_out[i] = px + beta * (px - ox[k]);
+        T.q_out[T.n + i] = py + beta * (py - oy[k]);
+        T.q_out[2 * T.n + i] = pz + beta * (pz - oz[k]);
+        T.p[i] = px;
+        T.p[T.n + i] = py;
+        T.p[2 * T.n + i] = pz;
+    }
+}
+
+// Vectorised fused FGP iteration (nx % 4 == 0): each thread owns 4 consecutive x voxels and
+// moves them with 16-byte loads / stores (the scalar kernel above tops out near 3.5 TB/s on
+// request count).  CTA = TV4_TY rows x 128 x of one plane + one warp for the halo row y0-1
+// (vectors) + TV4_TY lanes for the halo column x0-1 (scalars).  Within a vector the x
+// difference is local; across lanes it comes by shuffle, at lane 0 from the halo column.
+constexpr int TV4_TX = 128;
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+    *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+
+// u at the 4 voxels (x..x+3, y) of plane z (x % 4 == 0); all lanes of the warp must call it
+// (the qx(x+4) neighbour comes from the next lane)
+__device__ __forceinline__ void tv_u4(const TvLaunch& T, const TvPlane& P, int x, int y, int z, bool act,
+                                      float w, float u[4]) {
+    const int nx = T.dims[0];
+    const int i = y * nx + x;
+    float4 qx = make_float4(0.f, 0.f, 0.f, 0.f), qy = qx, qyn = qx, qz = qx, qz1 = qx, b = qx;
+    float qxe = 0.f;
+    if (act) {
+        qx = ld4(P.qx + i);
+        qy = ld4(P.qy + i);
+        if (y + 1 < T.dims[1]) qyn = ld4(P.qy + i + nx);
+        qz = ld4(P.qz + i);
+        if (z + 1 < T.dims[2]) qz1 = ld4(P.qz1 + i);
+        b = ld4(P.b + i);
+    }
+    float qx4 = __shfl_down_sync(0xffffffffu, qx.x, 1);
+    if ((threadIdx.x & 31) == 31 && act && x + 4 < nx) qxe = P.qx[i + 4];
+    if ((threadIdx.x & 31) == 31) qx4 = qxe;
+    if (!act) return;
+    const float qxa[5] = {qx.x, qx.y, qx.z, qx.w, x + 4 < nx ? qx4 : 0.f};
+    const float qya[4] = {qy.x, qy.y, qy.z, qy.w}, qyb[4] = {qyn.x, qyn.y, qyn.z, qyn.w};
+    const float qza[4] = {qz.x, qz.y, qz.z, qz.w}, qzb[4] = {qz1.x, qz1.y, qz1.z, qz1.w};
+    const float ba[4] = {b.x, b.y, b.z, b.w};
+    const float cy = y >= 1 ? 1.f : 0.f, cz = z >= 1 ? 1.f : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float t = (x + k >= 1 ? qxa[k] : 0.f) - qxa[k + 1];   // qxa[4] is 0 at the last column
+        t += cy * qya[k] - qyb[k] + cz * qza[k] - qzb[k];     // qyb / qzb are 0 past the boundary
+        u[k] = fmaf(-w, t, ba[k]);
+    }
+}
+
+template <int TV4_TY, int MINB>
+__global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLaunch T) {
+    constexpr int RS = TV4_TX + 8;                 // row stride (16-byte aligned rows)
+    __shared__ __align__(16) float su[TV4_TY + 1][RS];   // slot 4 + (x - x0) <-> x; slot 3 <-> x0 - 1
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x0 = blockIdx.x * TV4_TX, y0 = blockIdx.y * TV4_TY, z = T.z0 + blockIdx.z;
+    const int nx = T.dims[0], ny = T.dims[1];
+    const float w = T.wf;
+    const TvPlane P = tv_plane(T, z);
+    if (warp > TV4_TY) {                           // halo column x0 - 1 (scalars), rows y0 .. y0+TY-1
+        const int y = y0 + lane;
+        if (lane < TV4_TY && x0 >= 1 && y < ny) su[lane + 1][3] = tv_u_at(T, P, x0 - 1, y, z, w);
+        __syncthreads();
+        return;
+    }
+    const int row = warp;                          // 0 = halo row y0 - 1, 1.. = output rows
+    const int y = y0 + row - 1, x = x0 + 4 * lane;
+    const bool act = y >= 0 && y < ny && x < nx;
+    const bool out = act && row >= 1;
+    float u[4], uz[4] = {0.f, 0.f, 0.f, 0.f};
+    tv_u4(T, P, x, y, z, act, w, u);
+    const long long plane = (long long)nx * ny;
+    const long long i = (long long)(z - T.z0) * plane + (long long)y * nx + x;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, p0 = q0, p1 = q0, p2 = q0;
+    if (row >= 1) {
+        if (z >= 1) tv_u4(T, tv_plane(T, z - 1), x, y, z - 1, out, w, uz);
+        if (out) {
+            q0 = ld4(T.q + i);
+            q1 = ld4(T.q + T.n + i);
+            q2 = ld4(T.q + 2 * T.n + i);
+            p0 = ld4(T.p + i);
+            p1 = ld4(T.p + T.n + i);
+            p2 = ld4(T.p + 2 * T.n + i);
+        }
+    }
+    if (act) *reinterpret_cast<float4*>(&su[row][4 + 4 * lane]) = make_float4(u[0], u[1], u[2], u[3]);
+    const float ul = __shfl_up_sync(0xffffffffu, u[3], 1);
+    __syncthreads();
+    if (!out) return;
+    const float uxm = lane > 0 ? ul : su[row][3];   // u(x - 1)
+    const float4 up = *reinterpret_cast<const float4*>(&su[row - 1][4 + 4 * lane]);
+    const float upa[4] = {up.x, up.y, up.z, up.w};
+    const float qa[3][4] = {{q0.x, q0.y, q0.z, q0.w}, {q1.x, q1.y, q1.z, q1.w}, {q2.x, q2.y, q2.z, q2.w}};
+    const float pa[3][4] = {{p0.x, p0.y, p0.z, p0.w}, {p1.x, p1.y, p1.z, p1.w}, {p2.x, p2.y, p2.z, p2.w}};
+    const float s = T.sf, beta = T.betaf;
+    float qo[3][4], po[3][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float left = k == 0 ? uxm : u[k - 1];
+        const float gx = x + k >= 1 ? u[k] - left : 0.f;
+        const float gy = y >= 1 ? u[k] - upa[k] : 0.f;
+        const float gz = z >= 1 ? u[k] - uz[k] : 0.f;
+        const float a0 = qa[0][k] + gx * s, a1 = qa[1][k] + gy * s, a2 = qa[2][k] + gz * s;
+        const float n2 = a0 * a0 + a1 * a1 + a2 * a2;
+        const float inv = n2 > 1.f ? rsqrtf(n2) : 1.f;
+        po[0][k] = a0 * inv;
+        po[1][k] = a1 * inv;
+        po[2][k] = a2 * inv;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) qo[c][k] = po[c][k] + beta * (po[c][k] - pa[c][k]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        st4(T.q_out + c * T.n + i, qo[c][0], qo[c][1], qo[c][2], qo[c][3]);
+        st4(T.p + c * T.n + i, po[c][0], po[c][1], po[c][2], po[c][3]);
+    }
+}
+
+// x = b - w grad^T p on a z-slab layout (the final step of the prox): one thread per voxel
+__global__ void __launch_bounds__(TV_TX * TV_TY) k_tv_out(const TvLaunch T, float* out) {
+    const int x = blockIdx.x * TV_TX + threadIdx.x, y = blockIdx.y * TV_TY + threadIdx.y,
+              z = T.z0 + blockIdx.z;
+    if (x >= T.dims[0] || y >= T.dims[1]) return;
+    const long long i = (long long)blockIdx.z * T.dims[0] * T.dims[1] + (long long)y * T.dims[0] + x;
+    out[i] = tv_u_at(T, tv_plane(T, z), x, y, z, T.wf);
+}
+
 unsigned grid_for(long long n, int per_thread = 1) {
     long long b = (n / per_thread + 255) / 256;
     if (b < 1) b = 1;
@@ -555,6 +793,29 @@ void launch_scale(float* v, long long n, const double* nrm, cudaStream_t st) {
 
 void launch_tv_u(const TvLaunch& T, const float* src, float* dst, cudaStream_t st) {
     k_tv_u<<<grid_for(T.n, 2), 256, 0, st>>>(T, src, dst);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_fgp(const TvLaunch& T, cudaStream_t st) {
+    if (T.dims[0] % 4 == 0) {   // float4 kernel: 4 x 128 tiles, 4 CTAs per SM (76 registers, no spills)
+        constexpr int TY = 4;
+        const dim3 g4((unsigned)((T.dims[0] + TV4_TX - 1) / TV4_TX), (unsigned)((T.dims[1] + TY - 1) / TY),
+                      (unsigned)(T.z1 - T.z0));
+        k_tv_fgp4<TY, 4><<<g4, (TY + 2) * 32, 0, st>>>(T);
+    } else {
+        const dim3 grid((unsigned)((T.dims[0] + TV_TX - 1) / TV_TX), (unsigned)((T.dims[1] + TV_TY - 1) / TV_TY),
+                        (unsigned)(T.z1 - T.z0));
+        k_tv_fgp<1><<<grid, TV_THREADS, 0, st>>>(T);
+    }
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_out(const TvLaunch& T, float* out, cudaStream_t st) {
+    const dim3 grid((unsigned)((T.dims[0] + TV_TX - 1) / TV_TX), (unsigned)((T.dims[1] + TV_TY - 1) / TV_TY),
+                    (unsigned)(T.z1 - T.z0));
+    k_tv_out<<<grid, dim3(TV_TX, TV_TY), 0, st>>>(T, out);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

@@ -514,3 +514,43 @@ def test_trajectory_fuzz(bs, seed):
     ctx.close()
     print(seed, beam, dims, blocks, "M", M, "aM", aM, "gN", gN, "flags", flags, _compare(o, res, xg, sgd=bool(flags & bs.SGD)))
 
+
+
+@pytest.mark.parametrize("dims,blocks,w,iters", [
+    ((45, 20, 36), (1, 1, 4), 0.3, 20),     # fused scalar path (nx % 4 != 0): ragged tiles, 9-plane slabs
+    ((64, 64, 64), (1, 1, 2), 0.2, 20),     # fused float4 path: partial 128-wide x tile
+    ((136, 20, 24), (1, 1, 3), 0.3, 20),    # fused float4 path: ragged x / y tiles, 3 slabs
+    ((64, 48, 1), (1, 1, 1), 0.5, 50),      # fused 2D (nz = 1, L = 8)
+    ((24, 16, 20), (2, 2, 2), 0.3, 20),     # octants: the generic two-kernel path
+])
+def test_tv_prox_parity(bs, dims, blocks, w, iters):
+    """bsgd_tv_prox (Algo 4 line 16; FGP, reading A16) per voxel against the
+    oracle's tv_prox on the same fp32 input: |d| <= 1e-5 (|b|_inf + w)."""
+    nx, ny, nz = dims
+    rng = np.random.default_rng(11)
+    vol = np.zeros((nz, ny, nx))
+    vol[nz // 4: 3 * nz // 4 + 1, ny // 3: 2 * ny // 3 + 1, nx // 5: 4 * nx // 5 + 1] = 1.0
+    vol[:, : ny // 4, : nx // 3] += 0.5
+    vol = (vol + 0.1 * rng.standard_normal(vol.shape)).astype(np.float32)
+    bx = BlockGrid(dims, blocks)
+    beam = "cone" if nz > 1 else "fan"
+    g = synth.Geometry(synth.BEAM_NAMES[beam],
+                       synth.circular(beam, 4, 360.0, 6.0 * max(dims), 4.0 * max(dims), 8, 8 if nz > 1 else 1,
+                                      1.0, 1.0), 8, 8 if nz > 1 else 1, dims)
+    ctx = bs.Context.from_geometry(g, blocks, 1)
+    x = torch.from_numpy(bx.to_blocks(vol).ravel().copy()).cuda()
+    ctx.tv_prox(x, w, iters)
+    torch.cuda.synchronize()
+    got = bx.from_blocks(x.cpu().numpy())
+    want = ob.tv_prox(vol.astype(np.float64), w, iters)
+    err = np.abs(got - want).max()
+    bar = 1e-5 * (np.abs(vol).max() + w)
+    print(f"tv_prox {dims} {blocks}: max|d| {err:.3g} (bar {bar:.3g}), max|x - b| {np.abs(want - vol).max():.3g}")
+    assert err <= bar
+    assert np.abs(want - vol).max() > 10 * bar          # the prox moved x: the check is not vacuous
+    # w = 0 and iters = 0 are the identity
+    x0 = torch.from_numpy(bx.to_blocks(vol).ravel().copy()).cuda()
+    ctx.tv_prox(x0, 0.0, iters)
+    ctx.tv_prox(x0, w, 0)
+    assert torch.equal(x0.cpu(), torch.from_numpy(bx.to_blocks(vol).ravel()))
+    ctx.close()
