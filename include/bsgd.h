@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define BSGD_ABI_VERSION 1
+#define BSGD_ABI_VERSION 2
 
 typedef struct bsgd_ctx_s* bsgd_ctx;
 
@@ -101,6 +101,13 @@ bsgd_status bsgd_geometry_circular(int32_t beam, int32_t n_views, double arc_deg
 /* SplitMix64 counter RNG (reading A3): m of n without replacement, sorted.
  * stream 0 = view partition, 1 = row blocks, 2 = column blocks, 3 = IM tiles. */
 bsgd_status bsgd_sample(uint64_t seed, int32_t stream, int32_t epoch, int32_t n, int32_t m, int32_t* out);
+/* Stratified column-block selection (BSGD_STRATIFIED, reading A31): the n
+ * blocks are cut into `strata` equal consecutive strata (the owners' block ranges) and
+ * m / strata blocks are drawn in each, by the partial Fisher-Yates of bsgd_sample over the
+ * stratum with draw counters k = s * (n / strata) + i on stream 2; out sorted.  strata = 1
+ * equals bsgd_sample(seed, 2, epoch, n, m).  Errors: strata must divide n and m.          */
+bsgd_status bsgd_sample_stratified(uint64_t seed, int32_t epoch, int32_t n, int32_t m, int32_t strata,
+                                   int32_t* out);
 /* Row-block partition: views_out [n_views] (blocks back to back, each sorted),
  * offsets_out [M+1].                                                          */
 bsgd_status bsgd_view_partition(int32_t n_views, int32_t M, int32_t kind, uint64_t seed,
@@ -161,7 +168,10 @@ enum {
     BSGD_AUTO_MU = 8,       /* Algo 3                             */
     BSGD_SGD = 16,          /* Eq. 4 mini-batch SGD baseline       */
     BSGD_RESUME = 32,       /* bsgd_run: continue from the current state (no reset)   */
-    BSGD_TIMING = 64        /* bsgd_run: per-phase CUDA-event times into the log      */
+    BSGD_TIMING = 64,       /* bsgd_run: per-phase CUDA-event times into the log      */
+    BSGD_STRATIFIED = 128   /* column blocks drawn per owner stratum (bsgd_sample_stratified,
+                               run_params.strata): under Eq. 8 with gamma N = G
+                               every rank gets gamma N / G blocks, none idles (reading A31) */
 };
 
 /* One epoch of Algo 1 / Algo 2 with an explicit selection (identical on all
@@ -187,6 +197,7 @@ typedef struct {
     int32_t tv_iters, tv_period;              /* FGP iterations (20); period 0 = round(1/(alpha gamma)) */
     double eps, delta, t1, t2;                /* Algo 3 constants (reading A12: .05, .4, .5, 0)   */
     int32_t is_off_last_epochs;               /* final epochs without IS           */
+    int32_t strata;                           /* BSGD_STRATIFIED: number of strata (0 = world)   */
 } bsgd_run_params;
 
 /* Per-epoch log; every pointer is host memory and nullable.                  */

@@ -55,6 +55,23 @@ def select(seed: int, stream: int, epoch: int, n: int, m: int) -> list[int]:
     return sorted(a[:m])
 
 
+def select_stratified(seed: int, epoch: int, n: int, m: int, strata: int) -> list[int]:
+    """Column blocks drawn per owner stratum (reading A31): blocks
+    [s n/S, (s+1) n/S) form stratum s; m/S of them are drawn by partial Fisher-Yates
+    with draws rnd(seed, 2, epoch, s n/S + i); strata concatenated in order (sorted)."""
+    if strata < 1 or n % strata or m % strata:
+        raise ValueError("strata must divide n and m")
+    ns, ms = n // strata, m // strata
+    out = []
+    for s in range(strata):
+        a = list(range(ns))
+        for i in range(ms):
+            j = i + bounded(rnd(seed, 2, epoch, s * ns + i), ns - i)
+            a[i], a[j] = a[j], a[i]
+        out += [s * ns + v for v in sorted(a[:ms])]
+    return out
+
+
 def permutation(seed: int, stream: int, epoch: int, n: int) -> list[int]:
     """Full Fisher-Yates permutation (unsorted) with the same draws as select()."""
     a = list(range(n))
@@ -254,6 +271,7 @@ class Params:
     tv_iters: int = 20
     tv_period: int = 0               # 0 = round(1/(alpha gamma))
     sgd: bool = False                # Eq. 4 mini-batch SGD baseline
+    strata: int = 0                  # > 0: stratified column selection
 
 
 class OracleBSGD:
@@ -302,7 +320,12 @@ class OracleBSGD:
     def selection(self, e):
         p = self.p
         rows = select(p.seed, 1, e, self.M, p.rows_per_epoch)
-        cols = list(range(self.N)) if p.sgd else select(p.seed, 2, e, self.N, p.cols_per_epoch)
+        if p.sgd:
+            cols = list(range(self.N))
+        elif p.strata > 0:
+            cols = select_stratified(p.seed, e, self.N, p.cols_per_epoch, p.strata)
+        else:
+            cols = select(p.seed, 2, e, self.N, p.cols_per_epoch)
         return rows, cols
 
     def tiles_for(self, e, rows, cols, use_im):

@@ -28,7 +28,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 PARALLEL, FAN, CONE = 0, 1, 2
-IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING = 1, 2, 4, 8, 16, 32, 64
+IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED = 1, 2, 4, 8, 16, 32, 64, 128
 STATUS = {0: "OK", 1: "E_GEOMETRY", 2: "E_PARTITION", 3: "E_DIMENSION", 4: "E_CONTRACT", 5: "E_CUDA",
           6: "E_NCCL", 7: "E_OOM", 8: "E_POISONED"}
 
@@ -87,7 +87,7 @@ class RunParams(C.Structure):
                 ("cols_per_epoch", C.c_int32), ("mu0", C.c_double), ("flags", C.c_uint32),
                 ("lambda_", C.c_double), ("tv_iters", C.c_int32), ("tv_period", C.c_int32),
                 ("eps", C.c_double), ("delta", C.c_double), ("t1", C.c_double), ("t2", C.c_double),
-                ("is_off_last_epochs", C.c_int32)]
+                ("is_off_last_epochs", C.c_int32), ("strata", C.c_int32)]
 
 
 class RunLog(C.Structure):
@@ -112,6 +112,7 @@ SIGS = {
     "bsgd_geometry_circular": ([C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_int32,
                                 C.c_double, C.c_double, P(C.c_double)], C.c_int),
     "bsgd_sample": ([C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32)], C.c_int),
+    "bsgd_sample_stratified": ([C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_int32)], C.c_int),
     "bsgd_view_partition": ([C.c_int32, C.c_int32, C.c_int32, C.c_uint64, P(C.c_int32), P(C.c_int32)], C.c_int),
     "bsgd_eq8": ([C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
     "bsgd_owned_blocks": ([C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
@@ -193,6 +194,12 @@ def geometry_circular(beam, n_views, arc_deg, OP, OD, det_u, det_v, pitch_u, pit
 def sample(seed, stream, epoch, n, m) -> list[int]:
     out = np.zeros(max(m, 1), dtype=np.int32)
     _check(_lib.bsgd_sample(seed, stream, epoch, n, m, out.ctypes.data_as(P(C.c_int32))))
+    return out[:m].tolist()
+
+
+def sample_stratified(seed, epoch, n, m, strata) -> list[int]:
+    out = np.zeros(max(m, 1), dtype=np.int32)
+    _check(_lib.bsgd_sample_stratified(seed, epoch, n, m, strata, out.ctypes.data_as(P(C.c_int32))))
     return out[:m].tolist()
 
 
@@ -369,9 +376,9 @@ class Context:
 
     def run(self, y, x, epochs, mu0, seed=1, x_true=None, rows_per_epoch=0, cols_per_epoch=0, flags=0,
             lam=0.1, tv_iters=20, tv_period=0, eps=0.05, delta=0.4, t1=0.5, t2=0.0, is_off_last=0,
-            stream=None) -> RunResult:
+            strata=0, stream=None) -> RunResult:
         prm = RunParams(seed, epochs, rows_per_epoch, cols_per_epoch, mu0, flags, lam, tv_iters, tv_period,
-                        eps, delta, t1, t2, is_off_last)
+                        eps, delta, t1, t2, is_off_last, strata)
         aM = rows_per_epoch or eq8(self.info.N // self.owned_count, self.M, self.N)[0]
         gN = cols_per_epoch or eq8(self.info.N // self.owned_count, self.M, self.N)[1]
         E = max(epochs, 1)

@@ -982,6 +982,16 @@ bsgd_status bsgd_sample(uint64_t seed, int32_t stream, int32_t epoch, int32_t n,
     });
 }
 
+bsgd_status bsgd_sample_stratified(uint64_t seed, int32_t epoch, int32_t n, int32_t m, int32_t strata,
+                                   int32_t* out) {
+    return guard(nullptr, [&] {
+        if (n < 1 || m < 0 || m > n || !out || epoch < 0 || epoch >= (1 << 24) || strata < 1 || n % strata ||
+            m % strata)
+            fail(BSGD_E_CONTRACT, "bad stratified sample arguments");
+        host::select_stratified(seed, epoch, n, m, strata, out);
+    });
+}
+
 bsgd_status bsgd_view_partition(int32_t n_views, int32_t M, int32_t kind, uint64_t seed, int32_t* views_out,
                                 int32_t* offsets_out) {
     return guard(nullptr, [&] {
@@ -1304,7 +1314,8 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (!c || !y_in || !x_in || !P) fail(BSGD_E_CONTRACT, "NULL");
         if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
         if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
-        const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING;
+        const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING |
+                               BSGD_STRATIFIED;
         if (P->flags & ~known) fail(BSGD_E_CONTRACT, "unknown flags");
         const bool sgd = P->flags & BSGD_SGD, im = (P->flags & (BSGD_IS | BSGD_IS_UNIFORM)) && !sgd;
         const bool uni = P->flags & BSGD_IS_UNIFORM, tv = P->flags & BSGD_TV, amu = P->flags & BSGD_AUTO_MU;
@@ -1316,6 +1327,10 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             if (!gN) gN = g2;
         }
         if (aM < 1 || aM > c->M || gN < 1 || gN > c->N) fail(BSGD_E_CONTRACT, "rows/cols per epoch out of range");
+        const bool strat = (P->flags & BSGD_STRATIFIED) && !sgd;
+        const int strata = P->strata > 0 ? P->strata : c->world;
+        if (strat && (P->strata < 0 || c->N % strata || gN % strata))
+            fail(BSGD_E_CONTRACT, "BSGD_STRATIFIED: strata must divide N and cols_per_epoch");
         if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
             fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
         if (tv && (P->tv_iters < 0 || !isfinite(P->lambda))) fail(BSGD_E_CONTRACT, "bad TV parameters");
@@ -1420,7 +1435,8 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             const int eg = c->epoch;          // global 0-based epoch (RNG counter)
             const int k = eg + 1;             // 1-based epoch of Algos 3 and 4
             host::select(P->seed, 1, eg, c->M, aM, rows.data());
-            if (!sgd) host::select(P->seed, 2, eg, c->N, gN, cols.data());
+            if (strat) host::select_stratified(P->seed, eg, c->N, gN, strata, cols.data());
+            else if (!sgd) host::select(P->seed, 2, eg, c->N, gN, cols.data());
             if (log && log->sel_rows) memcpy(log->sel_rows + (size_t)e * aM, rows.data(), sizeof(int) * aM);
             if (log && log->sel_cols && !sgd) memcpy(log->sel_cols + (size_t)e * gN, cols.data(), sizeof(int) * gN);
             std::vector<int> tiles;

@@ -85,6 +85,20 @@ void select(uint64_t seed, int stream, int epoch, int n, int m, int32_t* out) {
     memcpy(out, a.data(), sizeof(int32_t) * m);
 }
 
+void select_stratified(uint64_t seed, int epoch, int n, int m, int strata, int32_t* out) {
+    const int ns = n / strata, ms = m / strata;
+    std::vector<int32_t> a(ns);
+    for (int s = 0; s < strata; ++s) {
+        std::iota(a.begin(), a.end(), 0);
+        for (int i = 0; i < ms; ++i) {
+            int j = i + (int)bounded(rnd(seed, 2, epoch, s * ns + i), (uint32_t)(ns - i));
+            std::swap(a[i], a[j]);
+        }
+        std::sort(a.begin(), a.begin() + ms);
+        for (int i = 0; i < ms; ++i) out[s * ms + i] = s * ns + a[i];
+    }
+}
+
 void view_partition(int n_views, int M, int kind, uint64_t seed, int32_t* views, int32_t* offsets) {
     std::vector<int32_t> order(n_views);
     std::iota(order.begin(), order.end(), 0);

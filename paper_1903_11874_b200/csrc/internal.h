@@ -30,6 +30,7 @@ uint64_t mix64(uint64_t z);
 uint64_t rnd(uint64_t seed, uint32_t stream, uint32_t epoch, uint32_t k);
 uint32_t bounded(uint64_t u, uint32_t n);
 void select(uint64_t seed, int stream, int epoch, int n, int m, int32_t* out);
+void select_stratified(uint64_t seed, int epoch, int n, int m, int strata, int32_t* out);
 void view_partition(int n_views, int M, int kind, uint64_t seed, int32_t* views, int32_t* offsets);
 void eq8(int nodes, int M, int N, int* aM, int* gN);
 int im_draw(uint64_t seed, int epoch, uint32_t k, const uint32_t* q, int T, bool uniform);

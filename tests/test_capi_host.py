@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(bs):
     want = set(declared_symbols())
     assert want, "header parse failed"
     assert want <= exported, want - exported
-    assert bs.abi_version() == 1
+    assert bs.abi_version() == 2
 
 
 def test_geometry_bit_exact(bs):
@@ -58,6 +58,16 @@ def test_sampler_bit_exact(bs):
     # survey KATs: seed 1, epoch 0: rows (10 choose 1) -> [7]; cols (8 choose 2) epochs 0..4
     assert bs.sample(1, 1, 0, 10, 1) == [7]
     assert [bs.sample(1, 2, e, 8, 2) for e in range(5)] == [[2, 3], [3, 5], [4, 7], [2, 7], [5, 7]]
+
+
+def test_stratified_sampler_bit_exact(bs):
+    for seed in [0, 3, 2 ** 62 + 1]:
+        for e in range(0, 200, 3):
+            for n, m, S in [(8, 2, 2), (8, 8, 4), (8, 4, 4), (16, 4, 2), (6, 3, 3), (8, 2, 1)]:
+                assert bs.sample_stratified(seed, e, n, m, S) == ob.select_stratified(seed, e, n, m, S)
+    for bad in [(8, 3, 2), (8, 2, 3), (8, 2, 0)]:
+        with pytest.raises(bs.BsgdError):
+            bs.sample_stratified(1, 0, *bad)
 
 
 def test_partition_and_eq8_bit_exact(bs):

@@ -309,6 +309,23 @@ def test_trajectory_tv_auto_mu(bs):
     print("cfg4-scaled TV+auto-mu", _compare(o, res, x), "mu:", res.mu[::10])
 
 
+def test_trajectory_stratified(bs):
+    """BSGD with stratified column selection: 4 strata of 2 blocks on a
+    scaled cfg3 (N = 8), gamma N = 4; the selection is bit-exact, the trajectory within 1e-3."""
+    p, g, vol32, y = problem("cfg3", K=48, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 0.5 / ob.power_iteration(P, 30, seed=1)
+    o, res, x = _run_pair(bs, p, g, vol32, y, 12, mu, flags=bs.STRATIFIED,
+                          oracle_kw=dict(strata=4), run_kw=dict(cols_per_epoch=4, strata=4))
+    assert all(sum(1 for j in c if 2 * s <= j < 2 * s + 2) == 1 for c in res.sel_cols.tolist() for s in range(4))
+    print("stratified", _compare(o, res, x))
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M)
+    with pytest.raises(bs.BsgdError):          # 3 strata do not divide N = 8
+        ctx.run(torch.from_numpy(y).cuda(), torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda"),
+                epochs=1, mu0=1e-6, cols_per_epoch=3, flags=bs.STRATIFIED, strata=3)
+    ctx.close()
+
+
 def test_power_iteration(bs):
     p, g, vol32, y = problem("cfg1")
     P = Projector(g, BlockGrid(g.dims, p.blocks))

@@ -77,6 +77,14 @@ def _worker(rank, world, port, q):
         z0, z1 = rank * 4, rank * 4 + 4
         out["tv_err"] = float(np.max(np.abs(_tv_sharded(vol[z0:z1], 0.3, 20, rank, world, vol.shape)
                                             - ob.tv_prox(vol, 0.3, 20)[z0:z1])))
+        out["tv_fused_err"] = float(np.max(np.abs(_tv_sharded_fused(vol[z0:z1], 0.3, 20, rank, world, vol.shape)
+                                                  - ob.tv_prox(vol, 0.3, 20)[z0:z1])))
+        # ---- stratified selection (strata = world): each rank owns gamma N / G of the draw
+        st = [bs.sample_stratified(9, e, N, 2, world) for e in range(20)]
+        out["strat_own"] = all(sum(1 for j in c if j in owned) == 2 // world for c in st)
+        allst = [None] * world
+        dist.all_gather_object(allst, st)
+        out["strat_same"] = allst[0] == allst[1]
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -152,6 +160,72 @@ def _tv_sharded(b, w, iters, rank, world, gshape):
     return b - w * gradT(p, hq)
 
 
+def _tv_sharded_fused(b, w, iters, rank, world, gshape):
+    """FGP on a z-slab with the fused kernel's halo schedule (engine tv_prox, z-slab path):
+    b of plane z0-1 once; per iteration q (3 components) of plane z0-1 from rank-1 and q_z
+    of plane z1 from rank+1; u is evaluated on planes z0-1 .. z1-1 locally (never exchanged)."""
+    import math
+    nzl, ny, nx = b.shape
+    z0 = rank * nzl
+    L = 4.0 * sum(1 for n in gshape if n > 1)
+    p = np.zeros((3,) + b.shape)
+    q = np.zeros_like(p)
+    s = 1.0
+
+    def xchg(plane, down):
+        recv = torch.zeros(plane.shape, dtype=torch.float64)
+        send = torch.from_numpy(np.ascontiguousarray(plane))
+        src, dst = (rank + 1, rank - 1) if down else (rank - 1, rank + 1)
+        reqs = []
+        if 0 <= dst < world:
+            reqs.append(dist.isend(send, dst))
+        if 0 <= src < world:
+            reqs.append(dist.irecv(recv, src))
+        for r in reqs:
+            r.wait()
+        return recv.numpy()
+
+    def u_planes(f, bb, zs, fz_next):
+        """b - w grad^T f on planes zs .. zs+len-1 (f: (3, n, ny, nx)); fz_next = f_z of the
+        plane after the last one."""
+        n = f.shape[1]
+        out = np.zeros((n, ny, nx))
+        for comp, ax in ((0, 2), (1, 1)):
+            sh = [slice(None)] * 3; sl = [slice(None)] * 3
+            sh[ax] = slice(1, None); sl[ax] = slice(None, -1)
+            out[tuple(sh)] += f[comp][tuple(sh)]
+            out[tuple(sl)] -= f[comp][tuple(sh)]
+        for k in range(n):
+            gz = zs + k
+            if gz >= 1:
+                out[k] += f[2][k]
+            if gz + 1 <= gshape[0] - 1:
+                out[k] -= f[2][k + 1] if k + 1 < n else fz_next
+        return bb - w * out
+
+    hb = xchg(b[-1], False)                       # b of plane z0 - 1
+    for _ in range(iters):
+        hq = np.stack([xchg(q[c][-1], False) for c in range(3)])   # q of plane z0 - 1
+        hz = xchg(q[2][0], True)                  # q_z of plane z1
+        fe = np.concatenate([hq[:, None], q], axis=1)
+        ue = u_planes(fe, np.concatenate([hb[None], b]), z0 - 1, hz)
+        u, um = ue[1:], ue[:-1]                   # u on own planes; u one plane below
+        gr = np.zeros((3,) + b.shape)
+        gr[0][:, :, 1:] = u[:, :, 1:] - u[:, :, :-1]
+        gr[1][:, 1:, :] = u[:, 1:, :] - u[:, :-1, :]
+        for k in range(nzl):
+            if z0 + k >= 1:
+                gr[2][k] = u[k] - um[k]
+        pn = q + gr / (L * w)
+        pn /= np.maximum(1.0, np.sqrt(np.sum(pn * pn, axis=0)))
+        s1 = (1 + math.sqrt(1 + 4 * s * s)) / 2
+        q = pn + ((s - 1) / s1) * (pn - p)
+        p = pn
+        s = s1
+    hz = xchg(p[2][0], True)
+    return u_planes(p, b, z0, hz)
+
+
 def test_two_ranks_gloo():
     world = 2
     ctx = mp.get_context("spawn")
@@ -168,3 +242,5 @@ def test_two_ranks_gloo():
         assert o["id_same"] and o["sel_same"] and o["partition_ok"]
         assert o["residual_err"] < 1e-12
         assert o["tv_err"] < 1e-12
+        assert o["tv_fused_err"] < 1e-12
+        assert o["strat_own"] and o["strat_same"]

@@ -286,3 +286,25 @@ def test_auto_mu_recovers_from_large_step():
     assert fixed.log[-1]["obj"] > f0
     assert auto.log[-1]["obj"] < 0.05 * f0
     assert auto.log[-1]["mu"] < base["mu"]
+
+
+def test_select_stratified():
+    """Stratified column selection (reading A31): one stratum is the plain
+    m-of-n draw on stream 2; every stratum gets m/S distinct blocks of its own range; the
+    draw inside a stratum is uniform and independent of the other strata."""
+    for e in range(50):
+        assert ob.select_stratified(9, e, 8, 2, 1) == ob.select(9, 2, e, 8, 2)
+    n, m, S = 8, 4, 2
+    counts = {}
+    for e in range(6000):
+        s = ob.select_stratified(4242, e, n, m, S)
+        assert s == sorted(s) and len(set(s)) == m
+        assert sum(v < 4 for v in s) == 2 and sum(v >= 4 for v in s) == 2
+        counts[tuple(s)] = counts.get(tuple(s), 0) + 1
+    assert len(counts) == math.comb(4, 2) ** 2          # every (pair, pair) combination occurs
+    exp = 6000 / len(counts)
+    chi2 = sum((c - exp) ** 2 / exp for c in counts.values())
+    assert chi2 < 75.0                                   # 35 dof, p ~ 1e-4
+    assert ob.select_stratified(1, 0, 8, 8, 8) == list(range(8))   # gamma N = N: every block
+    with pytest.raises(ValueError):
+        ob.select_stratified(1, 0, 8, 3, 2)
