@@ -155,6 +155,9 @@ bsgd_status bsgd_back(bsgd_ctx ctx, int32_t n_views, const int32_t* views, const
  * and the integer importance table q = floor(2^16 w / sum_t w) used by the
  * sampler.  host out: [owned_count][n_views][tiles].                        */
 bsgd_status bsgd_im_weights(bsgd_ctx ctx, double* w_out, uint32_t* q_out);
+/* As bsgd_im_weights for a chosen weight kind: 0 = L1 mass (chord sums, the default of
+ * BSGD_IS), 1 = projection area (count of tile rays with chord > 1e-6, BSGD_IS_AREA).     */
+bsgd_status bsgd_im_table(bsgd_ctx ctx, int32_t kind, double* w_out, uint32_t* q_out);
 
 /* ---- algorithm state ------------------------------------------------------ */
 /* Algo 1 line 1: z^j = 0, g_hat^i = 0, g = 0, r = y, epoch = 0.
@@ -169,9 +172,12 @@ enum {
     BSGD_SGD = 16,          /* Eq. 4 mini-batch SGD baseline       */
     BSGD_RESUME = 32,       /* bsgd_run: continue from the current state (no reset)   */
     BSGD_TIMING = 64,       /* bsgd_run: per-phase CUDA-event times into the log      */
-    BSGD_STRATIFIED = 128   /* column blocks drawn per owner stratum (bsgd_sample_stratified,
+    BSGD_STRATIFIED = 128,  /* column blocks drawn per owner stratum (bsgd_sample_stratified,
                                run_params.strata): under Eq. 8 with gamma N = G
                                every rank gets gamma N / G blocks, none idles (reading A31) */
+    BSGD_IS_AREA = 256      /* with BSGD_IS: weights = number of tile rays that cross the block
+                               (chord > 1e-6), the "projection area" reading of PAPER.md:162,
+                               instead of the default L1 mass (reading A9)                  */
 };
 
 /* One epoch of Algo 1 / Algo 2 with an explicit selection (identical on all

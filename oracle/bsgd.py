@@ -131,17 +131,19 @@ def tile_rects(nu: int, nv: int, tiles: tuple) -> list[tuple[int, int, int, int]
 IM_SCALE = 1 << 16
 
 
-def im_table(proj: Projector, tiles: tuple) -> np.ndarray:
+def im_table(proj: Projector, tiles: tuple, area: bool = False) -> np.ndarray:
     """Integer importance table q[j][view][t] ("the denser a
     sub-matrix is, the higher the probability ... computes the fraction of a
     volume block's projection area on each sub-detector"; reading A9: weight =
-    L1 mass of A_{tile}^{J} = ones-pass chord sums).  q = floor(2^16 w/sum w)."""
+    L1 mass of A_{tile}^{J} = ones-pass chord sums; area=True: the number of tile
+    rays crossing the block, chord > 1e-6 — the "projection area" reading, IS_AREA).
+    q = floor(2^16 w/sum w)."""
     N, V = proj.grid.N, proj.g.n_views
     T = tiles[0] * tiles[1]
     q = np.zeros((N, V, T), dtype=np.uint32)
     views = np.arange(V)
     for j in range(N):
-        w = proj.tile_mass(views, j, tiles)
+        w = proj.tile_mass(views, j, tiles, area)
         s = w.sum(axis=1, keepdims=True)
         with np.errstate(invalid="ignore", divide="ignore"):
             f = np.where(s > 0, np.floor(IM_SCALE * w / np.where(s > 0, s, 1.0)), 0.0)
@@ -259,6 +261,7 @@ class Params:
     cols_per_epoch: int = 1          # gamma N
     im: bool = False                 # BSGD-IM (Algo 2)
     im_uniform: bool = False         # BSGD-RAN
+    im_area: bool = False            # IS_AREA weights (reading A9 alternative)
     is_off_last: int = 0             # epochs at the end run without IS
     total_epochs: int = 0            # needed for is_off_last
     auto_mu: bool = False            # Algo 3
@@ -291,7 +294,7 @@ class OracleBSGD:
         self.rows = view_partition(geom.n_views, M, row_kind, rs)
         self.tiles = tuple(tiles)
         self.rects = tile_rects(geom.det_u, geom.det_v, self.tiles)
-        self.q = im_table(self.P, self.tiles) if params.im and not params.im_uniform else None
+        self.q = im_table(self.P, self.tiles, params.im_area) if params.im and not params.im_uniform else None
         self.y = np.asarray(y, dtype=np.float64).ravel()
         nb = self.grid.bsize
         self.x = np.zeros((self.N, nb)) if x0 is None else np.array(x0, dtype=np.float64).reshape(self.N, nb)

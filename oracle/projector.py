@@ -29,7 +29,7 @@ def lib():
         common = [i, P(d), i, i, P(i), P(i), P(i)]
         _lib.oracle_fp.argtypes = common + [P(i), i, P(i), P(d), P(d), i]
         _lib.oracle_bp.argtypes = common + [P(i), i, P(i), P(d), P(d)]
-        _lib.oracle_tile_mass.argtypes = common + [P(i), i, i, i, P(d)]
+        _lib.oracle_tile_mass.argtypes = common + [P(i), i, i, i, i, P(d)]
         _lib.oracle_csr_count.argtypes = common + [P(i), i, P(i64)]
         _lib.oracle_csr_fill.argtypes = common + [P(i), i, P(i64), P(i64), P(d)]
         _lib.oracle_count.argtypes = common + [P(i), i, P(i)]
@@ -134,12 +134,12 @@ class Projector:
                         _p(gblk, C.c_double))
         return gblk
 
-    def tile_mass(self, views, j, tiles):
+    def tile_mass(self, views, j, tiles, area=False):
         views = np.ascontiguousarray(np.asarray(views, dtype=np.int32))
         T = tiles[0] * tiles[1]
         w = np.zeros(len(views) * T, dtype=np.float64)
         common, _ = self._common(j)
-        lib().oracle_tile_mass(*common, _p(views, C.c_int), len(views), tiles[0], tiles[1],
+        lib().oracle_tile_mass(*common, _p(views, C.c_int), len(views), tiles[0], tiles[1], int(area),
                                _p(w, C.c_double))
         return w.reshape(len(views), T)
 

@@ -200,10 +200,12 @@ void oracle_bp(int beam, const double *vecs, int nu, int nv, const int *dims,
 
 /* Ones-pass per detector tile: w[s*T + t] = sum over rays of tile t of
  * sum of segment lengths through the box (= (A_tile^J 1) summed), the block
- * weight of BSGD-IM (§II-A; SURVEY §8c A9 reading).       */
+ * weight of BSGD-IM (§II-A; SURVEY §8c A9 reading).  With
+ * area != 0: the number of tile rays whose chord through the box exceeds 1e-6
+ * (the "fraction of a volume block's projection area", IS_AREA).           */
 void oracle_tile_mass(int beam, const double *vecs, int nu, int nv, const int *dims,
                       const int *lo, const int *hi, const int *views, int n_sel,
-                      int tiles_u, int tiles_v, double *w)
+                      int tiles_u, int tiles_v, int area, double *w)
 {
     int T = tiles_u * tiles_v;
     for (int s = 0; s < n_sel; ++s) {
@@ -221,7 +223,11 @@ void oracle_tile_mass(int beam, const double *vecs, int nu, int nv, const int *d
                 double len[SEGCAP];
                 oracle_ray(beam, vecs + 12 * (long)view, nu, nv, iu, iv, dims, a, b);
                 int n = oracle_trace(a, b, lo, hi, idx, len, SEGCAP);
-                for (int k = 0; k < n; ++k) sum += len[k];
+                double chord = 0.0;
+                for (int k = 0; k < n; ++k) chord += len[k];
+                /* area mode: the ray belongs to the block's shadow (reading A9, threshold
+                 * 1e-6 voxel so that corner touches do not count)                        */
+                sum += area ? (chord > 1e-6 ? 1.0 : 0.0) : chord;
             }
             w[(long)s * T + t] = sum;
         }

@@ -28,7 +28,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 PARALLEL, FAN, CONE = 0, 1, 2
-IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED = 1, 2, 4, 8, 16, 32, 64, 128
+IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED, IS_AREA = 1, 2, 4, 8, 16, 32, 64, 128, 256
 STATUS = {0: "OK", 1: "E_GEOMETRY", 2: "E_PARTITION", 3: "E_DIMENSION", 4: "E_CONTRACT", 5: "E_CUDA",
           6: "E_NCCL", 7: "E_OOM", 8: "E_POISONED"}
 
@@ -126,6 +126,7 @@ SIGS = {
     "bsgd_back": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p, C.c_float,
                    C.c_int32, C.c_void_p], C.c_int),
     "bsgd_im_weights": ([_ctx, P(C.c_double), P(C.c_uint32)], C.c_int),
+    "bsgd_im_table": ([_ctx, C.c_int32, P(C.c_double), P(C.c_uint32)], C.c_int),
     "bsgd_reset": ([_ctx, C.c_void_p, C.c_void_p], C.c_int),
     "bsgd_step": ([_ctx, C.c_void_p, C.c_void_p, P(Selection), C.c_float, C.c_uint32, C.c_void_p], C.c_int),
     "bsgd_run": ([_ctx, C.c_void_p, C.c_void_p, C.c_void_p, P(RunParams), P(RunLog), C.c_void_p], C.c_int),
@@ -354,12 +355,14 @@ class Context:
         self._c(_lib.bsgd_back(self.h, len(v), vp, rp, col_block, _ptr(proj), _ptr(g_block), float(scale),
                                int(accumulate), _stream(stream)))
 
-    def im_weights(self):
+    def im_weights(self, area=False):
+        """(w, q) of the IM table: L1 mass (default) or, area=True, the BSGD_IS_AREA counts."""
         T = self.info.tiles
         n = self.owned_count * self.info.n_views * T
         w = np.zeros(n, dtype=np.float64)
         q = np.zeros(n, dtype=np.uint32)
-        self._c(_lib.bsgd_im_weights(self.h, w.ctypes.data_as(P(C.c_double)), q.ctypes.data_as(P(C.c_uint32))))
+        self._c(_lib.bsgd_im_table(self.h, int(bool(area)), w.ctypes.data_as(P(C.c_double)),
+                                   q.ctypes.data_as(P(C.c_uint32))))
         shape = (self.owned_count, self.info.n_views, T)
         return w.reshape(shape), q.reshape(shape)
 

@@ -113,6 +113,7 @@ struct bsgd_ctx_s {
     std::vector<uint32_t> q;            // IM table [s][n_views][T]
     std::vector<double> w;
     bool q_ready = false;
+    int q_kind = 0;
     // Algo 3 state
     bool have_prev_eud = false, have_theta_prev = false;
     double theta_prev = 0.0;
@@ -606,8 +607,10 @@ struct bsgd_ctx_s {
         vtab_ready = true;
     }
 
-    void ensure_im_table(cudaStream_t st) {
-        if (q_ready) return;
+    // IM table of the given kind (0: L1 mass = ones-pass chord sums; 1: IS_AREA = count of
+    // tile rays crossing the block), recomputed when the kind changes
+    void ensure_im_table(cudaStream_t st, int kind = 0) {
+        if (q_ready && q_kind == kind) return;
         double* dw = dnew<double>((long long)s * n_views * T);
         std::vector<BlockDesc> bl(s);
         for (int b = 0; b < s; ++b) box(first + b, bl[b].lo, bl[b].hi);
@@ -620,6 +623,8 @@ struct bsgd_ctx_s {
         I.tiles_u = tiles_u;
         I.tiles_v = tiles_v;
         I.w = dw;
+        I.area = kind;
+        BSGD_CUDA(cudaMemsetAsync(dw, 0, sizeof(double) * (size_t)s * n_views * T, st));
         tab_upload(staging, off, st);
         launch_im_weights(I, st);
         w.assign((size_t)s * n_views * T, 0.0);
@@ -632,6 +637,7 @@ struct bsgd_ctx_s {
             for (int t = 0; t < T; ++t) q[e + t] = S > 0 ? (uint32_t)floor(65536.0 * w[e + t] / S) : 0u;
         }
         q_ready = true;
+        q_kind = kind;
     }
 
     // FGP TV prox (Algo 4 line 16) on the owned volume: x <- argmin 1/2|t-x|^2 + w TV(t)
@@ -1246,9 +1252,13 @@ bsgd_status bsgd_back(bsgd_ctx c, int32_t n, const int32_t* views, const int32_t
 }
 
 bsgd_status bsgd_im_weights(bsgd_ctx c, double* w_out, uint32_t* q_out) {
+    return bsgd_im_table(c, 0, w_out, q_out);
+}
+
+bsgd_status bsgd_im_table(bsgd_ctx c, int32_t kind, double* w_out, uint32_t* q_out) {
     return guard(c, [&] {
-        if (!c) fail(BSGD_E_CONTRACT, "NULL");
-        c->ensure_im_table(nullptr);
+        if (!c || kind < 0 || kind > 1) fail(BSGD_E_CONTRACT, "bad arguments");
+        c->ensure_im_table(nullptr, kind);
         if (w_out) memcpy(w_out, c->w.data(), sizeof(double) * c->w.size());
         if (q_out) memcpy(q_out, c->q.data(), sizeof(uint32_t) * c->q.size());
     });
@@ -1315,7 +1325,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
         if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
         const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING |
-                               BSGD_STRATIFIED;
+                               BSGD_STRATIFIED | BSGD_IS_AREA;
         if (P->flags & ~known) fail(BSGD_E_CONTRACT, "unknown flags");
         const bool sgd = P->flags & BSGD_SGD, im = (P->flags & (BSGD_IS | BSGD_IS_UNIFORM)) && !sgd;
         const bool uni = P->flags & BSGD_IS_UNIFORM, tv = P->flags & BSGD_TV, amu = P->flags & BSGD_AUTO_MU;
@@ -1403,7 +1413,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             if (y_host && up.yev) BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
             push_r0(c->d_normsq);
         }
-        if (im && !uni) c->ensure_im_table(st);
+        if (im && !uni) c->ensure_im_table(st, (P->flags & BSGD_IS_AREA) ? 1 : 0);
         std::vector<int> all_slots(c->s);
         for (int b = 0; b < c->s; ++b) all_slots[b] = b;
         if (x_host && P->epochs == 0) {   // no epoch to hide the upload behind

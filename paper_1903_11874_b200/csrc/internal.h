@@ -152,7 +152,8 @@ struct ImLaunch {
     int n_blocks;
     const BlockDesc* blocks;   // boxes only
     int tiles_u, tiles_v;
-    double* w;                 // [n_blocks][n_views][T]
+    double* w;
+    int area;                  // 1: count rays with chord > 1e-6 (IS_AREA) instead of chord sums                 // [n_blocks][n_views][T]
 };
 void launch_im_weights(const ImLaunch& I, cudaStream_t st);
 

@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(256) k_im_weights(const ImLaunch I) {
         const BlockDesc& B = I.blocks[bb];
         double amin, amax, c = 0.0;
         if (in && clip(a, b, inv, B.lo, B.hi, amin, amax)) c = (amax - amin) * blen;
+        if (I.area) c = c > 1e-6 ? 1.0 : 0.0;   // IS_AREA: rays of the block's shadow (reading A9)
         double* dst = I.w + ((size_t)bb * I.g.n_views + view) * T;
         if (uniform_tile) {
 #pragma unroll

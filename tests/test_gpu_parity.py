@@ -221,6 +221,13 @@ def test_im_table(bs):
         margin = np.abs(frac - np.round(frac))
         ambiguous = margin < 1e-7
         assert np.array_equal(q[~ambiguous], qo[~ambiguous]), "IM table differs away from rounding boundaries"
+        # IS_AREA: ray counts (integers) and their table
+        wa, qa = ctx.im_weights(area=True)
+        qoa = ob.im_table(P, p.tiles, area=True)
+        for j in range(p.N):
+            assert np.array_equal(wa[j], P.tile_mass(np.arange(g.n_views), j, p.tiles, area=True))
+        assert np.array_equal(qa, qoa)
+        assert not np.array_equal(qa, q)           # the two weightings differ
         ctx.close()
 
 
@@ -279,15 +286,15 @@ def test_trajectory_cfg1_gd_and_stochastic(bs):
     print("cfg1 stochastic", _compare(o, res, x))
 
 
-@pytest.mark.parametrize("uniform", [False, True])
-def test_trajectory_cfg2_im(bs, uniform):
+@pytest.mark.parametrize("uniform,area", [(False, False), (True, False), (False, True)])
+def test_trajectory_cfg2_im(bs, uniform, area):
     p, g, vol32, y = problem("cfg2")
     P = Projector(g, BlockGrid(g.dims, p.blocks))
     mu = 0.5 / ob.power_iteration(P, 30, seed=1)
-    flags = bs.IS | (bs.IS_UNIFORM if uniform else 0)
+    flags = bs.IS | (bs.IS_UNIFORM if uniform else 0) | (bs.IS_AREA if area else 0)
     o, res, x = _run_pair(bs, p, g, vol32, y, 20, mu, flags=flags,
-                          oracle_kw=dict(im=True, im_uniform=uniform))
-    print("cfg2 IM" if not uniform else "cfg2 RAN", _compare(o, res, x))
+                          oracle_kw=dict(im=True, im_uniform=uniform, im_area=area))
+    print("cfg2 RAN" if uniform else ("cfg2 IM-area" if area else "cfg2 IM"), _compare(o, res, x))
 
 
 def test_trajectory_cfg3_bsgd_and_sgd(bs):

@@ -190,6 +190,43 @@ def test_im_table_and_containment():
     assert list(q[0, 0]) == [ob.IM_SCALE, 0] and list(q[1, 0]) == [0, ob.IM_SCALE]
 
 
+def test_im_area_counts_brute_force():
+    """IS_AREA weights (reading A9 alternative) = number of tile rays whose chord through the
+    block box exceeds 1e-6, checked against an independent vectorised slab test on the ray
+    endpoints; and the containment case of test_im_table_and_containment."""
+    p = synth.PRESETS["cfg2"]
+    g = p.geometry()
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    views = np.arange(g.n_views)
+    A, B = synth.ray_endpoints(g, views)
+    A = A.reshape(g.n_views, -1, 3) + np.array(g.dims) / 2.0
+    B = B.reshape(g.n_views, -1, 3)
+    L = np.linalg.norm(B, axis=2)
+    nu = g.det_u
+    T = p.tiles[0] * p.tiles[1]
+    for j in range(P.grid.N):
+        lo, hi = P.grid.box(j)
+        t0 = np.zeros(A.shape[:2])
+        t1 = np.ones(A.shape[:2])
+        for c in range(2 if g.dims[2] == 1 else 3):
+            with np.errstate(divide="ignore", invalid="ignore"):
+                u0 = (lo[c] - A[..., c]) / B[..., c]
+                u1 = (hi[c] - A[..., c]) / B[..., c]
+            par = B[..., c] == 0
+            inside = (A[..., c] >= lo[c]) & (A[..., c] < hi[c])
+            t0 = np.where(par, np.where(inside, t0, 2.0), np.maximum(t0, np.minimum(u0, u1)))
+            t1 = np.where(par, np.where(inside, t1, -1.0), np.minimum(t1, np.maximum(u0, u1)))
+        chord = np.maximum(t1 - t0, 0.0) * L
+        want = np.zeros((g.n_views, T))
+        ch = chord.reshape(g.n_views, g.det_v, nu)
+        for t, (u0_, u1_, v0_, v1_) in enumerate(ob.tile_rects(nu, g.det_v, p.tiles)):
+            want[:, t] = (ch[:, v0_:v1_, u0_:u1_] > 1e-6).sum(axis=(1, 2))
+        got = P.tile_mass(views, j, p.tiles, area=True)
+        assert np.array_equal(got, want), j
+    q = ob.im_table(P, p.tiles, area=True)
+    assert np.all(q.sum(axis=2) <= ob.IM_SCALE) and np.all(q.sum(axis=2) >= ob.IM_SCALE - T)
+
+
 def test_im_epoch_touches_only_tile_rows():
     g, grid, A, x_true, y = sec3a_system(4, 4, noise=False)
     prm = ob.Params(seed=3, mu=1e-4, rows_per_epoch=1, cols_per_epoch=2, im=True)
