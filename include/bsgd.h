@@ -175,9 +175,10 @@ enum {
     BSGD_STRATIFIED = 128,  /* column blocks drawn per owner stratum (bsgd_sample_stratified,
                                run_params.strata): under Eq. 8 with gamma N = G
                                every rank gets gamma N / G blocks, none idles (reading A31) */
-    BSGD_IS_AREA = 256      /* with BSGD_IS: weights = number of tile rays that cross the block
+    BSGD_IS_AREA = 256,     /* with BSGD_IS: weights = number of tile rays that cross the block
                                (chord > 1e-6), the "projection area" reading of PAPER.md:162,
                                instead of the default L1 mass (reading A9)                  */
+    BSGD_TV_CHAMBOLLE = 512 /* with BSGD_TV: Chambolle-2004 dual iteration instead of FGP   */
 };
 
 /* One epoch of Algo 1 / Algo 2 with an explicit selection (identical on all
@@ -247,8 +248,11 @@ bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, dou
  * (zero difference at index 0).  x_owned: device, this rank's owned blocks, block-major (the
  * layout of bsgd_run's x_owned), modified in place; enqueued on `stream`.  Collective when
  * world > 1 (z-slab halo planes by ncclSend/Recv; every rank calls it).  w = 0 or iters = 0
- * leaves x unchanged.  Errors: BSGD_E_CONTRACT for NULL x, w < 0 or iters < 0.          */
-bsgd_status bsgd_tv_prox(bsgd_ctx ctx, float* x_owned, double w, int32_t iters, void* stream);
+ * leaves x unchanged.  method: 0 = FGP (default of bsgd_run), 1 = Chambolle 2004 (tau = 1/8
+ * in 2D, 1/12 in 3D; SURVEY §8c step 7's flag; bsgd_run with BSGD_TV_CHAMBOLLE).
+ * Errors: BSGD_E_CONTRACT for NULL x, w < 0, iters < 0 or an unknown method.             */
+bsgd_status bsgd_tv_prox(bsgd_ctx ctx, float* x_owned, double w, int32_t iters, int32_t method,
+                         void* stream);
 
 /* Comparison solvers on the same operators (the methods the paper
  * compares against in Figs. 12 and 18, cited but not listed

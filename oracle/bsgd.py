@@ -204,7 +204,7 @@ def tv_value(u: np.ndarray) -> float:
     return float(np.sum(np.sqrt(np.sum(g * g, axis=0))))
 
 
-def tv_prox(b: np.ndarray, w: float, iters: int = 20) -> np.ndarray:
+def tv_prox(b: np.ndarray, w: float, iters: int = 20, method: str = "fgp") -> np.ndarray:
     """argmin_t 1/2|t - b|^2 + w TV(t)  (Algo 4 line 16 with w = mu*lambda:
     argmin |t-x|^2 + 2 mu lambda TV(t)), by FGP (Beck & Teboulle
     2009) on the dual: p in unit balls, t = b - w grad^T p; cold start p = q = 0,
@@ -213,6 +213,8 @@ def tv_prox(b: np.ndarray, w: float, iters: int = 20) -> np.ndarray:
     if w == 0.0:
         return b.copy()
     L = 4.0 * sum(1 for n in b.shape if n > 1)
+    if method == "chambolle":
+        return _tv_prox_chambolle(b, w, iters, L)
     p = np.zeros((3,) + b.shape)
     q = np.zeros_like(p)
     s = 1.0
@@ -225,6 +227,19 @@ def tv_prox(b: np.ndarray, w: float, iters: int = 20) -> np.ndarray:
         q = pn + ((s - 1.0) / s_new) * (pn - p)
         p = pn
         s = s_new
+    return b - w * tv_grad_T(p)
+
+
+def _tv_prox_chambolle(b, w, iters, L):
+    """Chambolle (2004) semi-implicit dual iteration, the flag of SURVEY §8c step 7: with
+    tau = 1/L (1/8 in 2D, 1/12 in 3D) and p_0 = 0,
+        u = b - w grad^T p;   p <- (p + tau grad(u) / w) / (1 + tau |grad(u)| / w)
+    (Chambolle's p with the sign of div = -grad^T folded in); result b - w grad^T p."""
+    tau = 1.0 / L
+    p = np.zeros((3,) + b.shape)
+    for _ in range(iters):
+        gu = tv_grad(b - w * tv_grad_T(p)) * (tau / w)
+        p = (p + gu) / (1.0 + np.sqrt(np.sum(gu * gu, axis=0)))
     return b - w * tv_grad_T(p)
 
 
@@ -273,6 +288,7 @@ class Params:
     lam: float = 0.1
     tv_iters: int = 20
     tv_period: int = 0               # 0 = round(1/(alpha gamma))
+    tv_method: str = "fgp"           # "chambolle": the Chambolle-2004 flag
     sgd: bool = False                # Eq. 4 mini-batch SGD baseline
     strata: int = 0                  # > 0: stratified column selection
 
@@ -398,7 +414,7 @@ class OracleBSGD:
         # Algo 4 lines 15-17: TV prox every 1/(alpha gamma) epochs
         if p.tv and k % self.tv_period() == 0:
             vol = self.grid.from_blocks(self.x)
-            vol = tv_prox(vol, self.mu * p.lam, p.tv_iters)
+            vol = tv_prox(vol, self.mu * p.lam, p.tv_iters, p.tv_method)
             self.x = self.grid.to_blocks(vol)
         # Algo 3 (after the epoch): EUD, theta, criteria
         if p.auto_mu:

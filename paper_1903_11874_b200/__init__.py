@@ -28,7 +28,8 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 PARALLEL, FAN, CONE = 0, 1, 2
-IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED, IS_AREA = 1, 2, 4, 8, 16, 32, 64, 128, 256
+IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED, IS_AREA, TV_CHAMBOLLE = \
+    1, 2, 4, 8, 16, 32, 64, 128, 256, 512
 STATUS = {0: "OK", 1: "E_GEOMETRY", 2: "E_PARTITION", 3: "E_DIMENSION", 4: "E_CONTRACT", 5: "E_CUDA",
           6: "E_NCCL", 7: "E_OOM", 8: "E_POISONED"}
 
@@ -133,7 +134,7 @@ SIGS = {
     "bsgd_get_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
-    "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_void_p], C.c_int),
+    "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
                    C.c_int),
 }
@@ -422,10 +423,11 @@ class Context:
         a = np.ascontiguousarray(arr, dtype=dt)
         self._c(_lib.bsgd_set_state(self.h, what, index, a.ctypes.data, a.nbytes))
 
-    def tv_prox(self, x, w, iters=20, stream=None):
+    def tv_prox(self, x, w, iters=20, method="fgp", stream=None):
         """x (CUDA float32, the owned blocks block-major) <- prox_{w TV}(x) in place by
-        `iters` FGP iterations (bsgd_tv_prox; Algo 4 line 16)."""
-        self._c(_lib.bsgd_tv_prox(self.h, _ptr(x), float(w), int(iters), _stream(stream)))
+        `iters` FGP (or Chambolle-2004) iterations (bsgd_tv_prox; Algo 4 line 16)."""
+        m = {"fgp": 0, "chambolle": 1}[method]
+        self._c(_lib.bsgd_tv_prox(self.h, _ptr(x), float(w), int(iters), m, _stream(stream)))
         return x
 
     def power_iteration(self, iters=30, seed=0, stream=None) -> float:

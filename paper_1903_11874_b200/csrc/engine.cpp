@@ -795,7 +795,9 @@ struct bsgd_ctx_s {
         epoch = 0;
     }
 
-    void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st) {
+    // method 0: FGP (Beck-Teboulle, reading A16); 1: Chambolle 2004 (tau = 1/L), the flag of
+    // one dual field (tv_q, double-buffered on the fused path)
+    void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st, int method = 0) {
         const long long n = (long long)s * bsize;
         // z-slab layouts (the owned volume is one [z][y][x] array) take the fused iteration
         const bool fused = bgrid[0] == 1 && bgrid[1] == 1;
@@ -837,6 +839,7 @@ struct bsgd_ctx_s {
         Tl.n = n;
         Tl.z0 = first * bd[2];
         Tl.z1 = (first + s) * bd[2];
+        Tl.chambolle = method == 1;
         double sk = 1.0;
         if (fused) {
             Tl.halo_prev = tv_hp;
@@ -857,8 +860,9 @@ struct bsgd_ctx_s {
                 std::swap(qa, qb);
                 sk = sk1;
             }
-            halo_exchange(tv_p + 2 * n, tv_hq, plane, true, st);
-            Tl.q = tv_p;
+            float* pf = method == 1 ? qa : tv_p;          // the final dual field
+            halo_exchange(pf + 2 * n, tv_hq, plane, true, st);
+            Tl.q = pf;
             Tl.wf = (float)wgt;
             launch_tv_out(Tl, x_owned, st);
             return;
@@ -874,8 +878,9 @@ struct bsgd_ctx_s {
             launch_tv_pq(Tl, st);
             sk = sk1;
         }
-        halo_exchange(tv_p + 2 * n, tv_hq, plane, true, st);
-        launch_tv_u(Tl, tv_p, x_owned, st);
+        float* pf = method == 1 ? tv_q : tv_p;                // Chambolle updates q in place
+        halo_exchange(pf + 2 * n, tv_hq, plane, true, st);
+        launch_tv_u(Tl, pf, x_owned, st);
     }
 
     // z-slab halo: `down` = send my first plane (src) to rank-1 and receive rank+1's first
@@ -1325,7 +1330,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
         if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
         const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING |
-                               BSGD_STRATIFIED | BSGD_IS_AREA;
+                               BSGD_STRATIFIED | BSGD_IS_AREA | BSGD_TV_CHAMBOLLE;
         if (P->flags & ~known) fail(BSGD_E_CONTRACT, "unknown flags");
         const bool sgd = P->flags & BSGD_SGD, im = (P->flags & (BSGD_IS | BSGD_IS_UNIFORM)) && !sgd;
         const bool uni = P->flags & BSGD_IS_UNIFORM, tv = P->flags & BSGD_TV, amu = P->flags & BSGD_AUTO_MU;
@@ -1504,7 +1509,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             launch_obj(c->d_normsq, c->M, c->d_log + 2 * e, st);
             if (amu) launch_axpy_eud(c->eud_cur, c->g, sb, st);            // Algo 3 line 2
             if (tv && k % period == 0) {                                      // Algo 4 lines 15-17
-                c->tv_prox(x, c->mu * P->lambda, P->tv_iters, st);
+                c->tv_prox(x, c->mu * P->lambda, P->tv_iters, st, (P->flags & BSGD_TV_CHAMBOLLE) ? 1 : 0);
                 c->refresh_xT(x, all_slots, st);
             }
             if (evp) BSGD_CUDA(cudaEventRecord(evp[5], st));
@@ -1654,10 +1659,11 @@ bsgd_status bsgd_set_state(bsgd_ctx c, int32_t what, int32_t index, const void* 
     });
 }
 
-bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, void* stream) {
+bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, int32_t method, void* stream) {
     return guard(c, [&] {
-        if (!c || !x_owned || !(w >= 0.0) || iters < 0) fail(BSGD_E_CONTRACT, "bad arguments");
-        c->tv_prox(x_owned, w, iters, S(stream));
+        if (!c || !x_owned || !(w >= 0.0) || iters < 0 || method < 0 || method > 1)
+            fail(BSGD_E_CONTRACT, "bad arguments");
+        c->tv_prox(x_owned, w, iters, S(stream), method);
     });
 }
 

@@ -438,6 +438,18 @@ __global__ void __launch_bounds__(256) k_tv_pq(const TvLaunch T) {
             pn[a] = (double)T.q[a * T.n + o] + gr * s;
             nrm += pn[a] * pn[a];
         }
+        if (T.chambolle) {   // pn = q + s g: p <- (q + s g) / (1 + s |g|), in place on q
+            double g2 = 0.0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double ga = pn[a] - (double)T.q[a * T.n + o];
+                g2 += ga * ga;
+            }
+            const double d = 1.0 + sqrt(g2);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) T.q[a * T.n + o] = (float)(pn[a] / d);
+            continue;
+        }
         const double d = fmax(1.0, sqrt(nrm));
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -534,9 +546,11 @@ __global__ void __launch_bounds__(TV_THREADS, ZT == 1 ? 3 : (ZT == 2 ? 2 : 1)) k
             qx[k] = T.q[i];
             qy[k] = T.q[T.n + i];
             qz[k] = T.q[2 * T.n + i];
-            ox[k] = T.p[i];
-            oy[k] = T.p[T.n + i];
-            oz[k] = T.p[2 * T.n + i];
+            if (!T.chambolle) {
+                ox[k] = T.p[i];
+                oy[k] = T.p[T.n + i];
+                oz[k] = T.p[2 * T.n + i];
+            }
         }
         if (inside) su[k][ty + 1][tx + 1] = u[k + 1];
     }
@@ -548,13 +562,21 @@ __global__ void __launch_bounds__(TV_THREADS, ZT == 1 ? 3 : (ZT == 2 ? 2 : 1)) k
         const int z = zb + k;
         if (z >= T.z1) break;
         const float uo = u[k + 1];
-        const float p0x = qx[k] + (x >= 1 ? uo - su[k][ty + 1][tx] : 0.f) * s;
-        const float p0y = qy[k] + (y >= 1 ? uo - su[k][ty][tx + 1] : 0.f) * s;
-        const float p0z = qz[k] + (z >= 1 ? uo - u[k] : 0.f) * s;
+        const float gx = (x >= 1 ? uo - su[k][ty + 1][tx] : 0.f) * s;
+        const float gy = (y >= 1 ? uo - su[k][ty][tx + 1] : 0.f) * s;
+        const float gz = (z >= 1 ? uo - u[k] : 0.f) * s;
+        const long long i = i0 + k * plane;
+        if (T.chambolle) {       // p <- (p + s g) / (1 + s |g|)
+            const float d = 1.f / (1.f + sqrtf(gx * gx + gy * gy + gz * gz));
+            T.q_out[i] = (qx[k] + gx) * d;
+            T.q_out[T.n + i] = (qy[k] + gy) * d;
+            T.q_out[2 * T.n + i] = (qz[k] + gz) * d;
+            continue;
+        }
+        const float p0x = qx[k] + gx, p0y = qy[k] + gy, p0z = qz[k] + gz;
         const float n2 = p0x * p0x + p0y * p0y + p0z * p0z;
         const float inv = n2 > 1.f ? rsqrtf(n2) : 1.f;      // projection onto |p| <= 1
         const float px = p0x * inv, py = p0y * inv, pz = p0z * inv;
-        const long long i = i0 + k * plane;
         T.q_out[i] = px + beta * (px - ox[k]);
         T.q_out[T.n + i] = py + beta * (py - oy[k]);
         T.q_out[2 * T.n + i] = pz + beta * (pz - oz[k]);
@@ -639,9 +661,11 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
             q0 = ld4(T.q + i);
             q1 = ld4(T.q + T.n + i);
             q2 = ld4(T.q + 2 * T.n + i);
-            p0 = ld4(T.p + i);
-            p1 = ld4(T.p + T.n + i);
-            p2 = ld4(T.p + 2 * T.n + i);
+            if (!T.chambolle) {
+                p0 = ld4(T.p + i);
+                p1 = ld4(T.p + T.n + i);
+                p2 = ld4(T.p + 2 * T.n + i);
+            }
         }
     }
     if (act) *reinterpret_cast<float4*>(&su[row][4 + 4 * lane]) = make_float4(u[0], u[1], u[2], u[3]);
@@ -662,6 +686,13 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
         const float gy = y >= 1 ? u[k] - upa[k] : 0.f;
         const float gz = z >= 1 ? u[k] - uz[k] : 0.f;
         const float a0 = qa[0][k] + gx * s, a1 = qa[1][k] + gy * s, a2 = qa[2][k] + gz * s;
+        if (T.chambolle) {       // p <- (p + s g) / (1 + s |g|); qo = the new p
+            const float d = 1.f / (1.f + s * sqrtf(gx * gx + gy * gy + gz * gz));
+            qo[0][k] = a0 * d;
+            qo[1][k] = a1 * d;
+            qo[2][k] = a2 * d;
+            continue;
+        }
         const float n2 = a0 * a0 + a1 * a1 + a2 * a2;
         const float inv = n2 > 1.f ? rsqrtf(n2) : 1.f;
         po[0][k] = a0 * inv;
@@ -673,7 +704,7 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         st4(T.q_out + c * T.n + i, qo[c][0], qo[c][1], qo[c][2], qo[c][3]);
-        st4(T.p + c * T.n + i, po[c][0], po[c][1], po[c][2], po[c][3]);
+        if (!T.chambolle) st4(T.p + c * T.n + i, po[c][0], po[c][1], po[c][2], po[c][3]);
     }
 }
 

@@ -306,14 +306,17 @@ def test_trajectory_cfg3_bsgd_and_sgd(bs):
     print("cfg3 SGD", _compare(o, res, x, sgd=True))
 
 
-def test_trajectory_tv_auto_mu(bs):
+@pytest.mark.parametrize("method", ["fgp", "chambolle"])
+def test_trajectory_tv_auto_mu(bs, method):
     """BSGD-TV (Algo 4) + auto-mu (Algo 3) on a scaled cfg4 (M = 10, N = 8)."""
     p, g, vol32, y = problem("cfg4", K=48, n_views=60)
     P = Projector(g, BlockGrid(g.dims, p.blocks))
     mu = 2.0 / ob.power_iteration(P, 30, seed=1)        # large: auto-mu must act
-    o, res, x = _run_pair(bs, p, g, vol32, y, 60, mu, flags=bs.TV | bs.AUTO_MU,
-                          oracle_kw=dict(tv=True, auto_mu=True, lam=0.1), run_kw=dict(lam=0.1, tv_iters=20))
-    print("cfg4-scaled TV+auto-mu", _compare(o, res, x), "mu:", res.mu[::10])
+    extra = bs.TV_CHAMBOLLE if method == "chambolle" else 0
+    o, res, x = _run_pair(bs, p, g, vol32, y, 60, mu, flags=bs.TV | bs.AUTO_MU | extra,
+                          oracle_kw=dict(tv=True, auto_mu=True, lam=0.1, tv_method=method),
+                          run_kw=dict(lam=0.1, tv_iters=20))
+    print(f"cfg4-scaled TV({method})+auto-mu", _compare(o, res, x), "mu:", res.mu[::10])
 
 
 def test_trajectory_stratified(bs):
@@ -547,7 +550,8 @@ def test_trajectory_fuzz(bs, seed):
     ((64, 48, 1), (1, 1, 1), 0.5, 50),      # fused 2D (nz = 1, L = 8)
     ((24, 16, 20), (2, 2, 2), 0.3, 20),     # octants: the generic two-kernel path
 ])
-def test_tv_prox_parity(bs, dims, blocks, w, iters):
+@pytest.mark.parametrize("method", ["fgp", "chambolle"])
+def test_tv_prox_parity(bs, dims, blocks, w, iters, method):
     """bsgd_tv_prox (Algo 4 line 16; FGP, reading A16) per voxel against the
     oracle's tv_prox on the same fp32 input: |d| <= 1e-5 (|b|_inf + w)."""
     nx, ny, nz = dims
@@ -563,13 +567,13 @@ def test_tv_prox_parity(bs, dims, blocks, w, iters):
                                       1.0, 1.0), 8, 8 if nz > 1 else 1, dims)
     ctx = bs.Context.from_geometry(g, blocks, 1)
     x = torch.from_numpy(bx.to_blocks(vol).ravel().copy()).cuda()
-    ctx.tv_prox(x, w, iters)
+    ctx.tv_prox(x, w, iters, method)
     torch.cuda.synchronize()
     got = bx.from_blocks(x.cpu().numpy())
-    want = ob.tv_prox(vol.astype(np.float64), w, iters)
+    want = ob.tv_prox(vol.astype(np.float64), w, iters, method)
     err = np.abs(got - want).max()
     bar = 1e-5 * (np.abs(vol).max() + w)
-    print(f"tv_prox {dims} {blocks}: max|d| {err:.3g} (bar {bar:.3g}), max|x - b| {np.abs(want - vol).max():.3g}")
+    print(f"tv_prox {method} {dims} {blocks}: max|d| {err:.3g} (bar {bar:.3g}), max|x - b| {np.abs(want - vol).max():.3g}")
     assert err <= bar
     assert np.abs(want - vol).max() > 10 * bar          # the prox moved x: the check is not vacuous
     # w = 0 and iters = 0 are the identity

@@ -345,3 +345,24 @@ def test_select_stratified():
     assert ob.select_stratified(1, 0, 8, 8, 8) == list(range(8))   # gamma N = N: every block
     with pytest.raises(ValueError):
         ob.select_stratified(1, 0, 8, 3, 2)
+
+
+def test_tv_prox_chambolle_closed_forms():
+    """The Chambolle-2004 flag converges to the same prox: the exact 1D-ROF step solutions
+    (levels w/L1, w/L2 toward each other) and the FGP result at many iterations; identity
+    for w = 0; a constant image is a fixed point."""
+    step = np.zeros((1, 8, 8))
+    step[..., 4:] = 1.0
+    for w, lo, hi in [(0.5, 0.125, 0.875), (3.0, 0.5, 0.5)]:
+        t = ob.tv_prox(step, w, iters=40000, method="chambolle")
+        assert np.max(np.abs(t[..., :4] - lo)) < 1e-6 and np.max(np.abs(t[..., 4:] - hi)) < 1e-6
+    s3 = np.zeros((3, 4, 8))
+    s3[..., 2:] = 1.0
+    t = ob.tv_prox(s3, 0.2, iters=40000, method="chambolle")
+    assert np.max(np.abs(t[..., :2] - 0.1)) < 1e-6 and np.max(np.abs(t[..., 2:] - (1 - 0.2 / 6))) < 1e-6
+    c = np.full((2, 5, 6), -1.5)
+    assert np.max(np.abs(ob.tv_prox(c, 0.7, 50, method="chambolle") - c)) < 1e-12
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((3, 6, 7))
+    assert np.array_equal(ob.tv_prox(b, 0.0, method="chambolle"), b)
+    assert np.max(np.abs(ob.tv_prox(b, 0.3, 30000, method="chambolle") - ob.tv_prox(b, 0.3, 5000))) < 1e-5
