@@ -74,9 +74,21 @@ typedef struct { int32_t bx, by, bz; } bsgd_block_grid;
  * groups"): kind 0 = seeded random partition, 1 = contiguous, 2 = interleaved.
  * tiles_u x tiles_v = sub-detector tiles of BSGD-IM (Fig. 2). */
 typedef struct { int32_t M, kind; uint64_t seed; int32_t tiles_u, tiles_v; } bsgd_row_grid;
+/* Virtual ranks: `world` logical ranks in ONE process on one GPU,
+ * each a bsgd_ctx driven by its own host thread and CUDA stream.  The collectives of the
+ * NCCL path become device copies between the ranks' buffers, ordered by events and host
+ * barriers: the allreduce is a fixed-order (rank-ascending) device sum, the halo
+ * send/recv a peer copy.  Exercises ownership, partial sums, allreduces and TV halos
+ * exactly as G GPUs would, on one GPU.  A rank that never reaches a collective makes the
+ * others fail with BSGD_E_NCCL after 120 s.                                              */
+typedef struct bsgd_vgroup_s* bsgd_vgroup;
+bsgd_status bsgd_vgroup_create(int32_t world, bsgd_vgroup* out);
+void bsgd_vgroup_destroy(bsgd_vgroup group);   /* after every member ctx is destroyed   */
+
 /* Multi-GPU: one process per GPU; nccl_id = 128 bytes from bsgd_nccl_unique_id
- * on rank 0, broadcast by the caller (NULL when world == 1).                 */
-typedef struct { int32_t rank, world; const uint8_t* nccl_id; } bsgd_dist;
+ * on rank 0, broadcast by the caller (NULL when world == 1).  vgroup: non-NULL for a
+ * virtual rank (bsgd_vgroup_create; nccl_id is then ignored).                   */
+typedef struct { int32_t rank, world; const uint8_t* nccl_id; bsgd_vgroup vgroup; } bsgd_dist;
 /* Device allocator used for ALL ctx state (Python points it at the torch
  * caching allocator).  NULL = cudaMalloc/cudaFree.                           */
 typedef struct {

@@ -60,7 +60,8 @@ class RowGrid(C.Structure):
 
 
 class Dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8))]
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8)),
+                ("vgroup", C.c_void_p)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -120,6 +121,8 @@ SIGS = {
     "bsgd_nccl_unique_id": ([P(C.c_uint8)], C.c_int),
     "bsgd_create": ([P(Geometry), Dims, BlockGrid, RowGrid, P(Dist), P(Alloc), P(_ctx)], C.c_int),
     "bsgd_destroy": ([_ctx], None),
+    "bsgd_vgroup_create": ([C.c_int32, P(C.c_void_p)], C.c_int),
+    "bsgd_vgroup_destroy": ([C.c_void_p], None),
     "bsgd_get_info": ([_ctx, P(Info)], C.c_int),
     "bsgd_row_block_views": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
     "bsgd_forward": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
@@ -284,11 +287,33 @@ class RunResult:
     t_ms: Optional[np.ndarray]
 
 
+class VirtualGroup:
+    """`world` logical ranks in this process on one GPU (bsgd_vgroup_create): create one
+    Context(..., rank=r, world=world, vgroup=group) per rank and drive each from its own
+    thread and CUDA stream; their collectives meet inside the library."""
+
+    def __init__(self, world):
+        h = C.c_void_p()
+        _check(_lib.bsgd_vgroup_create(int(world), C.byref(h)))
+        self.h, self.world = h.value, int(world)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.bsgd_vgroup_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One BSGD problem on this process's GPU (bsgd_create ... bsgd_destroy)."""
 
     def __init__(self, beam, vecs, det, dims, blocks, M, kind=0, row_seed=0, tiles=(1, 1),
-                 rank=0, world=1, nccl_id=None, torch_alloc=True, device=None):
+                 rank=0, world=1, nccl_id=None, torch_alloc=True, device=None, vgroup=None):
         import torch
         self.device = torch.cuda.current_device() if device is None else device
         self.vecs = np.ascontiguousarray(vecs, dtype=np.float64)
@@ -297,9 +322,12 @@ class Context:
         g = Geometry(int(b), self.vecs.shape[0], int(det[0]), int(det[1]), self.vecs.ctypes.data_as(P(C.c_double)))
         self._idbuf = None
         dist = None
-        if world > 1:
+        if world > 1 and vgroup is not None:      # virtual rank (VirtualGroup)
+            dist = Dist(rank, world, None, vgroup.h)
+            self._vgroup = vgroup                  # keep the group alive while this ctx lives
+        elif world > 1:
             self._idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-            dist = Dist(rank, world, C.cast(self._idbuf, P(C.c_uint8)))
+            dist = Dist(rank, world, C.cast(self._idbuf, P(C.c_uint8)), None)
         self._alloc = _TorchAllocator(self.device) if torch_alloc else None
         h = _ctx()
         with torch.cuda.device(self.device):

@@ -14,6 +14,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstdio>
 #include <memory>
 #include <new>
@@ -50,6 +53,29 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
 
 using namespace bsgd;
 
+// Virtual-rank group (bsgd_vgroup_create): `world` contexts of one process share it.
+struct bsgd_vgroup_s {
+    int world = 1;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long gen = 0;
+    std::vector<const void*> src;          // per rank: the buffer it offers in the current collective
+    std::vector<cudaEvent_t> ev1, ev2;     // per rank: "offered buffer ready", "my reads are done"
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const unsigned long long g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; }))
+            fail(BSGD_E_NCCL, "virtual group: barrier timeout (a rank did not reach the collective)");
+    }
+};
+
 struct bsgd_ctx_s {
     // ---- configuration
     int beam = 0, n_views = 0, nu = 0, nv = 0;
@@ -59,6 +85,10 @@ struct bsgd_ctx_s {
     uint64_t row_seed = 0;
     int rank = 0, world = 1, first = 0, s = 1;
     bool coll = false;     // collective code path (world > 1, or BSGD_FORCE_NCCL=1 with one rank)
+    bsgd_vgroup vg = nullptr;   // virtual rank: collectives through the in-process group
+    void* vg_tmp = nullptr;
+    double* d_rpart = nullptr;   // k_residual per-CTA partials of ||r||^2
+    size_t vg_tmp_bytes = 0;
     long long bsize = 0, n_rays = 0, per = 0;
     double R = 0.0;
     std::vector<std::vector<int>> rows;   // views of each row block (sorted)
@@ -351,10 +381,40 @@ struct bsgd_ctx_s {
     }
 
     void allreduce_f(float* p, size_t n, cudaStream_t st) {
-        if (coll) BSGD_NCCL(ncclAllReduce(p, p, n, ncclFloat, ncclSum, comm, st));
+        if (vg) vg_allreduce(p, n, false, st);
+        else if (coll) BSGD_NCCL(ncclAllReduce(p, p, n, ncclFloat, ncclSum, comm, st));
     }
     void allreduce_d(double* p, size_t n, cudaStream_t st) {
-        if (coll) BSGD_NCCL(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, st));
+        if (vg) vg_allreduce(p, n, true, st);
+        else if (coll) BSGD_NCCL(ncclAllReduce(p, p, n, ncclDouble, ncclSum, comm, st));
+    }
+
+    // ---- virtual ranks: the two collective shapes as events + host barriers + device work
+    void vg_offer(const void* p, cudaStream_t st) {
+        BSGD_CUDA(cudaEventRecord(vg->ev1[rank], st));
+        vg->src[rank] = p;
+        vg->barrier();
+    }
+    void vg_release(cudaStream_t st) {   // nobody reuses an offered buffer before all have read it
+        BSGD_CUDA(cudaEventRecord(vg->ev2[rank], st));
+        vg->barrier();
+        for (int g = 0; g < world; ++g) BSGD_CUDA(cudaStreamWaitEvent(st, vg->ev2[g], 0));
+    }
+    void vg_allreduce(void* p, size_t n, bool dbl, cudaStream_t st) {
+        const size_t bytes = n * (dbl ? sizeof(double) : sizeof(float));
+        if (bytes > vg_tmp_bytes) {
+            vg_tmp = dalloc(bytes);
+            vg_tmp_bytes = bytes;
+        }
+        vg_offer(p, st);
+        const void* srcs[8];
+        for (int g = 0; g < world; ++g) {
+            srcs[g] = vg->src[g];
+            BSGD_CUDA(cudaStreamWaitEvent(st, vg->ev1[g], 0));
+        }
+        launch_sum_ptrs(vg_tmp, srcs, world, (long long)n, dbl, st);   // rank-ascending order
+        vg_release(st);
+        BSGD_CUDA(cudaMemcpyAsync(p, vg_tmp, bytes, cudaMemcpyDeviceToDevice, st));
     }
 
     // ------------------------------------------------------------ one epoch
@@ -461,6 +521,8 @@ struct bsgd_ctx_s {
             Rl.r = r;
             Rl.pc = pc;
             Rl.normsq = d_normsq;
+            Rl.part = d_rpart;
+            Rl.M = M;
             launch_zero_rows(d_normsq, drows, (int)sel_rows.size(), st);
             if (!coll) {
                 Rl.mode = 0;
@@ -575,6 +637,8 @@ struct bsgd_ctx_s {
         Rl.r = r;
         Rl.pc = pc;
         Rl.normsq = d_normsq;
+        Rl.part = d_rpart;
+        Rl.M = M;
         Rl.mode = 0;
         launch_residual(Rl, st);   // no allreduce needed
     }
@@ -690,6 +754,8 @@ struct bsgd_ctx_s {
             Rl.r = r;
             Rl.pc = pc;
             Rl.normsq = d_normsq;
+            Rl.part = d_rpart;
+            Rl.M = M;
             launch_zero_rows(d_normsq, drows, (int)rsel.size(), st);
             Rl.mode = coll ? 1 : 0;
             launch_residual(Rl, st);
@@ -887,6 +953,16 @@ struct bsgd_ctx_s {
     // plane into dst; otherwise send my last plane (src) to rank+1, receive from rank-1.
     void halo_exchange(const float* src, float* dst, long long plane, bool down, cudaStream_t st) {
         if (world == 1) return;
+        if (vg) {
+            vg_offer(src, st);
+            const int from = down ? rank + 1 : rank - 1;
+            if (from >= 0 && from < world) {
+                BSGD_CUDA(cudaStreamWaitEvent(st, vg->ev1[from], 0));
+                BSGD_CUDA(cudaMemcpyAsync(dst, vg->src[from], sizeof(float) * plane, cudaMemcpyDeviceToDevice, st));
+            }
+            vg_release(st);
+            return;
+        }
         BSGD_NCCL(ncclGroupStart());
         if (down) {
             if (rank > 0) BSGD_NCCL(ncclSend(src, plane, ncclFloat, rank - 1, comm, st));
@@ -1082,7 +1158,13 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
             c->world = dist->world;
             if (c->rank < 0 || c->rank >= c->world) fail(BSGD_E_CONTRACT, "bad rank");
             if (c->N % c->world) fail(BSGD_E_PARTITION, "N must be divisible by the number of ranks");
-            if (!dist->nccl_id) fail(BSGD_E_CONTRACT, "nccl_id required when world > 1");
+            if (dist->vgroup) {
+                if (dist->vgroup->world != c->world) fail(BSGD_E_CONTRACT, "world differs from the virtual group's");
+                if (c->world > 8) fail(BSGD_E_CONTRACT, "virtual groups hold at most 8 ranks");
+                c->vg = dist->vgroup;
+            } else if (!dist->nccl_id) {
+                fail(BSGD_E_CONTRACT, "nccl_id required when world > 1");
+            }
         }
         c->s = c->N / c->world;
         c->first = c->rank * c->s;
@@ -1147,12 +1229,17 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         if (c->world > 1) c->coll = true;
         c->pc = c->coll ? c->dnew<float>(c->n_rays) : nullptr;
         c->d_normsq = c->dnew<double>(c->M);
+        c->d_rpart = c->dnew<double>((long long)c->n_views * RES_GX);
         c->d_red = c->dnew<double>(16);
         c->d_visits = c->dnew<unsigned long long>(1);
         c->tab_bytes = 2 * (size_t)(64 + 16 * ((size_t)c->n_views * (2 + 4LL * c->s + 1) + 64LL * c->s + c->M) + 4096);
         c->d_tab = (char*)c->dalloc(c->tab_bytes);
         c->h_normsq.assign(c->M, 0.0);
-        if (c->world > 1) {
+        if (c->vg) {
+            std::lock_guard<std::mutex> lk(c->vg->m);
+            BSGD_CUDA(cudaEventCreateWithFlags(&c->vg->ev1[c->rank], cudaEventDisableTiming));
+            BSGD_CUDA(cudaEventCreateWithFlags(&c->vg->ev2[c->rank], cudaEventDisableTiming));
+        } else if (c->world > 1) {
             ncclUniqueId id;
             memcpy(&id, dist->nccl_id, sizeof id);
             BSGD_NCCL(ncclCommInitRank(&c->comm, c->world, id, c->rank));
@@ -1170,6 +1257,26 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
     }
     *out = c.release();
     return BSGD_OK;
+}
+
+bsgd_status bsgd_vgroup_create(int32_t world, bsgd_vgroup* out) {
+    return guard(nullptr, [&] {
+        if (!out || world < 1 || world > 8) fail(BSGD_E_CONTRACT, "virtual group: 1 <= world <= 8");
+        auto* g = new bsgd_vgroup_s();
+        g->world = world;
+        g->src.assign(world, nullptr);
+        g->ev1.assign(world, nullptr);
+        g->ev2.assign(world, nullptr);
+        *out = g;
+    });
+}
+
+void bsgd_vgroup_destroy(bsgd_vgroup g) {
+    if (!g) return;
+    cudaDeviceSynchronize();
+    for (auto e : g->ev1) if (e) cudaEventDestroy(e);
+    for (auto e : g->ev2) if (e) cudaEventDestroy(e);
+    delete g;
 }
 
 void bsgd_destroy(bsgd_ctx ctx) {

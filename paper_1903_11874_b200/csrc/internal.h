@@ -130,8 +130,11 @@ struct ResLaunch {
     float* r;
     float* pc;              // compact partial sums [n_slots*per] (world > 1)
     double* normsq;         // [M]
+    double* part;           // [n_slots][RES_GX] per-CTA partial ||r||^2 (fixed-order final sum)
+    int M;                  // row blocks (normsq entries)
     int mode;               // 0 = fused r = y - sum z (world 1); 1 = pc = sum z; 2 = r = y - pc
 };
+constexpr int RES_GX = 64;   // max CTAs per view slot of k_residual
 void launch_residual(const ResLaunch& R, cudaStream_t st);
 
 void launch_zero_rows(double* normsq, const int* rows, int n, cudaStream_t st);
@@ -182,6 +185,8 @@ struct TvLaunch {
 };
 void launch_tv_u(const TvLaunch& T, const float* src_q, float* dst, cudaStream_t st);
 void launch_tv_pq(const TvLaunch& T, cudaStream_t st);
+// out[i] = sum_{g = 0..G-1} ptrs[g][i] in ascending g (virtual-rank allreduce), G <= 8
+void launch_sum_ptrs(void* out, const void* const* ptrs, int G, long long n, bool dbl, cudaStream_t st);
 // One fused FGP iteration (u, projection, momentum) for z-slab layouts (bgrid = 1 x 1 x N):
 // reads q, p, b (+ halos), writes q_out, p.
 void launch_tv_fgp(const TvLaunch& T, cudaStream_t st);

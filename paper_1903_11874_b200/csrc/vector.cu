@@ -258,10 +258,29 @@ __global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
             }
         }
     }
-    if (R.mode != 1) {
-        ss = block_sum(ss);
-        if (threadIdx.x == 0) atomicAdd(R.normsq + R.slot_row[slot], ss);
+    if (R.mode != 1) {   // per-CTA partial; k_normsq_final sums them in a fixed order so
+        ss = block_sum(ss);  // that ||r_I||^2 (Algo 3's decisions) is bit-identical on every rank
+        if (threadIdx.x == 0) R.part[(size_t)slot * RES_GX + blockIdx.x] = ss;
     }
+}
+
+// normsq[i] = sum of the partials of the slots of row block i (CTA i; fixed assignment of
+// partials to threads and a fixed reduction tree: deterministic).  Rows without slots keep
+// their value.
+__global__ void __launch_bounds__(256) k_normsq_final(const ResLaunch R, int gx) {
+    const int i = blockIdx.x;
+    double ss = 0.0;
+    int hit = 0;
+    for (long long q = threadIdx.x; q < (long long)R.n_slots * gx; q += blockDim.x) {
+        const int slot = (int)(q / gx), b = (int)(q % gx);
+        if (R.slot_row[slot] == i) {
+            ss += R.part[(size_t)slot * RES_GX + b];
+            hit = 1;
+        }
+    }
+    ss = block_sum(ss);
+    hit = __syncthreads_or(hit);
+    if (threadIdx.x == 0 && hit) R.normsq[i] = ss;
 }
 
 __global__ void __launch_bounds__(256) k_zero_rects(float* proj, const int* views, const int4* rects, int nu,
@@ -717,6 +736,20 @@ __global__ void __launch_bounds__(TV_TX * TV_TY) k_tv_out(const TvLaunch T, floa
     out[i] = tv_u_at(T, tv_plane(T, z), x, y, z, T.wf);
 }
 
+struct PtrPack {
+    const void* p[8];
+};
+
+template <class T>
+__global__ void __launch_bounds__(256) k_sum_ptrs(T* out, const PtrPack P, int G, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        T s = static_cast<const T*>(P.p[0])[i];
+        for (int g = 1; g < G; ++g) s += static_cast<const T*>(P.p[g])[i];
+        out[i] = s;
+    }
+}
+
 unsigned grid_for(long long n, int per_thread = 1) {
     long long b = (n / per_thread + 255) / 256;
     if (b < 1) b = 1;
@@ -753,10 +786,15 @@ void launch_block_update(int mode, const UpdLaunch& U, cudaStream_t st) {
 void launch_residual(const ResLaunch& R, cudaStream_t st) {
     if (R.n_slots == 0) return;
     long long nvec = (R.per % 4 == 0) ? R.per / 4 : R.per;
-    unsigned gx = (unsigned)std::min<long long>((nvec + 255) / 256, 64);
+    unsigned gx = (unsigned)std::min<long long>((nvec + 255) / 256, RES_GX);
     k_residual<<<dim3(gx, (unsigned)R.n_slots), 256, 0, st>>>(R);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
+    if (R.mode != 1) {
+        k_normsq_final<<<R.M, 256, 0, st>>>(R, (int)gx);
+        BSGD_CUDA(cudaGetLastError());
+        note_launch();
+    }
 }
 
 void launch_zero_rects(float* proj, const int* views, const int4* rects, int n, int nu, int nv, cudaStream_t st) {
@@ -824,6 +862,15 @@ void launch_scale(float* v, long long n, const double* nrm, cudaStream_t st) {
 
 void launch_tv_u(const TvLaunch& T, const float* src, float* dst, cudaStream_t st) {
     k_tv_u<<<grid_for(T.n, 2), 256, 0, st>>>(T, src, dst);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_sum_ptrs(void* out, const void* const* ptrs, int G, long long n, bool dbl, cudaStream_t st) {
+    PtrPack P;
+    for (int g = 0; g < 8; ++g) P.p[g] = g < G ? ptrs[g] : nullptr;
+    if (dbl) k_sum_ptrs<double><<<grid_for(n, 4), 256, 0, st>>>(static_cast<double*>(out), P, G, n);
+    else k_sum_ptrs<float><<<grid_for(n, 4), 256, 0, st>>>(static_cast<float*>(out), P, G, n);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
