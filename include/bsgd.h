@@ -170,6 +170,11 @@ bsgd_status bsgd_im_weights(bsgd_ctx ctx, double* w_out, uint32_t* q_out);
 /* As bsgd_im_weights for a chosen weight kind: 0 = L1 mass (chord sums, the default of
  * BSGD_IS), 1 = projection area (count of tile rays with chord > 1e-6, BSGD_IS_AREA).     */
 bsgd_status bsgd_im_table(bsgd_ctx ctx, int32_t kind, double* w_out, uint32_t* q_out);
+/* The visit table behind the intersections/s metric (SURVEY §8b, §8d "exact visit counts"):
+ * nnz_out[b][view][tile] (host, owned blocks x n_views x tiles) = number of ray-voxel
+ * intersections of block first+b, view `view`, detector tile `tile` -- Siddon segments longer
+ * than 1e-6 of a main-axis slice, from one COUNT traversal at the first call (cached).  */
+bsgd_status bsgd_visit_table(bsgd_ctx ctx, uint64_t* nnz_out);
 
 /* ---- algorithm state ------------------------------------------------------ */
 /* Algo 1 line 1: z^j = 0, g_hat^i = 0, g = 0, r = y, epoch = 0.

@@ -131,6 +131,7 @@ SIGS = {
                    C.c_int32, C.c_void_p], C.c_int),
     "bsgd_im_weights": ([_ctx, P(C.c_double), P(C.c_uint32)], C.c_int),
     "bsgd_im_table": ([_ctx, C.c_int32, P(C.c_double), P(C.c_uint32)], C.c_int),
+    "bsgd_visit_table": ([_ctx, P(C.c_uint64)], C.c_int),
     "bsgd_reset": ([_ctx, C.c_void_p, C.c_void_p], C.c_int),
     "bsgd_step": ([_ctx, C.c_void_p, C.c_void_p, P(Selection), C.c_float, C.c_uint32, C.c_void_p], C.c_int),
     "bsgd_run": ([_ctx, C.c_void_p, C.c_void_p, C.c_void_p, P(RunParams), P(RunLog), C.c_void_p], C.c_int),
@@ -383,6 +384,13 @@ class Context:
         r, rp = _i32(rects) if rects is not None else (None, None)
         self._c(_lib.bsgd_back(self.h, len(v), vp, rp, col_block, _ptr(proj), _ptr(g_block), float(scale),
                                int(accumulate), _stream(stream)))
+
+    def visit_table(self):
+        """uint64 [owned block][view][tile] ray-voxel intersection counts (bsgd_visit_table)."""
+        T = self.info.tiles
+        out = np.zeros((self.owned_count, self.info.n_views, T), dtype=np.uint64)
+        self._c(_lib.bsgd_visit_table(self.h, out.ctypes.data_as(P(C.c_uint64))))
+        return out
 
     def im_weights(self, area=False):
         """(w, q) of the IM table: L1 mass (default) or, area=True, the BSGD_IS_AREA counts."""

@@ -1376,6 +1376,14 @@ bsgd_status bsgd_im_table(bsgd_ctx c, int32_t kind, double* w_out, uint32_t* q_o
     });
 }
 
+bsgd_status bsgd_visit_table(bsgd_ctx c, uint64_t* nnz_out) {
+    return guard(c, [&] {
+        if (!c || !nnz_out) fail(BSGD_E_CONTRACT, "NULL");
+        c->ensure_visit_table(nullptr);
+        for (size_t k = 0; k < c->vtab.size(); ++k) nnz_out[k] = c->vtab[k];
+    });
+}
+
 bsgd_status bsgd_reset(bsgd_ctx c, const float* y, void* stream) {
     return guard(c, [&] {
         if (!c || !y) fail(BSGD_E_CONTRACT, "NULL");

@@ -200,6 +200,13 @@ def test_visit_counts(bs, name, kw):
         want = sum(int(np.count_nonzero(P.csr(views, int(j)).data > 1.2e-6)) for j in res.sel_cols[e])
         got = int(res.visits[e])
         assert abs(got - want) <= 2, (e, got, want)
+    # the table itself (bsgd_visit_table) per (block, view) for a few views
+    vt = ctx.visit_table()
+    assert vt.shape == (p.N, g.n_views, p.tiles[0] * p.tiles[1])
+    for v in (0, g.n_views // 3, g.n_views - 1):
+        for j in range(p.N):
+            want = int(np.count_nonzero(P.csr([v], j).data > 1.2e-6))
+            assert abs(int(vt[j, v].sum()) - want) <= 1, (v, j, int(vt[j, v].sum()), want)
     ctx.close()
 
 
