@@ -262,6 +262,8 @@ def run_ours(args, rank, world, local_rank):
     # cfg4's schedule: BSGD-TV (Algo 4, lambda = 0.1; period
     # round(1/(alpha gamma)) = 40 epochs) + automatic mu (Algo 3)
     sched = (bs.TV | bs.AUTO_MU) if args.config == "cfg4" else 0
+    if args.det:   # order-independent 64-bit fixed-point BP reductions (bit-reproducible runs)
+        sched |= bs.DETERMINISTIC
     if args.eq8:   # Eq. 8 with NodeNum = G, columns stratified by owner (N3)
         aM, gN = 0, 0
         sched |= bs.STRATIFIED
@@ -355,7 +357,8 @@ def run_ours(args, rank, world, local_rank):
         "intersections_per_s": visits_all / (t_ms / 1e3),
         "config": {"workload": workload(p) + (f" [Eq. 8 schedule at NodeNum = {world}: alpha*M = "
                                               f"{res.sel_rows.shape[1]}, gamma*N = {res.sel_cols.shape[1]}, "
-                                              "columns stratified by owner]" if args.eq8 else ""),
+                                              "columns stratified by owner]" if args.eq8 else "")
+                   + (" [BSGD_DETERMINISTIC: fixed-point BP]" if args.det else ""),
                    "global_batch": int(res.sel_rows.shape[1]) * (g.n_views // p.M),
                    "parallelism": f"z-slab{world}" if p.blocks[:2] == (1, 1) else f"blocks{world}",
                    "l2": ("inputs larger than L2 (537 MB slabs, 3.0 GB y); no flush needed" if p.name == "cfg5"
@@ -436,6 +439,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-tv", action="store_true", help="skip the separate TV-prox timing")
+    ap.add_argument("--det", action="store_true", help="BSGD_DETERMINISTIC (fixed-point BP reductions)")
     ap.add_argument("--eq8", action="store_true",
                     help="Eq. 8 schedule (gamma N = G, alpha M from Eq. 8), stratified by owner: weak scaling")
     ap.add_argument("--cheap-data", action="store_true", help="uniform random y instead of analytic projections")

@@ -195,14 +195,19 @@ enum {
     BSGD_IS_AREA = 256,     /* with BSGD_IS: weights = number of tile rays that cross the block
                                (chord > 1e-6), the "projection area" reading of PAPER.md:162,
                                instead of the default L1 mass (reading A9)                  */
-    BSGD_TV_CHAMBOLLE = 512 /* with BSGD_TV: Chambolle-2004 dual iteration instead of FGP   */
+    BSGD_TV_CHAMBOLLE = 512, /* with BSGD_TV: Chambolle-2004 dual iteration instead of FGP  */
+    BSGD_DETERMINISTIC = 1024 /* bsgd_run / bsgd_step: BP by 64-bit fixed-point reductions
+                               (scale 2^e from max|r|, resolution ~1e-15 max|r|): g_hat, g and
+                               x do not depend on the order of the BP threads; bit-identical
+                               runs (SURVEY §8b Determinism).  64-bit REDs double the BP's L2
+                               reduction traffic: cfg5 BP 105 -> 197 ms, 4.6 -> 3.2 epochs/s */
 };
 
 /* One epoch of Algo 1 / Algo 2 with an explicit selection (identical on all
  * ranks).  rows: sorted row-block ids; cols: sorted column-block ids;
  * im_tiles: NULL (Algo 1) or host [n_cols][V_sel] tile ids, V_sel = number of
  * views of the selected row blocks in ascending row-block order (Algo 2 l.5).
- * flags: BSGD_SGD only.  Contains the residual allreduce when world > 1.     */
+ * flags: BSGD_SGD, BSGD_DETERMINISTIC.  Contains the residual allreduce when world > 1. */
 typedef struct {
     int32_t n_rows; const int32_t* rows;
     int32_t n_cols; const int32_t* cols;

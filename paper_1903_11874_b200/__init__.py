@@ -28,8 +28,8 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 PARALLEL, FAN, CONE = 0, 1, 2
-IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED, IS_AREA, TV_CHAMBOLLE = \
-    1, 2, 4, 8, 16, 32, 64, 128, 256, 512
+IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED, IS_AREA, TV_CHAMBOLLE, DETERMINISTIC = \
+    1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024
 STATUS = {0: "OK", 1: "E_GEOMETRY", 2: "E_PARTITION", 3: "E_DIMENSION", 4: "E_CONTRACT", 5: "E_CUDA",
           6: "E_NCCL", 7: "E_OOM", 8: "E_POISONED"}
 

@@ -88,6 +88,12 @@ struct bsgd_ctx_s {
     bsgd_vgroup vg = nullptr;   // virtual rank: collectives through the in-process group
     void* vg_tmp = nullptr;
     double* d_rpart = nullptr;   // k_residual per-CTA partials of ||r||^2
+    // deterministic BP (BSGD_DETERMINISTIC): int64 fixed-point twins of accN / accT
+    bool det = false;
+    long long* acc64N = nullptr;
+    long long* acc64T = nullptr;
+    float* d_det_scale = nullptr;
+    unsigned* d_det_max = nullptr;
     size_t vg_tmp_bytes = 0;
     long long bsize = 0, n_rays = 0, per = 0;
     double R = 0.0;
@@ -348,6 +354,7 @@ struct bsgd_ctx_s {
         L.scale = scale;
         L.accumulate = accumulate;
         L.visits = (mode == PROJ_COUNT) ? count_target : nullptr;
+        L.det_scale = d_det_scale;
         if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
         BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_off, staging.data() + tab_off, off - tab_off,
                                   cudaMemcpyHostToDevice, st));
@@ -545,7 +552,7 @@ struct bsgd_ctx_s {
         }
         if (sgd) {   // Eq. 4: g = 2 A_I^T r_I over all selected rows, no memory
             std::vector<int4> rc((size_t)nb * V, make_int4(0, nu, 0, nv));
-            project(PROJ_BP, vsel, oslots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
+            bp(vsel, oslots, rc, oN, oT, st);
             if (ev) BSGD_CUDA(cudaEventRecord(ev[3], st));
             for (int b = 0; b < nb; ++b)
                 update(UPD_SGD, oslots[b], x_owned + oslots[b] * bsize, mu_, 1, nullptr, 0, st);
@@ -569,7 +576,7 @@ struct bsgd_ctx_s {
                                                       sizeof(float) * bsize, cudaMemcpyDeviceToHost, copy_st));
                     for (int b = 0; b < nb; ++b) {
                         std::vector<int4> rcb(rc.begin() + (size_t)b * Vi, rc.begin() + (size_t)(b + 1) * Vi);
-                        project(PROJ_BP, vi, {oslots[b]}, rcb, none, none, {oN[b]}, {oT[b]}, {}, r, 2.f, 0, st, 0);
+                        bp(vi, {oslots[b]}, rcb, {oN[b]}, {oT[b]}, st);
                         update(UPD_BSGD, oslots[b], x_owned + oslots[b] * bsize, mu_, fin, nullptr, 0, st,
                                nullptr, nullptr, nullptr, i);
                         BSGD_CUDA(cudaEventRecord(up_ev[b], st));
@@ -580,7 +587,7 @@ struct bsgd_ctx_s {
                     }
                     if (ev) BSGD_CUDA(cudaEventRecord(ev[3], st));
                 } else {
-                    project(PROJ_BP, vi, oslots, rc, none, none, oN, oT, {}, r, 2.f, 0, st, 0);
+                    bp(vi, oslots, rc, oN, oT, st);
                     if (ev && fin) BSGD_CUDA(cudaEventRecord(ev[3], st));
                     for (int b = 0; b < nb; ++b)
                         update(UPD_BSGD, oslots[b], x_owned + oslots[b] * bsize, mu_, fin, nullptr, 0, st,
@@ -590,6 +597,38 @@ struct bsgd_ctx_s {
             }
         }
         if (ev) BSGD_CUDA(cudaEventRecord(ev[4], st));
+    }
+
+    // BP of views `vv` into the accumulators of `slots` (oN / oT: their accN / accT interiors):
+    // fp32 REDs, or with `det` 64-bit fixed-point REDs into int64 twins converted afterwards,
+    // which makes g_hat independent of the order of the ray threads (SURVEY §8b Determinism)
+    void bp(const std::vector<int>& vv, const std::vector<int>& slots, const std::vector<int4>& rc,
+            const std::vector<float*>& oN, const std::vector<float*>& oT, cudaStream_t st) {
+        if (!det) {
+            project(PROJ_BP, vv, slots, rc, {}, {}, oN, oT, {}, r, 2.f, 0, st, 0);
+            return;
+        }
+        const size_t rawN = (size_t)s * padN + 2 * slack, rawT = (size_t)s * padT + 2 * slack;
+        if (!acc64N) {
+            acc64N = dnew<long long>((long long)rawN) + slack;
+            acc64T = dnew<long long>((long long)rawT) + slack;
+            d_det_scale = dnew<float>(1);
+            d_det_max = dnew<unsigned>(1);
+        }
+        launch_det_scale(r, n_rays, (int)vv.size(), 2.f, d_det_max, d_det_scale, st);
+        std::vector<float*> dN, dT;
+        for (size_t k = 0; k < slots.size(); ++k) {   // the int64 twin at the same element offsets
+            dN.push_back(reinterpret_cast<float*>(acc64N + (oN[k] - accN)));
+            dT.push_back(reinterpret_cast<float*>(acc64T + (oT[k] - accT)));
+        }
+        project(PROJ_BPD, vv, slots, rc, {}, {}, dN, dT, {}, r, 2.f, 0, st, 0);
+        for (size_t k = 0; k < slots.size(); ++k) {   // whole padded block regions (borders too)
+            const long long bN = (long long)slots[k] * padN, bT = (long long)slots[k] * padT;
+            launch_acc64_to_f32(acc64N + bN, accN + bN, padN, d_det_scale, st);
+            launch_acc64_to_f32(acc64T + bT, accT + bT, padT, d_det_scale, st);
+        }
+        BSGD_CUDA(cudaMemsetAsync(acc64N - slack, 0, sizeof(long long) * rawN, st));
+        BSGD_CUDA(cudaMemsetAsync(acc64T - slack, 0, sizeof(long long) * rawT, st));
     }
 
     void reset(const float* y, cudaStream_t st) {
@@ -1396,8 +1435,10 @@ bsgd_status bsgd_step(bsgd_ctx c, const float* y, float* x_owned, const bsgd_sel
     return guard(c, [&] {
         if (!c || !y || !x_owned || !sel) fail(BSGD_E_CONTRACT, "NULL");
         if (!isfinite(mu)) fail(BSGD_E_CONTRACT, "mu not finite");
-        if (flags & ~(uint32_t)BSGD_SGD) fail(BSGD_E_CONTRACT, "bsgd_step accepts BSGD_SGD only");
+        if (flags & ~(uint32_t)(BSGD_SGD | BSGD_DETERMINISTIC))
+            fail(BSGD_E_CONTRACT, "bsgd_step accepts BSGD_SGD and BSGD_DETERMINISTIC only");
         const bool sgd = flags & BSGD_SGD;
+        c->det = (flags & BSGD_DETERMINISTIC) != 0;
         if (sel->n_rows < 1 || !sel->rows) fail(BSGD_E_CONTRACT, "empty row selection");
         check_sorted_unique(sel->rows, sel->n_rows, c->M, "row block");
         if (!sgd) {
@@ -1445,7 +1486,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
         if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
         const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING |
-                               BSGD_STRATIFIED | BSGD_IS_AREA | BSGD_TV_CHAMBOLLE;
+                               BSGD_STRATIFIED | BSGD_IS_AREA | BSGD_TV_CHAMBOLLE | BSGD_DETERMINISTIC;
         if (P->flags & ~known) fail(BSGD_E_CONTRACT, "unknown flags");
         const bool sgd = P->flags & BSGD_SGD, im = (P->flags & (BSGD_IS | BSGD_IS_UNIFORM)) && !sgd;
         const bool uni = P->flags & BSGD_IS_UNIFORM, tv = P->flags & BSGD_TV, amu = P->flags & BSGD_AUTO_MU;
@@ -1458,6 +1499,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         }
         if (aM < 1 || aM > c->M || gN < 1 || gN > c->N) fail(BSGD_E_CONTRACT, "rows/cols per epoch out of range");
         const bool strat = (P->flags & BSGD_STRATIFIED) && !sgd;
+        c->det = (P->flags & BSGD_DETERMINISTIC) != 0;
         const int strata = P->strata > 0 ? P->strata : c->world;
         if (strat && (P->strata < 0 || c->N % strata || gN % strata))
             fail(BSGD_E_CONTRACT, "BSGD_STRATIFIED: strata must divide N and cols_per_epoch");

@@ -91,9 +91,16 @@ struct ProjLaunch {
     float scale;               // BP scale (2 in Algo 1)
     int accumulate;            // FP: add into z instead of overwriting
     unsigned long long* visits;  // nullable counter
+    const float* det_scale;    // PROJ_BPD: device scalar S (a power of two); the BP targets
+                               // are then int64 fixed-point accumulators (value * S)
 };
 
-enum { PROJ_FP = 0, PROJ_BP = 1, PROJ_COUNT = 2 };
+// PROJ_BPD: the BP with order-independent (deterministic) 64-bit fixed-point reductions
+enum { PROJ_FP = 0, PROJ_BP = 1, PROJ_COUNT = 2, PROJ_BPD = 3 };
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr bool is_bp(int mode) { return mode == PROJ_BP || mode == PROJ_BPD; }
 void launch_project(int mode, const ProjLaunch& L, cudaStream_t st);
 
 // Block update / transpose modes of k_block_update.
@@ -136,6 +143,9 @@ struct ResLaunch {
 };
 constexpr int RES_GX = 64;   // max CTAs per view slot of k_residual
 void launch_residual(const ResLaunch& R, cudaStream_t st);
+// deterministic BP: S (power of two) from max|r| over n rays and V views; out += a / S
+void launch_det_scale(const float* r, long long n, int V, float scale, unsigned* mx, float* S, cudaStream_t st);
+void launch_acc64_to_f32(const long long* a, float* out, long long n, const float* S, cudaStream_t st);
 
 void launch_zero_rows(double* normsq, const int* rows, int n, cudaStream_t st);
 void launch_zero_rects(float* proj, const int* views, const int4* rects, int n, int nu, int nv, cudaStream_t st);

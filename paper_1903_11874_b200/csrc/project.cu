@@ -47,6 +47,19 @@ __device__ __forceinline__ int sgn(double v) { return (v > 0.0) - (v < 0.0); }
 __device__ __forceinline__ void red_add(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+// BP reduction at element `off` of the target: fp32 RED (PROJ_BP) or, PROJ_BPD, a 64-bit
+// integer RED of round(v S) into the int64 accumulator behind the same base (integer
+// addition is associative: the result does not depend on the order of the ray threads)
+template <int MODE>
+__device__ __forceinline__ void red_acc(float* base, int off, float v, float S) {
+    if (MODE == PROJ_BPD) {
+        const long long q = __float2ll_rn(v * S);
+        asm volatile("red.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<unsigned long long*>(base) + off),
+                     "l"((unsigned long long)q) : "memory");
+    } else {
+        red_add(base + off, v);
+    }
+}
 __device__ __forceinline__ bool lane_steep(const double b[3]) {
     // |b_c / b_1| < 1 with a margin (the v3 increments K = |b_c / b_1| 2^64 stay < 2^64)
     const double lim = fabs(b[1]) * (1.0 - 1.0 / 1073741824.0);
@@ -165,7 +178,8 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     // v3 companion mode: only the warps k_project3 leaves (a lane with a steep ray)
     if (STEEP_ONLY && !__any_sync(0xffffffffu, hit && (steep3 || amin == 0.0 || amax == 1.0))) return;
     float rs = 0.f;
-    if (MODE == PROJ_BP) {
+    const float S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
+    if (is_bp(MODE)) {
         if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
         hit = hit && (rs != 0.f);
     }
@@ -251,11 +265,11 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                     const float x2 = p2 ? __ldg(src + o2) : 0.f;
                     acc32 = fmaf(l0, x0, fmaf(l1, x1, fmaf(l2, x2, acc32)));
                 }
-                if (MODE == PROJ_BP) {   // zero-length segments (exact-boundary ties) add 0
-                    red_add(dst + o, l0 * wbp);
+                if (is_bp(MODE)) {       // zero-length segments (exact-boundary ties) add 0
+                    red_acc<MODE>(dst, (int)o, l0 * wbp, S);
                     if (p1) {            // p2 implies p1: one reconvergence region
-                        red_add(dst + o1, l1 * wbp);
-                        if (p2) red_add(dst + o2, l2 * wbp);
+                        red_acc<MODE>(dst, (int)o1, l1 * wbp, S);
+                        if (p2) red_acc<MODE>(dst, (int)o2, l2 * wbp, S);
                     }
                 }
                 if (MODE == PROJ_COUNT)
@@ -273,7 +287,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
                         if (tn > tt) {
                             const float len = (float)(tn - tt);   // t units (see above)
                             if (MODE == PROJ_FP) acc32 = fmaf(len, __ldg(src + o), acc32);
-                            if (MODE == PROJ_BP) red_add(dst + o, len * wbp);
+                            if (is_bp(MODE)) red_acc<MODE>(dst, (int)o, len * wbp, S);
                             if (MODE == PROJ_COUNT && len > cthr) ++nvis;
                             tt = tn;
                         }
@@ -353,13 +367,14 @@ __device__ __forceinline__ void gather3(unsigned rel, unsigned nk, const float* 
 // region per slice instead of three; measured BP 136 -> 121 ms at cfg5):
 // segment 0 iff the lane is in its slice range, segment 1 iff also a plane is crossed
 // (m_or != 0), segment 2 iff both planes are (m_and != 0).
-__device__ __forceinline__ void scatter3(bool in, unsigned m_or, unsigned m_and, float* p0, float* p1,
-                                         float* p2, float v0, float v1, float v2) {
+template <int MODE>
+__device__ __forceinline__ void scatter3(bool in, unsigned m_or, unsigned m_and, float* base, int o0, int o1, int o2,
+                                         float v0, float v1, float v2, float S) {
     if (in) {
-        red_add(p0, v0);
+        red_acc<MODE>(base, o0, v0, S);
         if (m_or) {
-            red_add(p1, v1);
-            if (m_and) red_add(p2, v2);
+            red_acc<MODE>(base, o1, v1, S);
+            if (m_and) red_acc<MODE>(base, o2, v2, S);
         }
     }
 }
@@ -429,7 +444,8 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     if (__any_sync(0xffffffffu, hit && (lane_steep(b) || amin == 0.0 || amax == 1.0))) return;
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     float rs = 0.f;
-    if (MODE == PROJ_BP) {
+    const float S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
+    if (is_bp(MODE)) {
         if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
         hit = hit && (rs != 0.f);
     }
@@ -559,9 +575,8 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
                 pl0 = l0; pl1 = l1; pl2 = l2;
                 pin = in;
             }
-            if (MODE == PROJ_BP)
-                scatter3(in, mor, mand, dst + (int)o, dst + (int)o1, dst + (int)o2, l0 * wbp, l1 * wbp,
-                         l2 * wbp);
+            if (is_bp(MODE))
+                scatter3<MODE>(in, mor, mand, dst, (int)o, (int)o1, (int)o2, l0 * wbp, l1 * wbp, l2 * wbp, S);
             if (MODE == PROJ_COUNT) {
                 const bool p1 = in && mor != 0u, p2 = in && mand != 0u;
                 // a segment counts when longer than 1e-6 of the slice: exact ties (a ray through
@@ -640,6 +655,7 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
     if (version == 2) {   // v2 alone (A/B reference)
         if (mode == PROJ_FP) k_project2<PROJ_FP><<<grid, 256, 0, st>>>(L);
         else if (mode == PROJ_BP) k_project2<PROJ_BP><<<grid, 256, 0, st>>>(L);
+        else if (mode == PROJ_BPD) k_project2<PROJ_BPD><<<grid, 256, 0, st>>>(L);
         else k_project2<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
         BSGD_CUDA(cudaGetLastError());
         note_launch();
@@ -649,11 +665,13 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
     // traversal for the warps v3 skipped (same launch geometry, same predicate)
     if (mode == PROJ_FP) k_project3<PROJ_FP><<<grid, 256, 0, st>>>(L);
     else if (mode == PROJ_BP) k_project3<PROJ_BP><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BPD) k_project3<PROJ_BPD><<<grid, 256, 0, st>>>(L);
     else k_project3<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
     if (mode == PROJ_FP) k_project2<PROJ_FP, true><<<grid, 256, 0, st>>>(L);
     else if (mode == PROJ_BP) k_project2<PROJ_BP, true><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BPD) k_project2<PROJ_BPD, true><<<grid, 256, 0, st>>>(L);
     else k_project2<PROJ_COUNT, true><<<grid, 256, 0, st>>>(L);
     BSGD_CUDA(cudaGetLastError());
     note_launch();

@@ -875,6 +875,50 @@ void launch_sum_ptrs(void* out, const void* const* ptrs, int G, long long n, boo
     note_launch();
 }
 
+// ---- deterministic BP (PROJ_BPD): the fixed-point scale and the int64 -> fp32 conversion
+__global__ void __launch_bounds__(256) k_absmax(const float* r, long long n, unsigned* out) {
+    unsigned m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(fabsf(r[i])));          // non-negative floats order as integers
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);         // max is order-independent
+}
+
+// S = 2^e with e = floor(log2(2^62 / bound)), bound = V * 512 * scale * max|r| >= any per-cell
+// sum of |l w r| (at most ~16 rays per view cross a cell, each with length <= sqrt(3))
+__global__ void k_det_scale(const unsigned* mx, int V, float scale, float* S) {
+    const double rmax = (double)__uint_as_float(*mx);
+    const double bound = (double)V * 512.0 * (double)scale * rmax;
+    int e = 40;
+    if (bound > 0.0 && isfinite(bound)) e = (int)floor(log2(4.611686018427388e18 / bound));
+    e = max(-60, min(120, e));
+    *S = ldexpf(1.f, e);
+}
+
+__global__ void __launch_bounds__(256) k_acc64_to_f32(const long long* a, float* out, long long n, const float* S) {
+    const double inv = 1.0 / (double)*S;                    // exact: S is a power of two
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] += (float)((double)a[i] * inv);
+}
+
+void launch_det_scale(const float* r, long long n, int V, float scale, unsigned* mx, float* S, cudaStream_t st) {
+    BSGD_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+    k_absmax<<<grid_for(n, 8), 256, 0, st>>>(r, n, mx);
+    BSGD_CUDA(cudaGetLastError());
+    k_det_scale<<<1, 1, 0, st>>>(mx, V, scale, S);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+    note_launch();
+}
+
+void launch_acc64_to_f32(const long long* a, float* out, long long n, const float* S, cudaStream_t st) {
+    k_acc64_to_f32<<<grid_for(n, 4), 256, 0, st>>>(a, out, n, S);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
 void launch_tv_fgp(const TvLaunch& T, cudaStream_t st) {
     if (T.dims[0] % 4 == 0) {   // float4 kernel: 4 x 128 tiles, 4 CTAs per SM (76 registers, no spills)
         constexpr int TY = 4;

@@ -202,7 +202,7 @@ def test_visit_counts(bs, name, kw):
         assert abs(got - want) <= 2, (e, got, want)
     # the table itself (bsgd_visit_table) per (block, view) for a few views
     vt = ctx.visit_table()
-    assert vt.shape == (p.N, g.n_views, p.tiles[0] * p.tiles[1])
+    assert vt.shape == (p.N, g.n_views, ctx.info.tiles)
     for v in (0, g.n_views // 3, g.n_views - 1):
         for j in range(p.N):
             want = int(np.count_nonzero(P.csr([v], j).data > 1.2e-6))
@@ -648,3 +648,29 @@ def test_virtual_ranks_trajectory(bs, G):
         assert np.array_equal(out[r][0].sel_cols, res0.sel_cols)
     x = np.concatenate([out[r][1] for r in range(G)])
     print(f"virtual ranks G={G}", _compare(o, res0, x), "mu:", res0.mu[::10])
+
+
+def test_deterministic_bp(bs):
+    """BSGD_DETERMINISTIC (SURVEY §8b Determinism): the BP reduces 64-bit fixed-point values,
+    so two runs from the same state are bit-identical (x, objective), and the trajectory
+    still matches the oracle within the 1e-3 bar (IM on, so the tile BP path is covered)."""
+    p, g, vol32, y = problem("cfg3", K=48, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 0.5 / ob.power_iteration(P, 30, seed=1)
+    o, res, x = _run_pair(bs, p, g, vol32, y, 10, mu, flags=bs.DETERMINISTIC | bs.IS, oracle_kw=dict(im=True),
+                          run_kw=dict(cols_per_epoch=3))
+    print("deterministic", _compare(o, res, x))
+    runs = []
+    for _ in range(2):
+        ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles)
+        yd = torch.from_numpy(y).cuda()
+        xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+        r = ctx.run(yd, xd, epochs=10, mu0=float(np.float32(mu)), seed=3, rows_per_epoch=1, cols_per_epoch=3,
+                    flags=bs.DETERMINISTIC | bs.IS)
+        runs.append((r.obj.copy(), xd.cpu().numpy()))
+        ctx.close()
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+    assert np.array_equal(runs[0][1], x.astype(np.float32))
+    # the per-thread SGD BP path too
+    o, res, x = _run_pair(bs, p, g, vol32, y, 3, mu, flags=bs.DETERMINISTIC | bs.SGD, oracle_kw=dict(sgd=True))
+    print("deterministic SGD", _compare(o, res, x, sgd=True))
