@@ -674,3 +674,57 @@ def test_deterministic_bp(bs):
     # the per-thread SGD BP path too
     o, res, x = _run_pair(bs, p, g, vol32, y, 3, mu, flags=bs.DETERMINISTIC | bs.SGD, oracle_kw=dict(sgd=True))
     print("deterministic SGD", _compare(o, res, x, sgd=True))
+
+
+def test_virtual_ranks_host_buffers_and_tv_prox(bs):
+    """The multi-rank paths bench.py takes at N > 1 besides the device-buffer run: bsgd_run
+    with pinned HOST y / x (the e2e leg: uploads overlapped per block, per-block downloads)
+    and the standalone bsgd_tv_prox with halos, on 2 virtual ranks.  With
+    BSGD_DETERMINISTIC the host-buffer run is bit-identical to the device-buffer run; the
+    sharded prox equals the oracle's prox of the whole volume."""
+    import threading
+    p, g, vol32, y = problem("cfg3", K=48, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
+    G, nb = 2, p.N // 2
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles, rank=r, world=G,
+                                     vgroup=group) for r in range(G)]
+    rng = np.random.default_rng(4)
+    vol = rng.random((g.dims[2], g.dims[1], g.dims[0])).astype(np.float32)
+    vb = P.grid.to_blocks(vol)
+    out, errs = [None] * G, []
+
+    def rank_main(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                kw = dict(epochs=4, mu0=mu, seed=3, rows_per_epoch=1, cols_per_epoch=4, flags=bs.DETERMINISTIC,
+                          stream=s)
+                yd = torch.from_numpy(y).cuda()
+                xd = torch.zeros(nb * P.grid.bsize, device="cuda")
+                ctxs[r].run(yd, xd, **kw)
+                yh = torch.from_numpy(y).pin_memory()
+                xh = torch.zeros(nb * P.grid.bsize).pin_memory()
+                ctxs[r].run(yh, xh, **kw)
+                xt = torch.from_numpy(vb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+                ctxs[r].tv_prox(xt, 0.2, 20, stream=s)
+                s.synchronize()
+                out[r] = (xd.cpu().numpy(), xh.numpy().copy(), xt.cpu().numpy())
+        except Exception as e:          # noqa: BLE001 -- surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in ctxs:
+        c.close()
+    group.close()
+    assert not errs, errs
+    for r in range(G):
+        assert np.array_equal(out[r][0], out[r][1]), r
+    got = P.grid.from_blocks(np.concatenate([out[r][2] for r in range(G)]))
+    want = ob.tv_prox(vol.astype(np.float64), 0.2, 20)
+    assert np.max(np.abs(got - want)) <= 1e-5 * (1.0 + 0.2)
