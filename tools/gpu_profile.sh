@@ -5,19 +5,19 @@
 # table, one per detector tile), warm-up FP, BP, timed FP, BP  ->  skip 6, capture 2.
 set -x
 TAG=${1:-r01}
-KSEL='regex:k_(project|residual|block_update|zero_rows|obj|axpy|dot3)'
+KSEL='regex:k_(project|residual|normsq_final|block_update|zero_rows|obj|axpy|dot3|tv_)'
 mkdir -p gpurun_out
 # every launch of ours with its device time (cold-cache, serialised: compare SHARES only)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k "$KSEL" \
   --log-file gpurun_out/launches_${TAG}.csv \
-  python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/launches_${TAG}.log 2>&1
+  python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-tv --cheap-data > gpurun_out/launches_${TAG}.log 2>&1
 # FP (full set) and BP (sections that replay reliably with the atomics)
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:k_project3 -s 6 -c 1 -o gpurun_out/prof_fp_${TAG} -f \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_fp_${TAG}.log 2>&1
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-tv --cheap-data > gpurun_out/prof_fp_${TAG}.log 2>&1
 timeout 900 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --section ComputeWorkloadAnalysis \
   --section WarpStateStats --section SchedulerStats --section Occupancy --section LaunchStats \
   --metrics lts__t_sectors_op_red.sum,lts__t_requests_op_red.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \
   --clock-control none -k regex:k_project3 -s 7 -c 1 -o gpurun_out/prof_bp_${TAG} -f \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --cheap-data > gpurun_out/prof_bp_${TAG}.log 2>&1
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-tv --cheap-data > gpurun_out/prof_bp_${TAG}.log 2>&1
 ls -la gpurun_out
