@@ -920,11 +920,11 @@ void launch_acc64_to_f32(const long long* a, float* out, long long n, const floa
 }
 
 void launch_tv_fgp(const TvLaunch& T, cudaStream_t st) {
-    if (T.dims[0] % 4 == 0) {   // float4 kernel: 4 x 128 tiles, 4 CTAs per SM (76 registers, no spills)
+    if (T.dims[0] % 4 == 0) {   // float4 kernel: 4 x 128 tiles, 6 CTAs per SM (56 registers, no spills)
         constexpr int TY = 4;
         const dim3 g4((unsigned)((T.dims[0] + TV4_TX - 1) / TV4_TX), (unsigned)((T.dims[1] + TY - 1) / TY),
                       (unsigned)(T.z1 - T.z0));
-        k_tv_fgp4<TY, 4><<<g4, (TY + 2) * 32, 0, st>>>(T);
+        k_tv_fgp4<TY, 6><<<g4, (TY + 2) * 32, 0, st>>>(T);
     } else {
         const dim3 grid((unsigned)((T.dims[0] + TV_TX - 1) / TV_TX), (unsigned)((T.dims[1] + TV_TY - 1) / TV_TY),
                         (unsigned)(T.z1 - T.z0));
