@@ -79,3 +79,59 @@ def test_tv_solver_parity_3d(bs, solver):
     mu = 0.5 / ob.power_iteration(P, 30, seed=1)
     e_obj, e_x, oo = _pair(bs, p, g, y, solver, 6, mu, lam=0.1, tv_iters=20)
     print(solver, "obj rel err", e_obj, "x rel err", e_x)
+
+
+@pytest.mark.parametrize("solver", ["gd_bb", "fista", "svrg"])
+def test_solver_virtual_ranks(bs, solver):
+    """The comparison solvers on 2 virtual ranks (bsgd_vgroup): the partial-FP allreduce of
+    the full gradient, the BB dot products and (FISTA) the sharded TV prox halos, against
+    the oracle on a scaled cfg4 (8 z-slabs, 4 per rank)."""
+    import threading
+    p, g, vol32, y = problem("cfg4", K=32, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
+    iters, lam = {"gd_bb": 8, "fista": 6, "svrg": 4}[solver], (0.1 if solver == "fista" else 0.0)
+    op = so.ProjectorOperator(g, p.blocks, p.M, "random", ROW_SEED)
+    x0 = np.zeros(op.grid.N * op.grid.bsize)
+    y64 = y.astype(np.float64)
+    if solver == "gd_bb":
+        xo, lo = so.gd_bb(op, y64, x0, mu, iters)
+    elif solver == "fista":
+        xo, lo = so.fista(op, y64, x0, mu, lam, iters, 20)
+    else:
+        xo, lo = so.svrg(op, y64, x0, mu, iters, p.M, 1)
+    G, nb = 2, p.N // 2
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=ROW_SEED, tiles=p.tiles, rank=r,
+                                     world=G, vgroup=group) for r in range(G)]
+    out, errs = [None] * G, []
+
+    def rank_main(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                yd = torch.from_numpy(y).cuda()
+                xd = torch.zeros(nb * ctxs[r].block_voxels, device="cuda")
+                obj, mus = ctxs[r].solve(solver, yd, xd, iters, mu, lam=lam, tv_iters=20, svrg_m=0, seed=1,
+                                         stream=s)
+                s.synchronize()
+                out[r] = (obj, mus, xd.cpu().numpy().astype(np.float64))
+        except Exception as e:          # noqa: BLE001 -- surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in ctxs:
+        c.close()
+    group.close()
+    assert not errs, errs
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    oo = np.array([r["obj"] for r in lo])
+    e_obj = float(np.max(np.abs(out[0][0] - oo) / oo))
+    xg = np.concatenate([out[r][2] for r in range(G)])
+    e_x = float(np.max(np.abs(xg - xo)) / np.max(np.abs(xo)))
+    print(solver, "virtual ranks: obj rel err", e_obj, "x rel err", e_x)
+    assert e_obj < 1e-3 and e_x < 1e-2
