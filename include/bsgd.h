@@ -196,6 +196,9 @@ enum {
                                (chord > 1e-6), the "projection area" reading of PAPER.md:162,
                                instead of the default L1 mass (reading A9)                  */
     BSGD_TV_CHAMBOLLE = 512, /* with BSGD_TV: Chambolle-2004 dual iteration instead of FGP  */
+    BSGD_LOG_TRUE_OBJ = 2048, /* bsgd_run: log obj_true[k] = 1/2 ||y - A x_k||^2 (GAP^2 / 2,
+                               PAPER.md:508) from a fresh FP of every view and block after
+                               every epoch (validation only: ~M x an epoch's FP)           */
     BSGD_DETERMINISTIC = 1024 /* bsgd_run / bsgd_step: BP by 64-bit fixed-point reductions
                                (scale 2^e from max|r|, resolution ~1e-15 max|r|): g_hat, g and
                                x do not depend on the order of the BP threads; bit-identical
@@ -238,6 +241,7 @@ typedef struct {
     int32_t* sel_cols;  /* [epochs][cols_per_epoch]                                     */
     uint64_t* visits;   /* [epochs] FP ray-voxel intersections (BP visits are equal)     */
     double* t_ms;       /* [epochs][6] fp, residual(+allreduce), bp, step, tv, total     */
+    double* obj_true;   /* [epochs] 1/2 ||y - A x||^2 after the epoch (BSGD_LOG_TRUE_OBJ)   */
 } bsgd_run_log;
 
 /* Run params->epochs epochs of BSGD (Algo 1) or its variants selected by

@@ -30,6 +30,7 @@ _lib = C.CDLL(LIB_PATH)
 PARALLEL, FAN, CONE = 0, 1, 2
 IS, IS_UNIFORM, TV, AUTO_MU, SGD, RESUME, TIMING, STRATIFIED, IS_AREA, TV_CHAMBOLLE, DETERMINISTIC = \
     1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024
+LOG_TRUE_OBJ = 2048
 STATUS = {0: "OK", 1: "E_GEOMETRY", 2: "E_PARTITION", 3: "E_DIMENSION", 4: "E_CONTRACT", 5: "E_CUDA",
           6: "E_NCCL", 7: "E_OOM", 8: "E_POISONED"}
 
@@ -95,7 +96,8 @@ class RunParams(C.Structure):
 class RunLog(C.Structure):
     _fields_ = [("obj", C.POINTER(C.c_double)), ("rmse", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
                 ("sel_rows", C.POINTER(C.c_int32)), ("sel_cols", C.POINTER(C.c_int32)),
-                ("visits", C.POINTER(C.c_uint64)), ("t_ms", C.POINTER(C.c_double))]
+                ("visits", C.POINTER(C.c_uint64)), ("t_ms", C.POINTER(C.c_double)),
+                ("obj_true", C.POINTER(C.c_double))]
 
 
 class SolveParams(C.Structure):
@@ -286,6 +288,7 @@ class RunResult:
     sel_cols: np.ndarray
     visits: np.ndarray
     t_ms: Optional[np.ndarray]
+    obj_true: Optional[np.ndarray] = None   # 1/2 |y - A x_k|^2 (LOG_TRUE_OBJ)
 
 
 class VirtualGroup:
@@ -427,14 +430,17 @@ class Context:
         sc = np.zeros(E * gN, dtype=np.int32)
         vis = np.zeros(E, dtype=np.uint64)
         tms = np.zeros(E * 6) if flags & TIMING else None
+        otrue = np.zeros(E) if flags & LOG_TRUE_OBJ else None
         log = RunLog(obj.ctypes.data_as(P(C.c_double)), rmse.ctypes.data_as(P(C.c_double)),
                      mu.ctypes.data_as(P(C.c_double)), sr.ctypes.data_as(P(C.c_int32)),
                      sc.ctypes.data_as(P(C.c_int32)), vis.ctypes.data_as(P(C.c_uint64)),
-                     tms.ctypes.data_as(P(C.c_double)) if tms is not None else None)
+                     tms.ctypes.data_as(P(C.c_double)) if tms is not None else None,
+                     otrue.ctypes.data_as(P(C.c_double)) if otrue is not None else None)
         self._c(_lib.bsgd_run(self.h, _ptr(y), _ptr(x), _ptr(x_true), C.byref(prm), C.byref(log), _stream(stream)))
         return RunResult(obj[:epochs], rmse[:epochs], mu[:epochs], sr.reshape(E, aM)[:epochs],
                          sc.reshape(E, gN)[:epochs], vis[:epochs],
-                         tms.reshape(E, 6)[:epochs] if tms is not None else None)
+                         tms.reshape(E, 6)[:epochs] if tms is not None else None,
+                         otrue[:epochs] if otrue is not None else None)
 
     def solve(self, solver, y, x, iters, mu0, lam=0.0, tv_iters=20, svrg_m=0, seed=1, stream=None):
         """Comparison solver `solver` in {"gd", "gd_bb", "ista", "fista", "svrg"} (bsgd_solve;

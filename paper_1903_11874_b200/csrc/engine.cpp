@@ -88,6 +88,9 @@ struct bsgd_ctx_s {
     bsgd_vgroup vg = nullptr;   // virtual rank: collectives through the in-process group
     void* vg_tmp = nullptr;
     double* d_rpart = nullptr;   // k_residual per-CTA partials of ||r||^2
+    float* gap_proj = nullptr;   // BSGD_LOG_TRUE_OBJ: A x (full length)
+    double* d_gap = nullptr;     // ... and 1/2-less |y - A x|^2 per epoch
+    int d_gap_n = 0;
     // deterministic BP (BSGD_DETERMINISTIC): int64 fixed-point twins of accN / accT
     bool det = false;
     long long* acc64N = nullptr;
@@ -1486,7 +1489,8 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
         if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
         const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING |
-                               BSGD_STRATIFIED | BSGD_IS_AREA | BSGD_TV_CHAMBOLLE | BSGD_DETERMINISTIC;
+                               BSGD_STRATIFIED | BSGD_IS_AREA | BSGD_TV_CHAMBOLLE | BSGD_DETERMINISTIC |
+                               BSGD_LOG_TRUE_OBJ;
         if (P->flags & ~known) fail(BSGD_E_CONTRACT, "unknown flags");
         const bool sgd = P->flags & BSGD_SGD, im = (P->flags & (BSGD_IS | BSGD_IS_UNIFORM)) && !sgd;
         const bool uni = P->flags & BSGD_IS_UNIFORM, tv = P->flags & BSGD_TV, amu = P->flags & BSGD_AUTO_MU;
@@ -1593,6 +1597,16 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         BSGD_CUDA(cudaMemsetAsync(c->d_log, 0, sizeof(double) * (2 * E + 2), st));
         std::vector<cudaEvent_t> ev;
         const bool timing = (P->flags & BSGD_TIMING) && log && log->t_ms;
+        const bool true_obj = (P->flags & BSGD_LOG_TRUE_OBJ) && log && log->obj_true;
+        std::vector<int> all_views;
+        if (true_obj) {
+            for (int v = 0; v < c->n_views; ++v) all_views.push_back(v);
+            if (!c->gap_proj) c->gap_proj = c->dnew<float>(c->n_rays, false);
+            if (c->d_gap_n < E) {
+                c->d_gap = c->dnew<double>(E);
+                c->d_gap_n = E;
+            }
+        }
         if (timing) {
             ev.resize((size_t)E * 7);
             for (auto& e : ev) BSGD_CUDA(cudaEventCreate(&e));
@@ -1670,6 +1684,15 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 c->refresh_xT(x, all_slots, st);
             }
             if (evp) BSGD_CUDA(cudaEventRecord(evp[5], st));
+            if (true_obj) {   // GAP^2 / 2 = 1/2 |y - A x|^2: FP of every view through every owned block
+                BSGD_CUDA(cudaMemsetAsync(c->gap_proj, 0, sizeof(float) * c->n_rays, st));
+                for (int b = 0; b < c->s; ++b)
+                    c->project(PROJ_FP, all_views, {b}, {}, {c->pN(c->xN, b)}, {c->pT(c->xT, b)}, {}, {},
+                               {c->gap_proj}, nullptr, 0.f, 1, st, 0);
+                c->allreduce_f(c->gap_proj, (size_t)c->n_rays, st);
+                BSGD_CUDA(cudaMemsetAsync(c->d_gap + e, 0, sizeof(double), st));
+                launch_sqdiff(y, c->gap_proj, c->n_rays, c->d_gap + e, st);
+            }
             if (xt) {
                 BSGD_CUDA(cudaMemsetAsync(c->d_red + 8, 0, sizeof(double), st));
                 launch_sqdiff(x, xt, sb, c->d_red + 8, st);
@@ -1723,14 +1746,16 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         } else if (x_host) {
             BSGD_CUDA(cudaMemcpyAsync(x_in, x, sizeof(float) * sb, cudaMemcpyDeviceToHost, st));
         }
-        std::vector<double> hl(2 * (size_t)E + 2);
+        std::vector<double> hl(2 * (size_t)E + 2), hgap(true_obj ? E : 0);
         BSGD_CUDA(cudaMemcpyAsync(hl.data(), c->d_log, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, st));
+        if (true_obj) BSGD_CUDA(cudaMemcpyAsync(hgap.data(), c->d_gap, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
         BSGD_CUDA(cudaStreamSynchronize(st));
         if (log) {
             const double nvox = (double)c->bsize * c->N;
             for (int e = 0; e < E; ++e) {
                 if (log->obj) log->obj[e] = hl[2 * e];
                 if (log->rmse) log->rmse[e] = xt ? sqrt(hl[2 * e + 1] / nvox) : NAN;
+                if (true_obj) log->obj_true[e] = 0.5 * hgap[e];
                 if (log->mu) log->mu[e] = mu_log[e];
                 if (log->visits) log->visits[e] = vis_log[e];
                 if (timing) {

@@ -728,3 +728,28 @@ def test_virtual_ranks_host_buffers_and_tv_prox(bs):
     got = P.grid.from_blocks(np.concatenate([out[r][2] for r in range(G)]))
     want = ob.tv_prox(vol.astype(np.float64), 0.2, 20)
     assert np.max(np.abs(got - want)) <= 1e-5 * (1.0 + 0.2)
+
+
+def test_log_true_objective(bs):
+    """BSGD_LOG_TRUE_OBJ: 1/2 |y - A x_k|^2 after every epoch (GAP of PAPER.md:508) against the
+    oracle's fresh full FP of the same trajectory; it differs from the maintained objective
+    (which uses the stale z of unselected blocks)."""
+    p, g, vol32, y = problem("cfg3", K=48, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
+    prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=3, total_epochs=6)
+    o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11, tiles=p.tiles)
+    want = []
+    for _ in range(6):
+        o.epoch()
+        want.append(o.true_objective())
+    ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles)
+    yd = torch.from_numpy(y).cuda()
+    xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    res = ctx.run(yd, xd, epochs=6, mu0=mu, seed=3, rows_per_epoch=1, cols_per_epoch=3, flags=bs.LOG_TRUE_OBJ)
+    ctx.close()
+    want = np.array(want)
+    err = np.max(np.abs(res.obj_true - want) / want)
+    print("true objective rel err", err, "maintained/true", res.obj / res.obj_true)
+    assert err < 1e-4
+    assert np.all(np.abs(res.obj - res.obj_true) > 1e-6 * want)     # stale z: the two differ
