@@ -340,8 +340,11 @@ def run_ours(args, rank, world, local_rank):
                         "overlapped with the first epoch), K epochs, x copied back")}
         del yh, xh
     tv = None
-    if not args.no_tv:
-        tv = time_tv(bs, ctx, x, mu0 * lam, p, aM, gN, world, stream, t_ms / args.steps, peak)
+    if not args.no_tv:   # an auxiliary measurement: never lose the main line over it
+        try:
+            tv = time_tv(bs, ctx, x, mu0 * lam, p, aM, gN, world, stream, t_ms / args.steps, peak)
+        except Exception as exc:   # noqa: BLE001
+            tv = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     ctx.close()
     if rank != 0:
         return 0
