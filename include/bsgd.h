@@ -242,6 +242,7 @@ typedef struct {
     uint64_t* visits;   /* [epochs] FP ray-voxel intersections (BP visits are equal)     */
     double* t_ms;       /* [epochs][6] fp, residual(+allreduce), bp, step, tv, total     */
     double* obj_true;   /* [epochs] 1/2 ||y - A x||^2 after the epoch (BSGD_LOG_TRUE_OBJ)   */
+    double* tv;         /* [epochs] TV(x) after the epoch (Eq. 6; with BSGD_LOG_TRUE_OBJ)     */
 } bsgd_run_log;
 
 /* Run params->epochs epochs of BSGD (Algo 1) or its variants selected by
@@ -279,6 +280,10 @@ bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, dou
  * Errors: BSGD_E_CONTRACT for NULL x, w < 0, iters < 0 or an unknown method.             */
 bsgd_status bsgd_tv_prox(bsgd_ctx ctx, float* x_owned, double w, int32_t iters, int32_t method,
                          void* stream);
+/* TV(x) = sum over voxels of |grad x|_2 (isotropic backward differences, zero at index 0;
+ * Eq. 6) of the whole volume: x_owned device (owned blocks, block-major),
+ * *out host.  Collective when world > 1 (one halo plane + a 1-double allreduce).  Synchronous. */
+bsgd_status bsgd_tv_value(bsgd_ctx ctx, const float* x_owned, double* out, void* stream);
 
 /* Comparison solvers on the same operators (the methods the paper
  * compares against in Figs. 12 and 18, cited but not listed

@@ -97,7 +97,7 @@ class RunLog(C.Structure):
     _fields_ = [("obj", C.POINTER(C.c_double)), ("rmse", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
                 ("sel_rows", C.POINTER(C.c_int32)), ("sel_cols", C.POINTER(C.c_int32)),
                 ("visits", C.POINTER(C.c_uint64)), ("t_ms", C.POINTER(C.c_double)),
-                ("obj_true", C.POINTER(C.c_double))]
+                ("obj_true", C.POINTER(C.c_double)), ("tv", C.POINTER(C.c_double))]
 
 
 class SolveParams(C.Structure):
@@ -141,6 +141,7 @@ SIGS = {
     "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
+    "bsgd_tv_value": ([_ctx, C.c_void_p, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
                    C.c_int),
 }
@@ -289,6 +290,7 @@ class RunResult:
     visits: np.ndarray
     t_ms: Optional[np.ndarray]
     obj_true: Optional[np.ndarray] = None   # 1/2 |y - A x_k|^2 (LOG_TRUE_OBJ)
+    tv: Optional[np.ndarray] = None         # TV(x_k) (LOG_TRUE_OBJ)
 
 
 class VirtualGroup:
@@ -431,16 +433,19 @@ class Context:
         vis = np.zeros(E, dtype=np.uint64)
         tms = np.zeros(E * 6) if flags & TIMING else None
         otrue = np.zeros(E) if flags & LOG_TRUE_OBJ else None
+        otv = np.zeros(E) if flags & LOG_TRUE_OBJ else None
         log = RunLog(obj.ctypes.data_as(P(C.c_double)), rmse.ctypes.data_as(P(C.c_double)),
                      mu.ctypes.data_as(P(C.c_double)), sr.ctypes.data_as(P(C.c_int32)),
                      sc.ctypes.data_as(P(C.c_int32)), vis.ctypes.data_as(P(C.c_uint64)),
                      tms.ctypes.data_as(P(C.c_double)) if tms is not None else None,
-                     otrue.ctypes.data_as(P(C.c_double)) if otrue is not None else None)
+                     otrue.ctypes.data_as(P(C.c_double)) if otrue is not None else None,
+                     otv.ctypes.data_as(P(C.c_double)) if otv is not None else None)
         self._c(_lib.bsgd_run(self.h, _ptr(y), _ptr(x), _ptr(x_true), C.byref(prm), C.byref(log), _stream(stream)))
         return RunResult(obj[:epochs], rmse[:epochs], mu[:epochs], sr.reshape(E, aM)[:epochs],
                          sc.reshape(E, gN)[:epochs], vis[:epochs],
                          tms.reshape(E, 6)[:epochs] if tms is not None else None,
-                         otrue[:epochs] if otrue is not None else None)
+                         otrue[:epochs] if otrue is not None else None,
+                         otv[:epochs] if otv is not None else None)
 
     def solve(self, solver, y, x, iters, mu0, lam=0.0, tv_iters=20, svrg_m=0, seed=1, stream=None):
         """Comparison solver `solver` in {"gd", "gd_bb", "ista", "fista", "svrg"} (bsgd_solve;
@@ -471,6 +476,12 @@ class Context:
         m = {"fgp": 0, "chambolle": 1}[method]
         self._c(_lib.bsgd_tv_prox(self.h, _ptr(x), float(w), int(iters), m, _stream(stream)))
         return x
+
+    def tv_value(self, x, stream=None) -> float:
+        """TV(x) of the whole volume (bsgd_tv_value; Eq. 6)."""
+        out = C.c_double()
+        self._c(_lib.bsgd_tv_value(self.h, _ptr(x), C.byref(out), _stream(stream)))
+        return out.value
 
     def power_iteration(self, iters=30, seed=0, stream=None) -> float:
         out = C.c_double()

@@ -89,6 +89,9 @@ struct bsgd_ctx_s {
     void* vg_tmp = nullptr;
     double* d_rpart = nullptr;   // k_residual per-CTA partials of ||r||^2
     float* gap_proj = nullptr;   // BSGD_LOG_TRUE_OBJ: A x (full length)
+    float* tvv_halo = nullptr;   // tv_value: x plane z0-1 from the previous rank
+    double* d_tvv = nullptr;     // per-epoch TV(x) (BSGD_LOG_TRUE_OBJ with log->tv)
+    double* d_tvv1 = nullptr;    // bsgd_tv_value
     double* d_gap = nullptr;     // ... and 1/2-less |y - A x|^2 per epoch
     int d_gap_n = 0;
     // deterministic BP (BSGD_DETERMINISTIC): int64 fixed-point twins of accN / accT
@@ -991,6 +994,29 @@ struct bsgd_ctx_s {
         launch_tv_u(Tl, pf, x_owned, st);
     }
 
+    // TV(x) (Eq. 6) of the whole volume into *d_out (device; summed over ranks)
+    void tv_value(const float* x_owned, double* d_out, cudaStream_t st) {
+        const long long n = (long long)s * bsize, plane = (long long)dims[0] * dims[1];
+        if (world > 1 && (bgrid[0] != 1 || bgrid[1] != 1))
+            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        if (!tvv_halo) tvv_halo = dnew<float>(plane);
+        TvLaunch Tl{};
+        for (int c = 0; c < 3; ++c) {
+            Tl.dims[c] = dims[c];
+            Tl.bdims[c] = bd[c];
+            Tl.bgrid[c] = bgrid[c];
+        }
+        Tl.block0 = first;
+        Tl.n = n;
+        Tl.z0 = first * bd[2];
+        Tl.z1 = (first + s) * bd[2];
+        Tl.halo_u_prev = tvv_halo;
+        halo_exchange(x_owned + n - plane, tvv_halo, plane, false, st);   // x of plane z0-1
+        BSGD_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), st));
+        launch_tv_value(Tl, x_owned, d_out, st);
+        allreduce_d(d_out, 1, st);
+    }
+
     // z-slab halo: `down` = send my first plane (src) to rank-1 and receive rank+1's first
     // plane into dst; otherwise send my last plane (src) to rank+1, receive from rank-1.
     void halo_exchange(const float* src, float* dst, long long plane, bool down, cudaStream_t st) {
@@ -1604,6 +1630,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             if (!c->gap_proj) c->gap_proj = c->dnew<float>(c->n_rays, false);
             if (c->d_gap_n < E) {
                 c->d_gap = c->dnew<double>(E);
+                c->d_tvv = c->dnew<double>(E);
                 c->d_gap_n = E;
             }
         }
@@ -1692,6 +1719,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 c->allreduce_f(c->gap_proj, (size_t)c->n_rays, st);
                 BSGD_CUDA(cudaMemsetAsync(c->d_gap + e, 0, sizeof(double), st));
                 launch_sqdiff(y, c->gap_proj, c->n_rays, c->d_gap + e, st);
+                if (log->tv) c->tv_value(x, c->d_tvv + e, st);
             }
             if (xt) {
                 BSGD_CUDA(cudaMemsetAsync(c->d_red + 8, 0, sizeof(double), st));
@@ -1748,7 +1776,9 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         }
         std::vector<double> hl(2 * (size_t)E + 2), hgap(true_obj ? E : 0);
         BSGD_CUDA(cudaMemcpyAsync(hl.data(), c->d_log, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, st));
+        std::vector<double> htv(true_obj && log->tv ? E : 0);
         if (true_obj) BSGD_CUDA(cudaMemcpyAsync(hgap.data(), c->d_gap, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
+        if (!htv.empty()) BSGD_CUDA(cudaMemcpyAsync(htv.data(), c->d_tvv, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
         BSGD_CUDA(cudaStreamSynchronize(st));
         if (log) {
             const double nvox = (double)c->bsize * c->N;
@@ -1756,6 +1786,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 if (log->obj) log->obj[e] = hl[2 * e];
                 if (log->rmse) log->rmse[e] = xt ? sqrt(hl[2 * e + 1] / nvox) : NAN;
                 if (true_obj) log->obj_true[e] = 0.5 * hgap[e];
+                if (!htv.empty()) log->tv[e] = htv[e];
                 if (log->mu) log->mu[e] = mu_log[e];
                 if (log->visits) log->visits[e] = vis_log[e];
                 if (timing) {
@@ -1846,6 +1877,17 @@ bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, in
         if (!c || !x_owned || !(w >= 0.0) || iters < 0 || method < 0 || method > 1)
             fail(BSGD_E_CONTRACT, "bad arguments");
         c->tv_prox(x_owned, w, iters, S(stream), method);
+    });
+}
+
+bsgd_status bsgd_tv_value(bsgd_ctx c, const float* x_owned, double* out, void* stream) {
+    return guard(c, [&] {
+        if (!c || !x_owned || !out) fail(BSGD_E_CONTRACT, "bad arguments");
+        cudaStream_t st = S(stream);
+        if (!c->d_tvv1) c->d_tvv1 = c->dnew<double>(1);
+        c->tv_value(x_owned, c->d_tvv1, st);
+        BSGD_CUDA(cudaMemcpyAsync(out, c->d_tvv1, sizeof(double), cudaMemcpyDeviceToHost, st));
+        BSGD_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -195,6 +195,8 @@ struct TvLaunch {
 };
 void launch_tv_u(const TvLaunch& T, const float* src_q, float* dst, cudaStream_t st);
 void launch_tv_pq(const TvLaunch& T, cudaStream_t st);
+// *out += TV(x) over the owned voxels (T: dims, bdims, bgrid, block0, n, halo_u_prev = x of plane z0-1)
+void launch_tv_value(const TvLaunch& T, const float* x, double* out, cudaStream_t st);
 // out[i] = sum_{g = 0..G-1} ptrs[g][i] in ascending g (virtual-rank allreduce), G <= 8
 void launch_sum_ptrs(void* out, const void* const* ptrs, int G, long long n, bool dbl, cudaStream_t st);
 // One fused FGP iteration (u, projection, momentum) for z-slab layouts (bgrid = 1 x 1 x N):

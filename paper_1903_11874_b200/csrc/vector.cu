@@ -435,6 +435,30 @@ __global__ void __launch_bounds__(256) k_tv_u(const TvLaunch T, const float* src
     }
 }
 
+// TV(x) = sum_i |(grad x)_i|_2 (isotropic, backward differences, zero at index 0; Eq. 6)
+// over the owned voxels; x of plane z0-1 comes from T.halo_u_prev when sharded
+__global__ void __launch_bounds__(256) k_tv_value(const TvLaunch T, const float* x, double* out) {
+    double acc = 0.0;
+    for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < T.n;
+         o += (long long)gridDim.x * blockDim.x) {
+        const Vox v = owned_coords(T, o);
+        const int c[3] = {v.x, v.y, v.z};
+        const double xo = x[o];
+        double s2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (c[a] < 1) continue;
+            const int nx = v.x - (a == 0), ny = v.y - (a == 1), nz = v.z - (a == 2);
+            const long long on = owned_index(T, nx, ny, nz);
+            const double xn = on >= 0 ? (double)x[on] : (double)T.halo_u_prev[(long long)ny * T.dims[0] + nx];
+            s2 += (xo - xn) * (xo - xn);
+        }
+        acc += sqrt(s2);
+    }
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) atomicAdd(out, acc);
+}
+
 // p_new = P(q + grad(u)/(L w)); q = p_new + beta (p_new - p); p = p_new
 __global__ void __launch_bounds__(256) k_tv_pq(const TvLaunch T) {
     const double s = 1.0 / (T.L * T.w);
@@ -856,6 +880,12 @@ void launch_fill_random(float* v, long long n, uint64_t seed, cudaStream_t st) {
 
 void launch_scale(float* v, long long n, const double* nrm, cudaStream_t st) {
     k_scale<<<grid_for(n, 4), 256, 0, st>>>(v, n, nrm);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_value(const TvLaunch& T, const float* x, double* out, cudaStream_t st) {
+    k_tv_value<<<grid_for(T.n, 4), 256, 0, st>>>(T, x, out);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

@@ -583,6 +583,9 @@ def test_tv_prox_parity(bs, dims, blocks, w, iters, method):
     print(f"tv_prox {method} {dims} {blocks}: max|d| {err:.3g} (bar {bar:.3g}), max|x - b| {np.abs(want - vol).max():.3g}")
     assert err <= bar
     assert np.abs(want - vol).max() > 10 * bar          # the prox moved x: the check is not vacuous
+    tv_got = ctx.tv_value(torch.from_numpy(bx.to_blocks(vol).ravel().copy()).cuda())
+    tv_want = ob.tv_value(vol.astype(np.float64))       # TV of Eq. 6 (bsgd_tv_value)
+    assert abs(tv_got - tv_want) <= 1e-9 * tv_want, (tv_got, tv_want)
     # w = 0 and iters = 0 are the identity
     x0 = torch.from_numpy(bx.to_blocks(vol).ravel().copy()).cuda()
     ctx.tv_prox(x0, 0.0, iters)
@@ -739,10 +742,11 @@ def test_log_true_objective(bs):
     mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
     prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=3, total_epochs=6)
     o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11, tiles=p.tiles)
-    want = []
+    want, tvw = [], []
     for _ in range(6):
         o.epoch()
         want.append(o.true_objective())
+        tvw.append(ob.tv_value(o.grid.from_blocks(o.x)))
     ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles)
     yd = torch.from_numpy(y).cuda()
     xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
@@ -753,3 +757,5 @@ def test_log_true_objective(bs):
     print("true objective rel err", err, "maintained/true", res.obj / res.obj_true)
     assert err < 1e-4
     assert np.all(np.abs(res.obj - res.obj_true) > 1e-6 * want)     # stale z: the two differ
+    tvw = np.array(tvw)
+    assert np.max(np.abs(res.tv - tvw) / tvw) < 1e-4, (res.tv, tvw)  # TV(x_k) log
