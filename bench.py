@@ -366,7 +366,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"z-slab{world}" if p.blocks[:2] == (1, 1) else f"blocks{world}",
                    "l2": ("inputs larger than L2 (537 MB slabs, 3.0 GB y); no flush needed" if p.name == "cfg5"
                           else "auxiliary workload: inputs may be L2-resident, no flush (not the headline)"),
-                   "visits_per_epoch_fp": vis_ep * world if world == 1 else None,
+                   "visits_per_epoch_fp": visits_all / 2.0 / args.steps,   # all ranks
                    "fp64": "ray parameters fp64, values fp32"},
         "phase_ms": {"fp": fp_ms, "residual_allreduce": res_ms, "bp": bp_ms, "step": st_ms},
         "allreduce": None if world == 1 else {
