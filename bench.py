@@ -398,8 +398,8 @@ def time_tv(bs, ctx, x, w, p, aM, gN, world, stream, epoch_ms, peak, iters=20, c
     """The TV proximal call of Algo 4 line 16 on this rank's owned volume,
     timed on its own (CUDA events on the launch stream, max over ranks): 20 FGP iterations.
     Algorithmic HBM bytes per call: per iteration read q (3), p (3), b and write q, p
-    (13 floats = 52 B per voxel), plus the set-up (copy x -> b, zero p and q: 32 B) and the
-    final x = b - w grad^T p (read b, 3 p, write x: 20 B)."""
+    (13 floats = 52 B per voxel; the first iteration reads neither q nor p: -24 B), plus the
+    final x = b - w grad^T p in place (read b, 3 p, write x: 20 B); no set-up pass."""
     import torch
     import torch.distributed as dist
     xt = x.clone()
@@ -420,13 +420,14 @@ def time_tv(bs, ctx, x, w, p, aM, gN, world, stream, epoch_ms, peak, iters=20, c
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     n = x.numel()
-    nbytes = n * (52.0 * iters + 32.0 + 20.0)
+    nbytes = n * (52.0 * iters - 24.0 + 20.0)
     period = max(1, round(p.M * p.N / (aM * gN)))
     del xt
     return {"ms_per_call": ms, "iters": iters, "w": w, "voxels_per_rank": n, "launches_per_call": int(launches),
             "kernel": "k_tv_fgp4 (fused FGP iteration, float4) x iters + k_tv_out" if p.blocks[:2] == (1, 1)
             else "k_tv_u + k_tv_pq per iteration + k_tv_u",
-            "algorithmic_bytes": f"{nbytes:.4g} B per call (52 B per voxel per FGP iteration + 52 B set-up/final)",
+            "algorithmic_bytes": f"{nbytes:.4g} B per call (52 B per voxel per FGP iteration, 28 B in the first, "
+                                 f"+ 20 B final)",
             "achieved_gbs": nbytes / (ms / 1e3) / 1e9, "frac": nbytes / (ms / 1e3) / 1e9 / peak,
             "period_epochs": period,
             "epochs_per_s_tv_amortised": 1e3 / (epoch_ms + ms / period)}

@@ -116,7 +116,7 @@ struct bsgd_ctx_s {
     float *accN = nullptr, *accT = nullptr, *pc = nullptr;
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
-          *tv_b = nullptr, *tv_q2 = nullptr, *tv_hp = nullptr;
+          *tv_q2 = nullptr, *tv_hp = nullptr;
     float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
@@ -916,7 +916,6 @@ struct bsgd_ctx_s {
         if (!tv_p) {
             tv_p = dnew<float>(3 * n, false);
             tv_q = dnew<float>(3 * n, false);
-            tv_b = dnew<float>(n, false);
             tv_hq = dnew<float>(plane);
             if (fused) {
                 tv_q2 = dnew<float>(3 * n, false);
@@ -927,17 +926,21 @@ struct bsgd_ctx_s {
             }
         }
         if (wgt == 0.0 || iters <= 0) return;
-        BSGD_CUDA(cudaMemcpyAsync(tv_b, x_owned, sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
-        BSGD_CUDA(cudaMemsetAsync(tv_p, 0, sizeof(float) * 3 * n, st));
-        BSGD_CUDA(cudaMemsetAsync(tv_q, 0, sizeof(float) * 3 * n, st));
-        TvLaunch Tl;
+        // b = x itself: read-only during the iterations, and the final x = b - w grad^T p reads
+        // b only at the voxel it writes.  The fused path's first iteration treats q = p = 0
+        // without reading them, so the dual fields need no clearing there.
+        if (!fused) {
+            BSGD_CUDA(cudaMemsetAsync(tv_p, 0, sizeof(float) * 3 * n, st));
+            BSGD_CUDA(cudaMemsetAsync(tv_q, 0, sizeof(float) * 3 * n, st));
+        }
+        TvLaunch Tl{};
         for (int c = 0; c < 3; ++c) {
             Tl.dims[c] = dims[c];
             Tl.bdims[c] = bd[c];
             Tl.bgrid[c] = bgrid[c];
         }
         Tl.block0 = first;
-        Tl.b = tv_b;
+        Tl.b = x_owned;
         Tl.u = tv_u;
         Tl.p = tv_p;
         Tl.q = tv_q;
@@ -954,7 +957,7 @@ struct bsgd_ctx_s {
         double sk = 1.0;
         if (fused) {
             Tl.halo_prev = tv_hp;
-            halo_exchange(tv_b + n - plane, tv_hp + 3 * plane, plane, false, st);   // b of plane z0-1
+            halo_exchange(x_owned + n - plane, tv_hp + 3 * plane, plane, false, st);   // b of plane z0-1
             float *qa = tv_q, *qb = tv_q2;
             for (int it = 0; it < iters; ++it) {
                 const double sk1 = (1.0 + sqrt(1.0 + 4.0 * sk * sk)) / 2.0;
@@ -964,6 +967,7 @@ struct bsgd_ctx_s {
                 halo_exchange(qa + 2 * n, tv_hq, plane, true, st);   // q_z of plane z1 from the next
                 Tl.q = qa;
                 Tl.q_out = qb;
+                Tl.first = it == 0;
                 Tl.wf = (float)wgt;
                 Tl.sf = (float)(1.0 / (Tl.L * wgt));
                 Tl.betaf = (float)Tl.beta;
@@ -971,6 +975,7 @@ struct bsgd_ctx_s {
                 std::swap(qa, qb);
                 sk = sk1;
             }
+            Tl.first = 0;
             float* pf = method == 1 ? qa : tv_p;          // the final dual field
             halo_exchange(pf + 2 * n, tv_hq, plane, true, st);
             Tl.q = pf;

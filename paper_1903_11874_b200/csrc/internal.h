@@ -188,6 +188,7 @@ struct TvLaunch {
     const float* halo_prev;    // fused FGP: qx, qy, qz, b of plane z0-1 (4 planes) or NULL
     float wf, sf, betaf;       // fused FGP in fp32: w, 1/(L w), beta
     int chambolle;             // 1: Chambolle-2004 step p <- (p + s g)/(1 + s|g|) on q (p unused)
+    int first;                 // fused path, first iteration: q = p = 0 (not read; no memsets)
     double w;           // weight mu*lambda
     double L;           // Lipschitz bound 4*(#axes > 1)
     double beta;        // FISTA momentum (s_k - 1)/s_{k+1}

@@ -545,6 +545,7 @@ __device__ __forceinline__ TvPlane tv_plane(const TvLaunch& T, int z) {
 // dual fields are stored in fp32 anyway; the oracle parity margin is ~100x)
 __device__ __forceinline__ float tv_u_at(const TvLaunch& T, const TvPlane& P, int x, int y, int z, float w) {
     const int i = y * T.dims[0] + x;
+    if (T.first) return P.b[i];
     float t = 0.f;
     if (x >= 1) t += P.qx[i];
     if (x + 1 < T.dims[0]) t -= P.qx[i + 1];
@@ -585,7 +586,9 @@ __global__ void __launch_bounds__(TV_THREADS, ZT == 1 ? 3 : (ZT == 2 ? 2 : 1)) k
         u[k + 1] = 0.f;
         if (inside && pin) u[k + 1] = tv_u_at(T, tv_plane(T, zb + k), x, y, zb + k, w);
         const long long i = i0 + k * plane;
-        if (out && pin) {
+        if (out && pin && T.first) {
+            qx[k] = qy[k] = qz[k] = ox[k] = oy[k] = oz[k] = 0.f;
+        } else if (out && pin) {
             qx[k] = T.q[i];
             qy[k] = T.q[T.n + i];
             qz[k] = T.q[2 * T.n + i];
@@ -649,6 +652,13 @@ __device__ __forceinline__ void tv_u4(const TvLaunch& T, const TvPlane& P, int x
     const int i = y * nx + x;
     float4 qx = make_float4(0.f, 0.f, 0.f, 0.f), qy = qx, qyn = qx, qz = qx, qz1 = qx, b = qx;
     float qxe = 0.f;
+    if (T.first) {                 // q = 0: u = b
+        if (act) {
+            b = ld4(P.b + i);
+            u[0] = b.x; u[1] = b.y; u[2] = b.z; u[3] = b.w;
+        }
+        return;
+    }
     if (act) {
         qx = ld4(P.qx + i);
         qy = ld4(P.qy + i);
@@ -700,7 +710,7 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, p0 = q0, p1 = q0, p2 = q0;
     if (row >= 1) {
         if (z >= 1) tv_u4(T, tv_plane(T, z - 1), x, y, z - 1, out, w, uz);
-        if (out) {
+        if (out && !T.first) {
             q0 = ld4(T.q + i);
             q1 = ld4(T.q + T.n + i);
             q2 = ld4(T.q + 2 * T.n + i);
