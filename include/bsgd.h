@@ -243,6 +243,8 @@ typedef struct {
     double* t_ms;       /* [epochs][6] fp, residual(+allreduce), bp, step, tv, total     */
     double* obj_true;   /* [epochs] 1/2 ||y - A x||^2 after the epoch (BSGD_LOG_TRUE_OBJ)   */
     double* tv;         /* [epochs] TV(x) after the epoch (Eq. 6; with BSGD_LOG_TRUE_OBJ)     */
+    double* rmse_seen;  /* [epochs] RMSE(x, x_true) over the voxels some ray crosses (A^T 1 > 0;
+                           reading A32), with BSGD_LOG_TRUE_OBJ and x_true                   */
 } bsgd_run_log;
 
 /* Run params->epochs epochs of BSGD (Algo 1) or its variants selected by

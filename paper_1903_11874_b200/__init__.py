@@ -97,7 +97,8 @@ class RunLog(C.Structure):
     _fields_ = [("obj", C.POINTER(C.c_double)), ("rmse", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
                 ("sel_rows", C.POINTER(C.c_int32)), ("sel_cols", C.POINTER(C.c_int32)),
                 ("visits", C.POINTER(C.c_uint64)), ("t_ms", C.POINTER(C.c_double)),
-                ("obj_true", C.POINTER(C.c_double)), ("tv", C.POINTER(C.c_double))]
+                ("obj_true", C.POINTER(C.c_double)), ("tv", C.POINTER(C.c_double)),
+                ("rmse_seen", C.POINTER(C.c_double))]
 
 
 class SolveParams(C.Structure):
@@ -291,6 +292,7 @@ class RunResult:
     t_ms: Optional[np.ndarray]
     obj_true: Optional[np.ndarray] = None   # 1/2 |y - A x_k|^2 (LOG_TRUE_OBJ)
     tv: Optional[np.ndarray] = None         # TV(x_k) (LOG_TRUE_OBJ)
+    rmse_seen: Optional[np.ndarray] = None  # RMSE over the voxels rays cross (LOG_TRUE_OBJ + x_true)
 
 
 class VirtualGroup:
@@ -434,18 +436,21 @@ class Context:
         tms = np.zeros(E * 6) if flags & TIMING else None
         otrue = np.zeros(E) if flags & LOG_TRUE_OBJ else None
         otv = np.zeros(E) if flags & LOG_TRUE_OBJ else None
+        oseen = np.zeros(E) if flags & LOG_TRUE_OBJ else None
         log = RunLog(obj.ctypes.data_as(P(C.c_double)), rmse.ctypes.data_as(P(C.c_double)),
                      mu.ctypes.data_as(P(C.c_double)), sr.ctypes.data_as(P(C.c_int32)),
                      sc.ctypes.data_as(P(C.c_int32)), vis.ctypes.data_as(P(C.c_uint64)),
                      tms.ctypes.data_as(P(C.c_double)) if tms is not None else None,
                      otrue.ctypes.data_as(P(C.c_double)) if otrue is not None else None,
-                     otv.ctypes.data_as(P(C.c_double)) if otv is not None else None)
+                     otv.ctypes.data_as(P(C.c_double)) if otv is not None else None,
+                     oseen.ctypes.data_as(P(C.c_double)) if oseen is not None else None)
         self._c(_lib.bsgd_run(self.h, _ptr(y), _ptr(x), _ptr(x_true), C.byref(prm), C.byref(log), _stream(stream)))
         return RunResult(obj[:epochs], rmse[:epochs], mu[:epochs], sr.reshape(E, aM)[:epochs],
                          sc.reshape(E, gN)[:epochs], vis[:epochs],
                          tms.reshape(E, 6)[:epochs] if tms is not None else None,
                          otrue[:epochs] if otrue is not None else None,
-                         otv[:epochs] if otv is not None else None)
+                         otv[:epochs] if otv is not None else None,
+                         oseen[:epochs] if (oseen is not None and x_true is not None) else None)
 
     def solve(self, solver, y, x, iters, mu0, lam=0.0, tv_iters=20, svrg_m=0, seed=1, stream=None):
         """Comparison solver `solver` in {"gd", "gd_bb", "ista", "fista", "svrg"} (bsgd_solve;

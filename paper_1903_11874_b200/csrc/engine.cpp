@@ -92,6 +92,8 @@ struct bsgd_ctx_s {
     float* tvv_halo = nullptr;   // tv_value: x plane z0-1 from the previous rank
     double* d_tvv = nullptr;     // per-epoch TV(x) (BSGD_LOG_TRUE_OBJ with log->tv)
     double* d_tvv1 = nullptr;    // bsgd_tv_value
+    float* seen = nullptr;       // A^T 1 over all views (owned voxels): > 0 where a ray passes
+    double* d_seenlog = nullptr; // per-epoch [sum (x - x_true)^2, count] over the seen voxels
     double* d_gap = nullptr;     // ... and 1/2-less |y - A x|^2 per epoch
     int d_gap_n = 0;
     // deterministic BP (BSGD_DETERMINISTIC): int64 fixed-point twins of accN / accT
@@ -999,6 +1001,20 @@ struct bsgd_ctx_s {
         launch_tv_u(Tl, pf, x_owned, st);
     }
 
+    // A^T 1 over every view into `seen` (once): the voxels some ray crosses (reading A32)
+    void ensure_seen(cudaStream_t st) {
+        if (seen) return;
+        seen = dnew<float>((long long)s * bsize, false);
+        float* ones = dnew<float>(n_rays, false);
+        launch_fill(ones, n_rays, 1.f, st);
+        std::vector<int> all(n_views);
+        for (int v = 0; v < n_views; ++v) all[v] = v;
+        for (int b = 0; b < s; ++b) {
+            project(PROJ_BP, all, {b}, {}, {}, {}, {pN(accN, b)}, {pT(accT, b)}, {}, ones, 1.f, 0, st, 0);
+            update(UPD_OUT, b, nullptr, 0.f, 0, seen + b * bsize, 0, st);
+        }
+    }
+
     // TV(x) (Eq. 6) of the whole volume into *d_out (device; summed over ranks)
     void tv_value(const float* x_owned, double* d_out, cudaStream_t st) {
         const long long n = (long long)s * bsize, plane = (long long)dims[0] * dims[1];
@@ -1636,8 +1652,10 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             if (c->d_gap_n < E) {
                 c->d_gap = c->dnew<double>(E);
                 c->d_tvv = c->dnew<double>(E);
+                c->d_seenlog = c->dnew<double>(2LL * E);
                 c->d_gap_n = E;
             }
+            if (log->rmse_seen && xt_in) c->ensure_seen(st);
         }
         if (timing) {
             ev.resize((size_t)E * 7);
@@ -1725,6 +1743,11 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 BSGD_CUDA(cudaMemsetAsync(c->d_gap + e, 0, sizeof(double), st));
                 launch_sqdiff(y, c->gap_proj, c->n_rays, c->d_gap + e, st);
                 if (log->tv) c->tv_value(x, c->d_tvv + e, st);
+                if (log->rmse_seen && xt) {
+                    BSGD_CUDA(cudaMemsetAsync(c->d_seenlog + 2 * e, 0, 2 * sizeof(double), st));
+                    launch_sqdiff_masked(x, xt, c->seen, sb, c->d_seenlog + 2 * e, st);
+                    c->allreduce_d(c->d_seenlog + 2 * e, 2, st);
+                }
             }
             if (xt) {
                 BSGD_CUDA(cudaMemsetAsync(c->d_red + 8, 0, sizeof(double), st));
@@ -1782,6 +1805,9 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         std::vector<double> hl(2 * (size_t)E + 2), hgap(true_obj ? E : 0);
         BSGD_CUDA(cudaMemcpyAsync(hl.data(), c->d_log, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, st));
         std::vector<double> htv(true_obj && log->tv ? E : 0);
+        std::vector<double> hseen(true_obj && log->rmse_seen && xt ? 2 * E : 0);
+        if (!hseen.empty())
+            BSGD_CUDA(cudaMemcpyAsync(hseen.data(), c->d_seenlog, sizeof(double) * 2 * E, cudaMemcpyDeviceToHost, st));
         if (true_obj) BSGD_CUDA(cudaMemcpyAsync(hgap.data(), c->d_gap, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
         if (!htv.empty()) BSGD_CUDA(cudaMemcpyAsync(htv.data(), c->d_tvv, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
         BSGD_CUDA(cudaStreamSynchronize(st));
@@ -1792,6 +1818,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 if (log->rmse) log->rmse[e] = xt ? sqrt(hl[2 * e + 1] / nvox) : NAN;
                 if (true_obj) log->obj_true[e] = 0.5 * hgap[e];
                 if (!htv.empty()) log->tv[e] = htv[e];
+                if (!hseen.empty()) log->rmse_seen[e] = hseen[2 * e + 1] > 0 ? sqrt(hseen[2 * e] / hseen[2 * e + 1]) : NAN;
                 if (log->mu) log->mu[e] = mu_log[e];
                 if (log->visits) log->visits[e] = vis_log[e];
                 if (timing) {

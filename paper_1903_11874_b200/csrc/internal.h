@@ -154,6 +154,9 @@ void launch_axpy_eud(float* eud, const float* g, long long n, cudaStream_t st);
 void launch_dot3(const float* a, const float* b, long long n, double* out3, cudaStream_t st);
 void launch_sqdiff(const float* a, const float* b, long long n, double* out, cudaStream_t st);
 void launch_fill_random(float* v, long long n, uint64_t seed, cudaStream_t st);
+void launch_fill(float* v, long long n, float val, cudaStream_t st);
+void launch_sqdiff_masked(const float* a, const float* b, const float* mask, long long n, double* out,
+                          cudaStream_t st);
 void launch_lincomb(float* out, float a, const float* x, float b, const float* y, float c, const float* z,
                     long long n, cudaStream_t st);
 void launch_bb_dots(const float* x, const float* xp, const float* gp, const float* g, long long n, double* out2,

@@ -338,6 +338,31 @@ __global__ void __launch_bounds__(256) k_sqdiff(const float* a, const float* b, 
     if (threadIdx.x == 0) atomicAdd(out, s);
 }
 
+// out[0] += sum (a - b)^2 and out[1] += count over the voxels with mask > 0 (RMSE over the
+// voxels some ray sees, reading A32)
+__global__ void __launch_bounds__(256) k_sqdiff_masked(const float* a, const float* b, const float* mask,
+                                                       long long n, double* out) {
+    double s = 0, c = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (mask[i] > 0.f) {
+            const double d = (double)a[i] - (double)b[i];
+            s += d * d;
+            c += 1.0;
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) atomicAdd(out, s);
+    c = block_sum(c);
+    if (threadIdx.x == 0) atomicAdd(out + 1, c);
+}
+
+__global__ void __launch_bounds__(256) k_fill(float* v, long long n, float val) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        v[i] = val;
+}
+
 // out = a x + b y (+ c z): the comparison solvers' vector updates.
 // Plain fp32 streaming (HBM-bound: 12-16 B per element).
 __global__ void __launch_bounds__(256) k_lincomb(float* out, float a, const float* x, float b,
@@ -878,6 +903,19 @@ void launch_lincomb(float* out, float a, const float* x, float b, const float* y
 void launch_bb_dots(const float* x, const float* xp, const float* gp, const float* g, long long n, double* out2,
                     cudaStream_t st) {
     k_bb_dots<<<grid_for(n, 8), 256, 0, st>>>(x, xp, gp, g, n, out2);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_sqdiff_masked(const float* a, const float* b, const float* mask, long long n, double* out,
+                          cudaStream_t st) {
+    k_sqdiff_masked<<<grid_for(n, 8), 256, 0, st>>>(a, b, mask, n, out);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_fill(float* v, long long n, float val, cudaStream_t st) {
+    k_fill<<<grid_for(n, 4), 256, 0, st>>>(v, n, val);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

@@ -742,15 +742,21 @@ def test_log_true_objective(bs):
     mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
     prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=3, total_epochs=6)
     o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11, tiles=p.tiles)
-    want, tvw = [], []
+    xtb = P.grid.to_blocks(vol32)
+    ones = np.ones(g.n_rays)
+    seen = np.array([P.bp(np.arange(g.n_views), j, ones) for j in range(p.N)]) > 0   # A^T 1 > 0 (A32)
+    want, tvw, rsw = [], [], []
     for _ in range(6):
         o.epoch()
         want.append(o.true_objective())
         tvw.append(ob.tv_value(o.grid.from_blocks(o.x)))
+        rsw.append(float(np.sqrt(np.mean((o.x[seen] - xtb[seen]) ** 2))))
     ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles)
     yd = torch.from_numpy(y).cuda()
     xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
-    res = ctx.run(yd, xd, epochs=6, mu0=mu, seed=3, rows_per_epoch=1, cols_per_epoch=3, flags=bs.LOG_TRUE_OBJ)
+    xt = torch.from_numpy(xtb.ravel().copy()).cuda()
+    res = ctx.run(yd, xd, epochs=6, mu0=mu, seed=3, x_true=xt, rows_per_epoch=1, cols_per_epoch=3,
+                  flags=bs.LOG_TRUE_OBJ)
     ctx.close()
     want = np.array(want)
     err = np.max(np.abs(res.obj_true - want) / want)
@@ -759,3 +765,6 @@ def test_log_true_objective(bs):
     assert np.all(np.abs(res.obj - res.obj_true) > 1e-6 * want)     # stale z: the two differ
     tvw = np.array(tvw)
     assert np.max(np.abs(res.tv - tvw) / tvw) < 1e-4, (res.tv, tvw)  # TV(x_k) log
+    rsw = np.array(rsw)
+    print("seen fraction", seen.mean(), "rmse_seen", res.rmse_seen, "rmse", res.rmse)
+    assert np.max(np.abs(res.rmse_seen - rsw) / rsw) < 1e-4, (res.rmse_seen, rsw)
