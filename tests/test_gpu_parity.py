@@ -768,3 +768,48 @@ def test_log_true_objective(bs):
     rsw = np.array(rsw)
     print("seen fraction", seen.mean(), "rmse_seen", res.rmse_seen, "rmse", res.rmse)
     assert np.max(np.abs(res.rmse_seen - rsw) / rsw) < 1e-4, (res.rmse_seen, rsw)
+
+
+def test_virtual_ranks_deterministic_reproducible(bs):
+    """BSGD_DETERMINISTIC on 2 virtual ranks: the fixed-point BP, the fixed-order norm and the
+    rank-ascending allreduce make two multi-rank runs bit-identical (x, objective)."""
+    import threading
+    p, g, vol32, y = problem("cfg3", K=48, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = float(np.float32(0.5 / ob.power_iteration(P, 30, seed=1)))
+    G, nb = 2, p.N // 2
+
+    def once():
+        group = bs.VirtualGroup(G)
+        ctxs = [bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles, rank=r,
+                                         world=G, vgroup=group) for r in range(G)]
+        out, errs = [None] * G, []
+
+        def rank_main(r):
+            try:
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    yd = torch.from_numpy(y).cuda()
+                    xd = torch.zeros(nb * P.grid.bsize, device="cuda")
+                    res = ctxs[r].run(yd, xd, epochs=6, mu0=mu, seed=3, rows_per_epoch=1, cols_per_epoch=4,
+                                      flags=bs.DETERMINISTIC | bs.IS | bs.AUTO_MU, stream=s)
+                    s.synchronize()
+                    out[r] = (res.obj.copy(), xd.cpu().numpy())
+            except Exception as e:      # noqa: BLE001 -- surfaced below
+                errs.append(e)
+
+        th = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+        for c in ctxs:
+            c.close()
+        group.close()
+        assert not errs, errs
+        return out
+
+    a, b = once(), once()
+    for r in range(G):
+        assert np.array_equal(a[r][0], b[r][0]) and np.array_equal(a[r][1], b[r][1]), r
+    assert np.array_equal(a[0][0], a[1][0])
