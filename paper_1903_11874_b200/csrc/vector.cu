@@ -786,6 +786,19 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
     }
 }
 
+// float4 form of k_tv_out (nx % 4 == 0): 4 x voxels per lane, in place (b = x is read only at
+// the lane's own voxels)
+__global__ void __launch_bounds__(256) k_tv_out4(const TvLaunch T, float* out) {
+    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
+    const int x = blockIdx.x * TV4_TX + 4 * lane, y = blockIdx.y * 8 + row, z = T.z0 + blockIdx.z;
+    const bool act = x < T.dims[0] && y < T.dims[1];
+    float u[4];
+    tv_u4(T, tv_plane(T, z), x, y, z, act, T.wf, u);
+    if (!act) return;
+    const long long i = (long long)blockIdx.z * T.dims[0] * T.dims[1] + (long long)y * T.dims[0] + x;
+    st4(out + i, u[0], u[1], u[2], u[3]);
+}
+
 // x = b - w grad^T p on a z-slab layout (the final step of the prox): one thread per voxel
 __global__ void __launch_bounds__(TV_TX * TV_TY) k_tv_out(const TvLaunch T, float* out) {
     const int x = blockIdx.x * TV_TX + threadIdx.x, y = blockIdx.y * TV_TY + threadIdx.y,
@@ -1015,7 +1028,13 @@ void launch_tv_fgp(const TvLaunch& T, cudaStream_t st) {
 void launch_tv_out(const TvLaunch& T, float* out, cudaStream_t st) {
     const dim3 grid((unsigned)((T.dims[0] + TV_TX - 1) / TV_TX), (unsigned)((T.dims[1] + TV_TY - 1) / TV_TY),
                     (unsigned)(T.z1 - T.z0));
-    k_tv_out<<<grid, dim3(TV_TX, TV_TY), 0, st>>>(T, out);
+    if (T.dims[0] % 4 == 0) {
+        const dim3 g4((unsigned)((T.dims[0] + TV4_TX - 1) / TV4_TX), (unsigned)((T.dims[1] + 7) / 8),
+                      (unsigned)(T.z1 - T.z0));
+        k_tv_out4<<<g4, 256, 0, st>>>(T, out);
+    } else {
+        k_tv_out<<<grid, dim3(TV_TX, TV_TY), 0, st>>>(T, out);
+    }
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
