@@ -152,79 +152,141 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- oracle (CPU) timing
 _ORACLE_CACHE = None
+# cfg5 views sampled for the CPU timing, spread over a quarter orbit (the cube's 4-fold
+# symmetry: a view's visit count depends on its angle mod 90 deg, e.g. +27 % at 45 deg vs
+# 0 deg), in bit-reversed order so that every prefix of the list spans the quarter
+SAMPLE_VIEWS = (0, 90, 45, 135, 23, 113, 68, 158)
 
 
-def oracle_sample(target_s=12.0, max_views=8):
-    """fp64 CPU oracle: FP + BP of whole views of the cfg5 workload through all 8
-    z-slabs (the same per-view work as the GPU epoch), on all host cores.
-    Returns (visits per second counting FP and BP separately, cores, sample text)."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_setup():
+    """Per sampled view: a one-view geometry (same rays as in the full geometry; keeps the
+    projection buffer at one view), its projector, and its exact FP visit count through
+    the 8 slabs (the oracle's own count, computed once, outside every timed region)."""
     global _ORACLE_CACHE
-    import synth
-    from oracle.projector import BlockGrid, Projector
-    p = synth.PRESETS["cfg5"]
-    g = p.geometry()
-    cores = os.cpu_count() or 1
     if _ORACLE_CACHE is None:
-        # one single-view geometry per sampled view (same rays as in the full geometry;
-        # keeps the projection buffer at one view) and its visit count, counted once
-        # outside the timed loop (a circular orbit gives every view the same count up to
-        # a few corner segments)
-        views = [synth.Geometry(g.beam, g.vecs[v:v + 1].copy(), g.det_u, g.det_v, g.dims)
-                 for v in (0, 97, 194, 291, 388, 485, 582, 679)]
-        projs = [Projector(gv, BlockGrid(g.dims, p.blocks)) for gv in views]
-        per_view = sum(projs[0].count([0], j) for j in range(p.N))
-        _ORACLE_CACHE = (projs, per_view, np.full(projs[0].grid.bsize, 0.5))
-    projs, per_view_visits, x = _ORACLE_CACHE
+        import synth
+        from oracle.projector import BlockGrid, Projector
+        p = synth.PRESETS["cfg5"]
+        g = p.geometry()
+        projs, counts = [], []
+        for v in SAMPLE_VIEWS:
+            gv = synth.Geometry(g.beam, g.vecs[v:v + 1].copy(), g.det_u, g.det_v, g.dims)
+            P = Projector(gv, BlockGrid(g.dims, p.blocks))
+            projs.append(P)
+            counts.append(sum(P.count([0], j) for j in range(p.N)))
+        # visits of one epoch (FP; BP visits are the same segments) = 72 views x the mean
+        # visits per view over the sampled quarter orbit
+        epoch_fp = (g.n_views // p.M) * float(np.mean(counts))
+        _ORACLE_CACHE = (p, g, projs, counts, epoch_fp, np.full(projs[0].grid.bsize, 0.5))
+    return _ORACLE_CACHE
+
+
+def oracle_sample(target_s=12.0, max_views=len(SAMPLE_VIEWS), first=0):
+    """fp64 CPU oracle: FP + BP of whole sampled cfg5 views through all 8 z-slabs (the same
+    per-view work as the GPU epoch) on all host cores, until `target_s` has elapsed.
+    Visits are the oracle's own per-view counts.  Returns a dict."""
+    p, g, projs, counts, epoch_fp, x = _oracle_setup()
     proj = np.zeros(g.det_u * g.det_v)
-    visits = 0
-    views_done = 0
-    t0 = time.perf_counter()
-    while views_done < max_views:
-        P = projs[views_done % len(projs)]
+    visits, done, t0 = 0, [], time.perf_counter()
+    while len(done) < max_views:
+        k = (first + len(done)) % len(projs)
+        P = projs[k]
         proj[:] = 0.0
         for j in range(p.N):
             P.fp([0], j, x, proj=proj, accumulate=True)
         for j in range(p.N):
             P.bp([0], j, proj)
-        visits += 2 * per_view_visits
-        views_done += 1
+        visits += 2 * counts[k]
+        done.append(SAMPLE_VIEWS[k])
         if time.perf_counter() - t0 > target_s:
             break
     dt = time.perf_counter() - t0
-    sample = (f"{views_done} whole view(s) of cfg5 (1024x1024 rays) FP+BP through all 8 z-slabs, fp64 merged-alpha "
-              f"Siddon, OpenMP on {cores} host threads; {visits:.3g} visits in {dt:.1f} s (visit count from one "
-              f"counting pass, excluded from the time)")
-    return visits / dt, cores, sample, visits, dt
+    threads = int(os.environ.get("OMP_NUM_THREADS", "0")) or (os.cpu_count() or 1)
+    return {"vps": visits / dt, "visits": visits, "seconds": dt, "views": done, "threads": threads,
+            "epochs_per_s": visits / dt / (2.0 * epoch_fp), "epoch_fp_visits": epoch_fp}
 
 
-def epoch_visits_estimate():
-    """Visits (FP) of one cfg5 epoch: 72 views x 1.155e9 visits/view."""
-    return 72 * 1.155e9
+def oracle_one_thread(seconds=3.0):
+    """The same oracle on ONE host thread (a subprocess with OMP_NUM_THREADS=1): FP + BP of
+    detector-row bands of sampled views; visits/s per core."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    code = ("import json,sys; sys.path.insert(0, %r); import bench; "
+            "print(json.dumps(bench._band_sample(%r)))" % (ROOT, seconds))
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:   # noqa: BLE001  (auxiliary figure)
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+
+def _band_sample(seconds):
+    """FP + BP of 8-row detector bands of the sampled views (the counts outside the timing)."""
+    import synth
+    from oracle.projector import BlockGrid, Projector
+    p = synth.PRESETS["cfg5"]
+    g = p.geometry()
+    x = None
+    visits, timed, n = 0, 0.0, 0
+    while timed < seconds:
+        v = SAMPLE_VIEWS[n % len(SAMPLE_VIEWS)]
+        gv = synth.Geometry(g.beam, g.vecs[v:v + 1].copy(), g.det_u, g.det_v, g.dims)
+        P = Projector(gv, BlockGrid(g.dims, p.blocks))
+        if x is None:
+            x = np.full(P.grid.bsize, 0.5)
+        rect = [(0, g.det_u, 480 + 8 * (n % 8), 488 + 8 * (n % 8))]
+        cnt = sum(P.count([0], j, rects=rect) for j in range(p.N))
+        t1 = time.perf_counter()
+        proj = np.zeros(g.det_u * g.det_v)
+        for j in range(p.N):
+            P.fp([0], j, x, proj=proj, rects=rect, accumulate=True)
+        for j in range(p.N):
+            P.bp([0], j, proj, rects=rect)
+        timed += time.perf_counter() - t1
+        visits += 2 * cnt
+        n += 1
+    return {"vps_per_core": visits / timed, "bands": n, "threads": 1}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
+    # rank 0 alone does the work: all host cores (torch.distributed.run exports
+    # OMP_NUM_THREADS=1 to every rank; BENCH_OMP_THREADS overrides)
+    os.environ["OMP_NUM_THREADS"] = os.environ.get("BENCH_OMP_THREADS", str(os.cpu_count() or 1))
     os.environ.setdefault("OMP_PROC_BIND", "close")
-    per_step = []
-    vps_all = []
-    cores = os.cpu_count()
-    sample = ""
+    _oracle_setup()
+    per_step, vps_all, views = [], [], []
     for it in range(args.warmup + args.steps):
-        vps, cores, sample, visits, dt = oracle_sample(target_s=4.0, max_views=1)
+        r = oracle_sample(target_s=4.0, max_views=1, first=it)
         if it >= args.warmup:
-            per_step.append(dt)
-            vps_all.append(vps)
+            per_step.append(r["seconds"])
+            vps_all.append(r["vps"])
+            views += r["views"]
+    p, g, projs, counts, epoch_fp, _ = _oracle_setup()
     vps = float(np.median(vps_all))
-    ev = 2 * 72 * _ORACLE_CACHE[1]      # FP + BP visits of one epoch: 72 views x (visits per view)
-    value = vps / ev
+    value = vps / (2.0 * epoch_fp)
+    cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or (os.cpu_count() or 1)
+    sample = (f"each step = one whole cfg5 view (1024x1024 rays) FP+BP through all 8 z-slabs, fp64 merged-alpha "
+              f"Siddon, OpenMP on {cores} host threads ({_cpu_model()}); views {views}; visits from the "
+              f"oracle's own per-view count; epoch = {g.n_views // p.M} views x the mean visits per view of "
+              f"the quarter-orbit sample {list(SAMPLE_VIEWS)} = {epoch_fp:.4g} FP visits")
     line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "epochs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per_step)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "intersections_per_s": vps,
-            "config": {"workload": WORKLOAD, "sample": "each step = " + sample},
+            "config": {"workload": WORKLOAD, "sample": sample},
             "cpu_baseline": {"value": value, "unit": "epochs/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": "epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -339,6 +401,21 @@ def run_ours(args, rank, world, local_rank):
                "what": ("bsgd_run(y, x on pinned host memory): y and x uploaded (on a copy stream, "
                         "overlapped with the first epoch), K epochs, x copied back")}
         del yh, xh
+    allreduce = None
+    if world > 1:   # the epoch's exchange on its own: the partial sums of one row block
+        count = (g.n_views // p.M) * g.det_u * g.det_v
+        ms = ctx.allreduce_time(count, iters=5, stream=stream)
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        nbytes = 4.0 * count
+        allreduce = {"bytes": nbytes, "ms": ms, "algbw_gbs": nbytes / (ms / 1e3) / 1e9,
+                     "bus_gbs": nbytes / (ms / 1e3) * 2 * (world - 1) / world / 1e9,
+                     "vs_gbs": 900.0, "measured_ref_gbs": 725.0,
+                     "what": "bsgd_allreduce_time: ncclAllReduce (sum, fp32) of the residual's partial-sum buffer "
+                             "(72 views x 1024^2 rays), 5 back-to-back calls timed with CUDA events on the launch "
+                             "stream, max over ranks; busbw = S/t x 2(G-1)/G",
+                     "residual_phase_ms": res_ms}
     tv = None
     if not args.no_tv:   # an auxiliary measurement: never lose the main line over it
         try:
@@ -350,9 +427,17 @@ def run_ours(args, rank, world, local_rank):
         return 0
     cpu = None
     if world == 1 and not args.no_cpu and args.config == "cfg5":
-        vps, cores, sample, _, _ = oracle_sample(target_s=args.cpu_seconds)
-        cpu = {"value": vps / (2 * vis_ep), "unit": "epochs/s", "cores": cores, "kind": "oracle",
-               "sample": sample, "intersections_per_s": vps}
+        r = oracle_sample(target_s=args.cpu_seconds)
+        one = oracle_one_thread()
+        cpu = {"value": r["epochs_per_s"], "unit": "epochs/s", "cores": r["threads"], "kind": "oracle",
+               "sample": (f"{len(r['views'])} whole cfg5 view(s) {r['views']} (1024x1024 rays each) FP+BP through all "
+                          f"8 z-slabs, fp64 merged-alpha Siddon, OpenMP on {r['threads']} host threads; "
+                          f"{r['visits']:.4g} visits (the oracle's own per-view counts, outside the timing) in "
+                          f"{r['seconds']:.1f} s; epoch = {g.n_views // p.M} views x the mean visits per view of "
+                          f"the quarter-orbit sample {list(SAMPLE_VIEWS)} = {r['epoch_fp_visits']:.4g} FP visits "
+                          f"(this run's GPU epochs: {vis_ep:.4g})"),
+               "intersections_per_s": r["vps"], "cpu_model": _cpu_model(),
+               "one_thread": one}
     line = {
         "metric": METRIC, "value": epochs_per_s, "unit": "epochs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -369,12 +454,7 @@ def run_ours(args, rank, world, local_rank):
                    "visits_per_epoch_fp": visits_all / 2.0 / args.steps,   # all ranks
                    "fp64": "ray parameters fp64, values fp32"},
         "phase_ms": {"fp": fp_ms, "residual_allreduce": res_ms, "bp": bp_ms, "step": st_ms},
-        "allreduce": None if world == 1 else {
-            "bytes_per_epoch": 4 * 72 * g.det_u * g.det_v,
-            "bus_gbs_lower_bound":(4 * 72 * g.det_u * g.det_v) / (res_ms / 1e3) * 2 * (world - 1) / world / 1e9,
-            "vs_gbs": 900.0,
-            "note": "residual phase time includes the partial-sum and residual kernels, so this is a lower bound "
-                    "on the collective's own bus bandwidth"},
+        "allreduce": allreduce,
         "roofline": {"bound": "hbm",
                      "kernel": "projector pair k_project3<FP> + k_project3<BP> (+ k_project2 steep-only companions)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -433,6 +513,39 @@ def time_tv(bs, ctx, x, w, p, aM, gN, world, stream, epoch_ms, peak, iters=20, c
             "epochs_per_s_tv_amortised": 1e3 / (epoch_ms + ms / period)}
 
 
+def self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks of this same command line with
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1), rank 0 prints."""
+    import socket
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are "
+                             f"visible; refusing to time fewer GPUs than requested\n")
+            return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world) -> int:
+    """--dry-run: the multi-rank plumbing only (gloo on CPU): every rank contributes 1 to an
+    all-reduce; rank 0 prints what would be timed."""
+    import torch
+    import torch.distributed as dist
+    t = torch.ones(1)
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": int(t.item()),
+                          "steps": args.steps, "warmup": args.warmup}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -447,14 +560,33 @@ def main():
     ap.add_argument("--eq8", action="store_true",
                     help="Eq. 8 schedule (gamma N = G, alpha M from Eq. 8), stratified by owner: weak scaling")
     ap.add_argument("--cheap-data", action="store_true", help="uniform random y instead of analytic projections")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank launch check on CPU (gloo), no GPU work")
     ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="workload (cfg5 = the BASELINE.json headline; the others for DESIGN tables)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl == "ours":
+        return self_launch(args)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(env_world) if env_world is not None else 1
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, world if env_world is not None else args.gpus)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; refusing to mislabel the run\n")
+        return 1
+    if args.dry_run:
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        try:
+            return dry_run(args, rank, world)
+        finally:
+            if world > 1:
+                import torch.distributed as dist
+                dist.destroy_process_group()
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -23,6 +23,10 @@
  *    cudaPointerGetAttributes; host buffers are copied in and x copied back).
  *  - Streams: every enqueueing call takes a cudaStream_t as void* (NULL = the
  *    legacy default stream).  Calls are asynchronous unless stated otherwise.
+ *    Consecutive calls on one ctx may use different streams: each call's stream
+ *    first waits for the work the previous call enqueued (the calls share the
+ *    ctx's launch tables and scratch buffers), so a ctx's calls execute in
+ *    call order whatever streams they name.
  *  - Ownership: the caller owns every buffer it passes; the ctx owns its
  *    internal state (z^j, g_hat^i, g, r, transposed image copy, scratch),
  *    allocated at create through `bsgd_alloc` (NULL = cudaMalloc).
@@ -44,7 +48,7 @@
 extern "C" {
 #endif
 
-#define BSGD_ABI_VERSION 2
+#define BSGD_ABI_VERSION 3
 
 typedef struct bsgd_ctx_s* bsgd_ctx;
 
@@ -230,6 +234,12 @@ typedef struct {
     double eps, delta, t1, t2;                /* Algo 3 constants (reading A12: .05, .4, .5, 0)   */
     int32_t is_off_last_epochs;               /* final epochs without IS           */
     int32_t strata;                           /* BSGD_STRATIFIED: number of strata (0 = world)   */
+    int32_t total_epochs;                     /* planned run length in GLOBAL epochs, for
+                                                 is_off_last_epochs: IS is off in the epochs
+                                                 k > total_epochs - is_off_last_epochs (k the
+                                                 1-based global epoch, counting across RESUME
+                                                 calls).  0 = this call ends the run (total =
+                                                 global epoch at entry + epochs)               */
 } bsgd_run_params;
 
 /* Per-epoch log; every pointer is host memory and nullable.                  */
@@ -270,6 +280,16 @@ bsgd_status bsgd_set_state(bsgd_ctx ctx, int32_t what, int32_t index, const void
 bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, double* sigma_max_sq,
                                  void* stream);
 
+/* The residual exchange of Algo 1 line 7 on its own (the ALLREDUCE of the partial
+ * projections): `iters` sum-allreduces of the first `count` floats of the
+ * ctx's partial-sum buffer over the ctx's communicator (NCCL, or the virtual-rank group),
+ * enqueued on `stream` and timed there with CUDA events; *ms_out = mean milliseconds per
+ * allreduce.  For the bench's bus-bandwidth figure; clobbers only that scratch buffer.
+ * Collective: every rank calls it with the same count / iters.  Synchronous.
+ * Errors: BSGD_E_CONTRACT if the ctx has no collective path (world == 1 without
+ * BSGD_FORCE_NCCL), count < 1 or count > n_rays, iters < 1.                      */
+bsgd_status bsgd_allreduce_time(bsgd_ctx ctx, int64_t count, int32_t iters, void* stream, double* ms_out);
+
 /* TV proximal step (Algo 4 line 16; TV of Eq. 5-6):
  * x_owned <- argmin_t 1/2 ||t - x_owned||^2 + w TV(t), by `iters` cold-start FGP iterations
  * on the dual (reading A16; the same call bsgd_run makes every tv_period epochs, with
@@ -279,7 +299,8 @@ bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, dou
  * world > 1 (z-slab halo planes by ncclSend/Recv; every rank calls it).  w = 0 or iters = 0
  * leaves x unchanged.  method: 0 = FGP (default of bsgd_run), 1 = Chambolle 2004 (tau = 1/8
  * in 2D, 1/12 in 3D; SURVEY §8c step 7's flag; bsgd_run with BSGD_TV_CHAMBOLLE).
- * Errors: BSGD_E_CONTRACT for NULL x, w < 0, iters < 0 or an unknown method.             */
+ * Errors: BSGD_E_CONTRACT for NULL x, w < 0 or not finite, iters < 0 or an unknown method;
+ * BSGD_E_PARTITION when world > 1 and the block grid is not z-slabs (1, 1, N).          */
 bsgd_status bsgd_tv_prox(bsgd_ctx ctx, float* x_owned, double w, int32_t iters, int32_t method,
                          void* stream);
 /* TV(x) = sum over voxels of |grad x|_2 (isotropic backward differences, zero at index 0;

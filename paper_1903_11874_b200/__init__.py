@@ -90,7 +90,7 @@ class RunParams(C.Structure):
                 ("cols_per_epoch", C.c_int32), ("mu0", C.c_double), ("flags", C.c_uint32),
                 ("lambda_", C.c_double), ("tv_iters", C.c_int32), ("tv_period", C.c_int32),
                 ("eps", C.c_double), ("delta", C.c_double), ("t1", C.c_double), ("t2", C.c_double),
-                ("is_off_last_epochs", C.c_int32), ("strata", C.c_int32)]
+                ("is_off_last_epochs", C.c_int32), ("strata", C.c_int32), ("total_epochs", C.c_int32)]
 
 
 class RunLog(C.Structure):
@@ -141,6 +141,7 @@ SIGS = {
     "bsgd_get_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
+    "bsgd_allreduce_time": ([_ctx, C.c_int64, C.c_int32, C.c_void_p, P(C.c_double)], C.c_int),
     "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "bsgd_tv_value": ([_ctx, C.c_void_p, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
@@ -423,9 +424,9 @@ class Context:
 
     def run(self, y, x, epochs, mu0, seed=1, x_true=None, rows_per_epoch=0, cols_per_epoch=0, flags=0,
             lam=0.1, tv_iters=20, tv_period=0, eps=0.05, delta=0.4, t1=0.5, t2=0.0, is_off_last=0,
-            strata=0, stream=None) -> RunResult:
+            strata=0, total_epochs=0, stream=None) -> RunResult:
         prm = RunParams(seed, epochs, rows_per_epoch, cols_per_epoch, mu0, flags, lam, tv_iters, tv_period,
-                        eps, delta, t1, t2, is_off_last, strata)
+                        eps, delta, t1, t2, is_off_last, strata, total_epochs)
         aM = rows_per_epoch or eq8(self.info.N // self.owned_count, self.M, self.N)[0]
         gN = cols_per_epoch or eq8(self.info.N // self.owned_count, self.M, self.N)[1]
         E = max(epochs, 1)
@@ -486,6 +487,13 @@ class Context:
         """TV(x) of the whole volume (bsgd_tv_value; Eq. 6)."""
         out = C.c_double()
         self._c(_lib.bsgd_tv_value(self.h, _ptr(x), C.byref(out), _stream(stream)))
+        return out.value
+
+    def allreduce_time(self, count, iters=5, stream=None) -> float:
+        """Mean ms of one sum-allreduce of `count` floats of the residual's partial-sum
+        buffer (bsgd_allreduce_time; the ALLREDUCE of PAPER.md:99 on its own)."""
+        out = C.c_double()
+        self._c(_lib.bsgd_allreduce_time(self.h, int(count), int(iters), _stream(stream), C.byref(out)))
         return out.value
 
     def power_iteration(self, iters=30, seed=0, stream=None) -> float:

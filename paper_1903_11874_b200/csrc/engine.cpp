@@ -102,6 +102,7 @@ struct bsgd_ctx_s {
     long long* acc64T = nullptr;
     float* d_det_scale = nullptr;
     unsigned* d_det_max = nullptr;
+    double rays_per_cell = 0.0;   // upper bound on the rays of one view crossing one cell (set at create)
     size_t vg_tmp_bytes = 0;
     long long bsize = 0, n_rays = 0, per = 0;
     double R = 0.0;
@@ -163,6 +164,30 @@ struct bsgd_ctx_s {
     double theta_prev = 0.0;
     std::vector<double> rnorm_hist;     // ||r||^{k} at k = 0, M, 2M, ...
     ncclComm_t comm = nullptr;
+    // Calls may come on different streams, but they share the launch-table arena (d_tab), the
+    // BP accumulators and the FP scratch copies: every call first waits for the work the
+    // previous call enqueued (an event recorded on its stream), so a table or accumulator is
+    // never rewritten while a kernel of an earlier call on another stream still reads it.
+    cudaEvent_t order_ev = nullptr;
+    cudaStream_t order_st = nullptr;
+    bool order_valid = false;
+    void stream_enter(cudaStream_t st) {
+        if (order_valid && order_st != st) BSGD_CUDA(cudaStreamWaitEvent(st, order_ev, 0));
+    }
+    void stream_leave(cudaStream_t st) {
+        if (!order_ev && cudaEventCreateWithFlags(&order_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            order_ev = nullptr;
+            return;
+        }
+        if (cudaEventRecord(order_ev, st) != cudaSuccess) {
+            cudaGetLastError();
+            order_valid = false;
+            return;
+        }
+        order_st = st;
+        order_valid = true;
+    }
     bool poisoned = false;
     std::string err;
 
@@ -205,6 +230,8 @@ struct bsgd_ctx_s {
     float* pN(float* base, long long b) const { return base + b * padN + orgN; }
     float* pT(float* base, long long b) const { return base + b * padT + orgT; }
     void release() {
+        if (order_ev) cudaEventDestroy(order_ev);
+        order_ev = nullptr;
         for (auto& e : up_ev) cudaEventDestroy(e);
         up_ev.clear();
         if (copy_st) cudaStreamDestroy(copy_st);
@@ -277,6 +304,34 @@ struct bsgd_ctx_s {
         u0 = (u0 / 32) * 32;
         u1 = std::min(nu, ((u1 + 31) / 32) * 32);
         return make_int4(u0, u1, v0, v1);
+    }
+
+    // Upper bound on the number of rays of one view that cross one cell (the deterministic BP's
+    // fixed-point range, k_det_scale).  A cell's projection spans at most sqrt(3) * magnification
+    // voxel units along each detector axis, i.e. ceil(sqrt(3) m / |u|) + 1 pixel columns and as
+    // many rows (+1 for a partial pixel); m = 1 for parallel beams and |s - d_c| / (distance of
+    // the source from the volume's bounding sphere) for fan / cone.  A source inside that sphere
+    // has no bound: every ray of the view is counted.
+    double compute_rays_per_cell() const {
+        const double Rv = 0.5 * sqrt((double)dims[0] * dims[0] + (double)dims[1] * dims[1] + (double)dims[2] * dims[2]);
+        double worst = 1.0;
+        for (int v = 0; v < n_views; ++v) {
+            const double* q = &vecs[12 * (size_t)v];
+            const double pu = sqrt(q[6] * q[6] + q[7] * q[7] + q[8] * q[8]);
+            const double pv = sqrt(q[9] * q[9] + q[10] * q[10] + q[11] * q[11]);
+            double m = 1.0;
+            if (beam != BSGD_PARALLEL) {
+                const double ds = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]) - Rv;
+                const double sd = sqrt((q[3] - q[0]) * (q[3] - q[0]) + (q[4] - q[1]) * (q[4] - q[1]) +
+                                       (q[5] - q[2]) * (q[5] - q[2]));
+                if (!(ds > 0.0)) return (double)nu * nv;
+                m = sd / ds;
+            }
+            const double cu = nu > 1 && pu > 0 ? std::min<double>(nu, ceil(1.7320508075688772 * m / pu) + 2.0) : 1.0;
+            const double cv = nv > 1 && pv > 0 ? std::min<double>(nv, ceil(1.7320508075688772 * m / pv) + 2.0) : 1.0;
+            worst = std::max(worst, cu * cv);
+        }
+        return worst;
     }
 
     // pack host tables into the device arena; returns device pointers
@@ -357,6 +412,18 @@ struct bsgd_ctx_s {
         L.max_rect_rays = maxr;
         L.rows_per_band = R;
         L.n_chunks = (R * maxw + 255) / 256;
+        // row pairs (k_project5): the two rays of one detector column in adjacent rows share
+        // their in-plane path when the detector's v step has no x / y component (circular
+        // orbits, A19), so one thread can carry both; the companion v2 launch keeps the one-ray
+        // warp decomposition, which requires warps that do not straddle detector rows
+        bool pairs = nv > 1 && mode != PROJ_COUNT;
+        for (int k = 0; pairs && k < ns; ++k) {
+            const double* q = &vecs[12 * (size_t)views[k]];
+            pairs = q[9] == 0.0 && q[10] == 0.0;
+        }
+        for (size_t e = 0; pairs && e < rc.size(); ++e)
+            pairs = ((rc[e].y - rc[e].x) % 32) == 0;
+        L.pair_chunks = pairs ? (((R + 1) / 2) * maxw + 255) / 256 : 0;
         L.n_bands = nbands;
         L.rproj = rproj;
         L.scale = scale;
@@ -623,7 +690,7 @@ struct bsgd_ctx_s {
             d_det_scale = dnew<float>(1);
             d_det_max = dnew<unsigned>(1);
         }
-        launch_det_scale(r, n_rays, (int)vv.size(), 2.f, d_det_max, d_det_scale, st);
+        launch_det_scale(r, n_rays, (int)vv.size(), rays_per_cell, 2.f, d_det_max, d_det_scale, st);
         std::vector<float*> dN, dT;
         for (size_t k = 0; k < slots.size(); ++k) {   // the int64 twin at the same element offsets
             dN.push_back(reinterpret_cast<float*>(acc64N + (oN[k] - accN)));
@@ -875,7 +942,7 @@ struct bsgd_ctx_s {
                 if (obj_log) obj_log[k] = half_normsq(st);
                 if (mu_log) mu_log[k] = mu;
                 launch_lincomb(sv_c, 1.f, sv_b, (float)mu, sv_a, 0.f, nullptr, n, st);   // v + mu g(v)
-                tv_prox(sv_c, mu * lam, tv_iters, st);        // z+ (lam = 0: identity)
+                if (lam > 0.0) tv_prox(sv_c, mu * lam, tv_iters, st);   // z+ (lam = 0: identity)
                 const double t1 = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0, beta = (t - 1.0) / t1;
                 // v+ = z+ + beta (z+ - z)   (z = x)
                 launch_lincomb(sv_b, (float)(1.0 + beta), sv_c, (float)(-beta), x, 0.f, nullptr, n, st);
@@ -915,6 +982,7 @@ struct bsgd_ctx_s {
         // z-slab layouts (the owned volume is one [z][y][x] array) take the fused iteration
         const bool fused = bgrid[0] == 1 && bgrid[1] == 1;
         const long long plane = (long long)dims[0] * dims[1];
+        if (wgt == 0.0 || iters <= 0) return;   // the identity: no dual fields needed
         if (!tv_p) {
             tv_p = dnew<float>(3 * n, false);
             tv_q = dnew<float>(3 * n, false);
@@ -927,7 +995,6 @@ struct bsgd_ctx_s {
                 tv_hu = dnew<float>(plane);
             }
         }
-        if (wgt == 0.0 || iters <= 0) return;
         // b = x itself: read-only during the iterations, and the final x = b - w grad^T p reads
         // b only at the voxel it writes.  The fused path's first iteration treats q = p = 0
         // without reading them, so the dual fields need no clearing there.
@@ -1095,6 +1162,15 @@ template <class F> bsgd_status guard(bsgd_ctx ctx, F&& f) {
 
 cudaStream_t S(void* p) { return (cudaStream_t)p; }
 
+// Orders a call's stream after the previous call's work on the same context (see
+// bsgd_ctx_s::stream_enter); records this call's end on its stream when the scope closes.
+struct Ordered {
+    bsgd_ctx c;
+    cudaStream_t st;
+    Ordered(bsgd_ctx c_, cudaStream_t st_) : c(c_), st(st_) { c->stream_enter(st); }
+    ~Ordered() { c->stream_leave(st); }
+};
+
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
     cudaError_t e = cudaPointerGetAttributes(&a, p);
@@ -1257,6 +1333,7 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         }
         c->s = c->N / c->world;
         c->first = c->rank * c->s;
+        c->rays_per_cell = c->compute_rays_per_cell();
         if (const char* e = getenv("BSGD_BAND_ROWS")) c->band_rows = std::max(1, atoi(e));
         if (c->bsize >= (1LL << 31)) fail(BSGD_E_PARTITION, "a column block must hold fewer than 2^31 voxels");
         // row blocks
@@ -1402,6 +1479,7 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
         if (!c || !x_block || !proj) fail(BSGD_E_CONTRACT, "NULL");
         check_views(c, n, views, rects);
         if (!c->owned(col_block)) fail(BSGD_E_DIMENSION, "column block not owned by this rank");
+        Ordered order_(c, S(stream));
         if (n == 0) return;
         if (!c->fp_scratchT) {
             c->fp_scratchT = c->pT(c->dnew_pad(1, true), 0);
@@ -1439,6 +1517,7 @@ bsgd_status bsgd_back(bsgd_ctx c, int32_t n, const int32_t* views, const int32_t
         check_views(c, n, views, rects);
         if (!c->owned(col_block)) fail(BSGD_E_DIMENSION, "column block not owned by this rank");
         if (!isfinite(scale)) fail(BSGD_E_CONTRACT, "scale not finite");
+        Ordered order_(c, S(stream));
         const int b = col_block - c->first;
         cudaStream_t st = S(stream);
         std::vector<int> vv(views, views + n);
@@ -1459,6 +1538,7 @@ bsgd_status bsgd_im_weights(bsgd_ctx c, double* w_out, uint32_t* q_out) {
 bsgd_status bsgd_im_table(bsgd_ctx c, int32_t kind, double* w_out, uint32_t* q_out) {
     return guard(c, [&] {
         if (!c || kind < 0 || kind > 1) fail(BSGD_E_CONTRACT, "bad arguments");
+        Ordered order_(c, nullptr);
         c->ensure_im_table(nullptr, kind);
         if (w_out) memcpy(w_out, c->w.data(), sizeof(double) * c->w.size());
         if (q_out) memcpy(q_out, c->q.data(), sizeof(uint32_t) * c->q.size());
@@ -1468,6 +1548,7 @@ bsgd_status bsgd_im_table(bsgd_ctx c, int32_t kind, double* w_out, uint32_t* q_o
 bsgd_status bsgd_visit_table(bsgd_ctx c, uint64_t* nnz_out) {
     return guard(c, [&] {
         if (!c || !nnz_out) fail(BSGD_E_CONTRACT, "NULL");
+        Ordered order_(c, nullptr);
         c->ensure_visit_table(nullptr);
         for (size_t k = 0; k < c->vtab.size(); ++k) nnz_out[k] = c->vtab[k];
     });
@@ -1476,6 +1557,7 @@ bsgd_status bsgd_visit_table(bsgd_ctx c, uint64_t* nnz_out) {
 bsgd_status bsgd_reset(bsgd_ctx c, const float* y, void* stream) {
     return guard(c, [&] {
         if (!c || !y) fail(BSGD_E_CONTRACT, "NULL");
+        Ordered order_(c, S(stream));
         c->reset(y, S(stream));
     });
 }
@@ -1506,6 +1588,7 @@ bsgd_status bsgd_step(bsgd_ctx c, const float* y, float* x_owned, const bsgd_sel
             for (int t : tiles)
                 if (t < 0 || t >= c->T) fail(BSGD_E_CONTRACT, "tile id out of range");
         }
+        Ordered order_(c, S(stream));
         c->epoch_step(y, x_owned, rows, cols, tiles, mu, sgd, S(stream), nullptr);
         c->epoch += 1;
     });
@@ -1523,6 +1606,7 @@ bsgd_status bsgd_solve(bsgd_ctx c, const float* y, float* x_owned, const bsgd_so
         const bool tv = (P->solver == BSGD_SOLVER_ISTA || P->solver == BSGD_SOLVER_FISTA) && P->lambda > 0.0;
         if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
             fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        Ordered order_(c, S(stream));
         c->solve(P->solver, y, x_owned, P->iters, P->mu0, tv ? P->lambda : 0.0, P->tv_iters, P->svrg_m, P->seed,
                  obj, mu, S(stream));
         BSGD_CUDA(cudaStreamSynchronize(S(stream)));
@@ -1534,6 +1618,8 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
     return guard(c, [&] {
         if (!c || !y_in || !x_in || !P) fail(BSGD_E_CONTRACT, "NULL");
         if (P->epochs < 0) fail(BSGD_E_CONTRACT, "epochs < 0");
+        if (P->total_epochs < 0 || P->is_off_last_epochs < 0)
+            fail(BSGD_E_CONTRACT, "total_epochs and is_off_last_epochs must be >= 0");
         if (!isfinite(P->mu0)) fail(BSGD_E_CONTRACT, "mu0 not finite");
         const uint32_t known = BSGD_IS | BSGD_IS_UNIFORM | BSGD_TV | BSGD_AUTO_MU | BSGD_SGD | BSGD_RESUME | BSGD_TIMING |
                                BSGD_STRATIFIED | BSGD_IS_AREA | BSGD_TV_CHAMBOLLE | BSGD_DETERMINISTIC |
@@ -1556,7 +1642,10 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             fail(BSGD_E_CONTRACT, "BSGD_STRATIFIED: strata must divide N and cols_per_epoch");
         if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
             fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
-        if (tv && (P->tv_iters < 0 || !isfinite(P->lambda))) fail(BSGD_E_CONTRACT, "bad TV parameters");
+        if (tv && (P->tv_iters < 0 || !isfinite(P->lambda) || P->lambda < 0.0))
+            fail(BSGD_E_CONTRACT, "bad TV parameters (lambda must be finite and >= 0, tv_iters >= 0)");
+        if (!(P->mu0 > 0.0)) fail(BSGD_E_CONTRACT, "mu0 must be > 0");
+        Ordered order_(c, S(stream));
         cudaStream_t st = S(stream);
         const long long sb = (long long)c->s * c->bsize;
         // host or device buffers.  Host y / x are uploaded on a copy stream that overlaps the
@@ -1665,6 +1754,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                                                   : std::max(1, (int)floor((double)c->M * c->N / ((double)aM * gN) + 0.5)))
                               : 0;
         std::vector<double> mu_log(E);
+        const long long total = P->total_epochs > 0 ? (long long)P->total_epochs : (long long)c->epoch + E;
         bool downloaded = false;
         std::vector<int> rows(aM), cols(gN);
         for (int e = 0; e < E; ++e) {
@@ -1676,7 +1766,9 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             if (log && log->sel_rows) memcpy(log->sel_rows + (size_t)e * aM, rows.data(), sizeof(int) * aM);
             if (log && log->sel_cols && !sgd) memcpy(log->sel_cols + (size_t)e * gN, cols.data(), sizeof(int) * gN);
             std::vector<int> tiles;
-            const bool use_im = im && !(P->is_off_last_epochs > 0 && e >= E - P->is_off_last_epochs);
+            // "the last few iterations without importance sampling", counted in
+            // global epochs k against the planned total (the oracle's rule, oracle/bsgd.py)
+            const bool use_im = im && !(P->is_off_last_epochs > 0 && k > total - P->is_off_last_epochs);
             if (use_im) {   // Algo 2 line 5: one tile per (selected block, view) by weight
                 int V = 0;
                 for (int i : rows) V += (int)c->rows[i].size();
@@ -1906,8 +1998,11 @@ bsgd_status bsgd_set_state(bsgd_ctx c, int32_t what, int32_t index, const void* 
 
 bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, int32_t method, void* stream) {
     return guard(c, [&] {
-        if (!c || !x_owned || !(w >= 0.0) || iters < 0 || method < 0 || method > 1)
+        if (!c || !x_owned || !(w >= 0.0) || !isfinite(w) || iters < 0 || method < 0 || method > 1)
             fail(BSGD_E_CONTRACT, "bad arguments");
+        if (c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
+            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        Ordered order_(c, S(stream));
         c->tv_prox(x_owned, w, iters, S(stream), method);
     });
 }
@@ -1915,6 +2010,7 @@ bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, in
 bsgd_status bsgd_tv_value(bsgd_ctx c, const float* x_owned, double* out, void* stream) {
     return guard(c, [&] {
         if (!c || !x_owned || !out) fail(BSGD_E_CONTRACT, "bad arguments");
+        Ordered order_(c, S(stream));
         cudaStream_t st = S(stream);
         if (!c->d_tvv1) c->d_tvv1 = c->dnew<double>(1);
         c->tv_value(x_owned, c->d_tvv1, st);
@@ -1923,9 +2019,33 @@ bsgd_status bsgd_tv_value(bsgd_ctx c, const float* x_owned, double* out, void* s
     });
 }
 
+bsgd_status bsgd_allreduce_time(bsgd_ctx c, int64_t count, int32_t iters, void* stream, double* ms_out) {
+    return guard(c, [&] {
+        if (!c || !ms_out || iters < 1) fail(BSGD_E_CONTRACT, "bad arguments");
+        if (!c->coll || !c->pc) fail(BSGD_E_CONTRACT, "no collective path (world == 1)");
+        if (count < 1 || count > c->n_rays) fail(BSGD_E_CONTRACT, "count out of range");
+        cudaStream_t st = S(stream);
+        Ordered order_(c, st);
+        cudaEvent_t e0, e1;
+        BSGD_CUDA(cudaEventCreate(&e0));
+        BSGD_CUDA(cudaEventCreate(&e1));
+        c->allreduce_f(c->pc, (size_t)count, st);   // untimed: first use of the buffers
+        BSGD_CUDA(cudaEventRecord(e0, st));
+        for (int it = 0; it < iters; ++it) c->allreduce_f(c->pc, (size_t)count, st);
+        BSGD_CUDA(cudaEventRecord(e1, st));
+        BSGD_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        BSGD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = (double)ms / iters;
+    });
+}
+
 bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, double* out, void* stream) {
     return guard(c, [&] {
         if (!c || !out || iters < 1) fail(BSGD_E_CONTRACT, "bad arguments");
+        Ordered order_(c, S(stream));
         cudaStream_t st = S(stream);
         const long long sb = (long long)c->s * c->bsize;
         if (!c->pw_v) {

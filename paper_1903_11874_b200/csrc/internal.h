@@ -87,6 +87,9 @@ struct ProjLaunch {
     int rows_per_band;         // R: detector rows per band (band-major CTA order)
     int n_chunks;              // CTAs per (band, slot)
     int n_bands;               // max bands per block (grid.x = n_bands * n_slots * n_chunks)
+    int pair_chunks;           // > 0: the row-pair traversal applies (every view's v step is
+                               // parallel to z, every rect width a multiple of 32): CTAs per
+                               // (band, slot) of k_project5 (two detector rows per thread)
     const float* rproj;        // BP input (full length)
     float scale;               // BP scale (2 in Algo 1)
     int accumulate;            // FP: add into z instead of overwriting
@@ -143,8 +146,10 @@ struct ResLaunch {
 };
 constexpr int RES_GX = 64;   // max CTAs per view slot of k_residual
 void launch_residual(const ResLaunch& R, cudaStream_t st);
-// deterministic BP: S (power of two) from max|r| over n rays and V views; out += a / S
-void launch_det_scale(const float* r, long long n, int V, float scale, unsigned* mx, float* S, cudaStream_t st);
+// deterministic BP: S (power of two) from max|r| over n rays, V views and rpc (an upper bound on
+// the rays of one view crossing one cell); out += a / S
+void launch_det_scale(const float* r, long long n, int V, double rpc, float scale, unsigned* mx, float* S,
+                      cudaStream_t st);
 void launch_acc64_to_f32(const long long* a, float* out, long long n, const float* S, cudaStream_t st);
 
 void launch_zero_rows(double* normsq, const int* rows, int n, cudaStream_t st);

@@ -976,11 +976,12 @@ __global__ void __launch_bounds__(256) k_absmax(const float* r, long long n, uns
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);         // max is order-independent
 }
 
-// S = 2^e with e = floor(log2(2^62 / bound)), bound = V * 512 * scale * max|r| >= any per-cell
-// sum of |l w r| (at most ~16 rays per view cross a cell, each with length <= sqrt(3))
-__global__ void k_det_scale(const unsigned* mx, int V, float scale, float* S) {
+// S = 2^e with e = floor(log2(2^62 / bound)), bound = V * rpc * sqrt(3) * scale * max|r| >= any
+// per-cell sum of |l w r|: at most rpc rays of one view cross a cell (the host's geometric bound,
+// bsgd_ctx_s::rays_per_cell), each with a length <= sqrt(3)
+__global__ void k_det_scale(const unsigned* mx, int V, double rpc, float scale, float* S) {
     const double rmax = (double)__uint_as_float(*mx);
-    const double bound = (double)V * 512.0 * (double)scale * rmax;
+    const double bound = (double)V * rpc * 1.7320508075688772 * (double)scale * rmax;
     int e = 40;
     if (bound > 0.0 && isfinite(bound)) e = (int)floor(log2(4.611686018427388e18 / bound));
     e = max(-60, min(120, e));
@@ -994,11 +995,12 @@ __global__ void __launch_bounds__(256) k_acc64_to_f32(const long long* a, float*
         out[i] += (float)((double)a[i] * inv);
 }
 
-void launch_det_scale(const float* r, long long n, int V, float scale, unsigned* mx, float* S, cudaStream_t st) {
+void launch_det_scale(const float* r, long long n, int V, double rpc, float scale, unsigned* mx, float* S,
+                      cudaStream_t st) {
     BSGD_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
     k_absmax<<<grid_for(n, 8), 256, 0, st>>>(r, n, mx);
     BSGD_CUDA(cudaGetLastError());
-    k_det_scale<<<1, 1, 0, st>>>(mx, V, scale, S);
+    k_det_scale<<<1, 1, 0, st>>>(mx, V, rpc, scale, S);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
     note_launch();

@@ -366,3 +366,96 @@ def test_tv_prox_chambolle_closed_forms():
     b = rng.standard_normal((3, 6, 7))
     assert np.array_equal(ob.tv_prox(b, 0.0, method="chambolle"), b)
     assert np.max(np.abs(ob.tv_prox(b, 0.3, 30000, method="chambolle") - ob.tv_prox(b, 0.3, 5000))) < 1e-5
+
+
+# --------------------------------------------------------------------------- pins added in r02
+def test_im_draw_interval_kat_and_zero_tiles():
+    """Algo 2 line 5: the tile is drawn with probability q_t / sum q.  The
+    draw x = bounded(rnd(seed, 3, epoch, k), sum q) (the pinned sampler) selects the tile
+    whose half-open interval [c_{t-1}, c_t) of the cumulative weights contains x.  Checked
+    by hand-written interval tables (not a cumulative-sum loop): zero-weight tiles are never
+    drawn, and a draw on an interval's upper end belongs to the NEXT tile (an off-by-one in
+    the comparison, x <= c, fails here)."""
+    cases = [
+        # q, [(lo, hi, tile)] with x in [lo, hi) -> tile
+        ([1, 0, 1], [(0, 1, 0), (1, 2, 2)]),
+        ([0, 5, 0, 3], [(0, 5, 1), (5, 8, 3)]),
+        ([2, 3, 0, 0, 1], [(0, 2, 0), (2, 5, 1), (5, 6, 4)]),
+        ([0, 0, 7], [(0, 7, 2)]),
+    ]
+    for q, table in cases:
+        S = sum(q)
+        seen = set()
+        for k in range(400):
+            x = ob.bounded(ob.rnd(99, 3, 5, k), S)
+            want = [t for lo, hi, t in table if lo <= x < hi]
+            assert len(want) == 1
+            got = ob.im_draw(99, 5, k, np.array(q, np.uint32), False)
+            assert got == want[0], (q, x, got, want)
+            seen.add(got)
+        assert seen == {t for _, _, t in table}          # every non-zero tile occurs
+    # uniform (RAN) and zero-total weights: bounded(rnd, T)
+    for k in range(50):
+        u = ob.rnd(7, 3, 1, k)
+        assert ob.im_draw(7, 1, k, np.array([5, 0, 0, 0], np.uint32), True) == ob.bounded(u, 4)
+        assert ob.im_draw(7, 1, k, np.zeros(3, np.uint32), False) == ob.bounded(u, 3)
+
+
+def test_im_draw_frequencies_match_weights():
+    """The draw frequencies of Algo 2's tiles match q / sum q (chi-square, 20000 draws,
+    4 tiles of weights 1:2:3:10 plus a zero tile that must never occur)."""
+    q = np.array([1, 2, 0, 3, 10], np.uint32) * 4096
+    n = 20000
+    cnt = np.zeros(len(q))
+    for k in range(n):
+        cnt[ob.im_draw(2024, 7, k, q, False)] += 1
+    assert cnt[2] == 0
+    p = q / q.sum()
+    nz = p > 0
+    chi2 = float(np.sum((cnt[nz] - n * p[nz]) ** 2 / (n * p[nz])))
+    assert chi2 < 21.1                          # 3 dof, p ~ 1e-4
+
+
+def test_power_iteration_is_spectral_norm():
+    """sigma_max(A)^2 from the oracle's power iteration (it sets every mu = omega/sigma_max^2
+    of the parity suite) equals the squared spectral norm of the explicitly assembled A
+    (LAPACK SVD), on the paper's §III-A system and on a small cone-beam system."""
+    g, grid, A, x_true, y = sec3a_system(4, 4, noise=False)
+    P = Projector(g, grid)
+    ref = np.linalg.norm(A, 2) ** 2
+    got = ob.power_iteration(P, 300, seed=1)
+    assert abs(got - ref) <= 1e-8 * ref, (got, ref)
+    p = synth.scaled(synth.PRESETS["cfg3"], 12, n_views=10)
+    gc = p.geometry()
+    Pc = Projector(gc, BlockGrid(gc.dims, (1, 1, 2)))
+    Ac = Pc.dense()
+    refc = np.linalg.norm(Ac, 2) ** 2
+    gotc = ob.power_iteration(Pc, 400, seed=2)
+    assert abs(gotc - refc) <= 1e-6 * refc, (gotc, refc)
+
+
+def test_is_off_last_switches_to_algo1_in_the_final_global_epochs():
+    """"the last few iterations without importance sampling" (reading A11):
+    with is_off_last = L and total_epochs = K, epochs k > K - L (1-based, global) are plain
+    Algo 1 epochs.  An IM run of K epochs equals an IM run of K - L epochs continued by L
+    epochs of Algo 1 from the same state, and the IM epochs before differ from Algo 1."""
+    g, grid, A, x_true, y = sec3a_system(4, 4, noise=False)
+    s0 = np.linalg.norm(A, 2)
+    base = dict(seed=21, mu=0.5 / s0 ** 2, rows_per_epoch=1, cols_per_epoch=2)
+    K, L = 9, 3
+    o = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(im=True, is_off_last=L, total_epochs=K, **base),
+                      tiles=(2, 1))
+    for _ in range(K):
+        o.epoch()
+    assert all("tiles" in r for r in o.log[:K - L]) and all("tiles" not in r for r in o.log[K - L:])
+    ref = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(im=True, **base), tiles=(2, 1))
+    for _ in range(K - L):
+        ref.epoch()
+    ref.p = ob.Params(im=False, **base)                 # the same state, Algo 1 from here
+    for _ in range(L):
+        ref.epoch()
+    assert np.array_equal(ref.x, o.x)
+    plain = ob.OracleBSGD(g, grid.blocks, 4, y, ob.Params(**base))
+    for _ in range(K):
+        plain.epoch()
+    assert not np.allclose(plain.x, o.x)
