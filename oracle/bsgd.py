@@ -10,6 +10,7 @@ Parity pins: see tests/test_oracle_*.py and DESIGN.md §"Oracle pins".
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -483,3 +484,100 @@ def power_iteration(P: Projector, iters: int = 50, seed: int = 0) -> float:
         lam = float(np.linalg.norm(w))
         v = w / lam
     return lam
+
+
+class OracleBSGDLean:
+    """Algo 1 exactly as OracleBSGD runs it, with storage restricted
+    to what the epochs touch, for the 1024^3 configuration (where the dense state, N
+    full-length z^j and M x N g-hat blocks, would need ~130 GB in fp64):
+
+    * z^j_{I_i} is kept per touched (i, j) pair over the rays of I_i only (z^j is zero
+      elsewhere: line 5 writes only rows of selected row blocks, from z = 0, line 1);
+    * g-hat^i_{J_j} per touched pair (zero otherwise, line 1), optionally file-backed;
+    * line 7's r = y - sum_j z^j is evaluated on the selected row blocks, the only rows
+      where it changes; 1/2 |r|^2 is kept per row block (initially |y_{I_i}|^2, r = y);
+    * line 11's g = sum_i g-hat^i is formed for the selected J_j, the only blocks line 13
+      reads it for.
+    The sums run in the dense oracle's order (j ascending, i ascending, absent terms = the
+    +0.0 the dense oracle adds), so the state equals OracleBSGD's (pinned against it in
+    tests/test_oracle_bsgd.py).  Plain Algo 1 only (no IM / TV / auto-mu / SGD)."""
+
+    def __init__(self, geom, blocks, M, y32, params: Params, row_kind="random", row_seed=None,
+                 x_true32=None, ghat_dir=None):
+        p = params
+        if p.im or p.tv or p.auto_mu or p.sgd or p.strata:
+            raise ValueError("OracleBSGDLean runs plain Algo 1 only")
+        self.geom = geom
+        self.grid = BlockGrid(geom.dims, blocks)
+        self.P = Projector(geom, self.grid)
+        self.M, self.N, self.p = M, self.grid.N, p
+        rs = p.seed if row_seed is None else row_seed
+        self.rows = view_partition(geom.n_views, M, row_kind, rs)
+        self.y = y32                                  # fp32 data, converted per row block
+        self.x_true = x_true32                        # block-major fp32 (N, bsize) or None
+        self.x = np.zeros((self.N, self.grid.bsize))
+        self.z, self.ghat = {}, {}
+        self.ghat_dir = ghat_dir
+        self.scratch = np.zeros(geom.n_rays)          # full-length ray buffer for the C calls
+        self.rn2 = [float(np.sum(self._y(i) ** 2)) for i in range(M)]
+        self.mu = float(p.mu)
+        self.k = 0
+        self.log = []
+
+    def _y(self, i):
+        return np.asarray(self.y[self.P.rows_of(self.rows[i])], dtype=np.float64)
+
+    def _new_ghat(self, key):
+        if self.ghat_dir is None:
+            return np.zeros(self.grid.bsize)
+        fn = os.path.join(self.ghat_dir, f"ghat_{key[0]}_{key[1]}.f64")
+        return np.memmap(fn, dtype=np.float64, mode="w+", shape=(self.grid.bsize,))
+
+    def selection(self, e):
+        return (select(self.p.seed, 1, e, self.M, self.p.rows_per_epoch),
+                select(self.p.seed, 2, e, self.N, self.p.cols_per_epoch))
+
+    def epoch(self):
+        self.k += 1
+        e = self.k - 1
+        rows, cols = self.selection(e)
+        # lines 4-6: z^j_{I_i} = A_{I_i}^{J_j} x_{J_j}
+        for i in rows:
+            ids = self.P.rows_of(self.rows[i])
+            for j in cols:
+                self.P.fp(self.rows[i], j, self.x[j], proj=self.scratch)
+                self.z[(i, j)] = self.scratch[ids].copy()
+        # line 7 on the selected row blocks: r_{I_i} = y_{I_i} - sum_{j=1}^{N} z^j_{I_i}
+        r = {}
+        for i in rows:
+            acc = np.zeros(len(self.rows[i]) * self.geom.det_u * self.geom.det_v)
+            for j in range(self.N):
+                if (i, j) in self.z:
+                    acc += self.z[(i, j)]
+            r[i] = self._y(i) - acc
+            self.rn2[i] = float(r[i] @ r[i])
+        # lines 8-10: g-hat^i_{J_j} = 2 (A_{I_i}^{J_j})^T r_{I_i}
+        for i in rows:
+            ids = self.P.rows_of(self.rows[i])
+            self.scratch[ids] = r[i]
+            for j in cols:
+                bp = self.P.bp(self.rows[i], j, self.scratch)
+                if (i, j) not in self.ghat:
+                    self.ghat[(i, j)] = self._new_ghat((i, j))
+                self.ghat[(i, j)][:] = 2.0 * bp
+        # lines 11-14: g_{J_j} = sum_{i=1}^{M} g-hat^i_{J_j}; x_{J_j} += mu g_{J_j}
+        for j in cols:
+            g = np.zeros(self.grid.bsize)
+            for i in range(self.M):
+                if (i, j) in self.ghat:
+                    g += self.ghat[(i, j)]
+            self.x[j] += self.mu * g
+        rec = dict(k=self.k, rows=list(rows), cols=list(cols), mu=self.mu, obj=0.5 * float(np.sum(self.rn2)))
+        if self.x_true is not None:
+            s = 0.0
+            for j in range(self.N):
+                d = self.x[j] - self.x_true[j]
+                s += float(d @ d)
+            rec["rmse"] = math.sqrt(s / (self.N * self.grid.bsize))
+        self.log.append(rec)
+        return rec

@@ -459,3 +459,68 @@ def test_is_off_last_switches_to_algo1_in_the_final_global_epochs():
     for _ in range(K):
         plain.epoch()
     assert not np.allclose(plain.x, o.x)
+
+
+# --------------------------------------------------------------------------- lean Algo 1
+def test_lean_algo1_gd_closed_form_and_sag():
+    """OracleBSGDLean (the touched-pairs-only storage used for the 1024^3 fixture) pinned
+    like the dense oracle: alpha = gamma = 1 is GD (SVD closed form) and
+    gamma = 1 is SAG (independent dense SAG)."""
+    M, N = 4, 2
+    g, grid, A, x_true, y = sec3a_system(M, N)
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    mu = 0.5 / s[0] ** 2
+    o = ob.OracleBSGDLean(g, grid.blocks, M, y.astype(np.float32),
+                          ob.Params(seed=9, mu=mu, rows_per_epoch=M, cols_per_epoch=N))
+    y32 = y.astype(np.float32).astype(np.float64)
+    keep = s > 1e-10 * s[0]
+    uy = U.T @ y32
+    for k in range(1, 21):
+        rec = o.epoch()
+        xk = (Vt[keep].T * ((1 - (1 - 2 * mu * s[keep] ** 2) ** k) / s[keep])) @ uy[keep]
+        xg = global_of(grid, o.x)
+        assert np.max(np.abs(xg - xk)) <= 1e-10 * np.max(np.abs(xk))
+        xprev = (Vt[keep].T * ((1 - (1 - 2 * mu * s[keep] ** 2) ** (k - 1)) / s[keep])) @ uy[keep]
+        f = 0.5 * np.sum((y32 - A @ xprev) ** 2)          # r of epoch k = y - A x_{k-1}
+        assert abs(rec["obj"] - f) <= 1e-9 * f
+    # gamma = 1: SAG over the M row blocks
+    mu = 0.3 / s[0] ** 2
+    o = ob.OracleBSGDLean(g, grid.blocks, M, y.astype(np.float32),
+                          ob.Params(seed=4, mu=mu, rows_per_epoch=1, cols_per_epoch=N))
+    rows = [o.P.rows_of(r) for r in o.rows]
+    x = np.zeros(A.shape[1])
+    d = [np.zeros(A.shape[1]) for _ in range(M)]
+    for k in range(40):
+        (i,) = ob.select(4, 1, k, M, 1)
+        Ai = A[rows[i]]
+        d[i] = 2 * Ai.T @ (y32[rows[i]] - Ai @ x)
+        x = x + mu * sum(d)
+        o.epoch()
+        assert np.max(np.abs(global_of(grid, o.x) - x)) <= 1e-11 * max(1.0, np.max(np.abs(x)))
+
+
+@pytest.mark.parametrize("aM,gN", [(1, 1), (2, 3)])
+def test_lean_algo1_equals_dense_state(tmp_path, aM, gN):
+    """Stochastic schedules (stale z and g-hat in lines 7 and 11): the lean storage gives
+    the dense oracle's trajectory (selections identical; x, objective, RMSE to fp64
+    rounding of the reordered norms), with g-hat file-backed as for the 1024^3 run."""
+    p = synth.scaled(synth.PRESETS["cfg3"], K=24, n_views=30)
+    g = p.geometry()
+    vol = synth.rasterise(synth.ellipsoids_world("shepp3d", g.dims), g.dims).astype(np.float32)
+    grid = BlockGrid(g.dims, p.blocks)
+    P = Projector(g, grid)
+    y = np.zeros(g.n_rays)
+    xb = grid.to_blocks(vol.astype(np.float64))
+    for j in range(grid.N):
+        P.fp(np.arange(g.n_views), j, xb[j], proj=y, accumulate=True)
+    y32 = y.astype(np.float32)
+    prm = ob.Params(seed=6, mu=0.3 / 2.2e4, rows_per_epoch=aM, cols_per_epoch=gN)
+    d = ob.OracleBSGD(g, p.blocks, p.M, y32.astype(np.float64), prm, row_seed=3, x_true=xb)
+    lean = ob.OracleBSGDLean(g, p.blocks, p.M, y32, prm, row_seed=3, x_true32=grid.to_blocks(vol),
+                             ghat_dir=str(tmp_path))
+    for _ in range(25):
+        a, b = d.epoch(), lean.epoch()
+        assert (a["rows"], a["cols"]) == (b["rows"], b["cols"])
+        assert abs(a["obj"] - b["obj"]) <= 1e-12 * a["obj"]
+        assert abs(a["rmse"] - b["rmse"]) <= 1e-12 * a["rmse"]
+    assert np.max(np.abs(d.x - lean.x)) <= 1e-13 * np.max(np.abs(d.x))
