@@ -412,18 +412,6 @@ struct bsgd_ctx_s {
         L.max_rect_rays = maxr;
         L.rows_per_band = R;
         L.n_chunks = (R * maxw + 255) / 256;
-        // row pairs (k_project5): the two rays of one detector column in adjacent rows share
-        // their in-plane path when the detector's v step has no x / y component (circular
-        // orbits, A19), so one thread can carry both; the companion v2 launch keeps the one-ray
-        // warp decomposition, which requires warps that do not straddle detector rows
-        bool pairs = nv > 1 && mode != PROJ_COUNT;
-        for (int k = 0; pairs && k < ns; ++k) {
-            const double* q = &vecs[12 * (size_t)views[k]];
-            pairs = q[9] == 0.0 && q[10] == 0.0;
-        }
-        for (size_t e = 0; pairs && e < rc.size(); ++e)
-            pairs = ((rc[e].y - rc[e].x) % 32) == 0;
-        L.pair_chunks = pairs ? (((R + 1) / 2) * maxw + 255) / 256 : 0;
         L.n_bands = nbands;
         L.rproj = rproj;
         L.scale = scale;

@@ -87,9 +87,6 @@ struct ProjLaunch {
     int rows_per_band;         // R: detector rows per band (band-major CTA order)
     int n_chunks;              // CTAs per (band, slot)
     int n_bands;               // max bands per block (grid.x = n_bands * n_slots * n_chunks)
-    int pair_chunks;           // > 0: the row-pair traversal applies (every view's v step is
-                               // parallel to z, every rect width a multiple of 32): CTAs per
-                               // (band, slot) of k_project5 (two detector rows per thread)
     const float* rproj;        // BP input (full length)
     float scale;               // BP scale (2 in Algo 1)
     int accumulate;            // FP: add into z instead of overwriting

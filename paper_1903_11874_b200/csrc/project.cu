@@ -379,17 +379,6 @@ __device__ __forceinline__ void scatter3(bool in, unsigned m_or, unsigned m_and,
     }
 }
 
-// The two gathers of a slice without a z crossing (v4 fast path), predicated like gather3.
-__device__ __forceinline__ void gather2(unsigned rel, unsigned nk, const float* p0, const float* p1, float& v0,
-                                        float& v1) {
-    asm("{\n\t.reg .pred a;\n\t"
-        "setp.le.u32 a, %2, %3;\n\t"
-        "@a ld.global.nc.f32 %0, [%4];\n\t"
-        "@a ld.global.nc.f32 %1, [%5];\n\t}"
-        : "=f"(v0), "=f"(v1)
-        : "r"(rel), "r"(nk), "l"(p0), "l"(p1));
-}
-
 // D -= K on the 64-bit plane distance; returns ~0u when it borrows (a plane is crossed).
 __device__ __forceinline__ unsigned sub_borrow(unsigned long long& D, unsigned long long K) {
     unsigned m;
@@ -412,9 +401,30 @@ __device__ __forceinline__ unsigned long long plane_dist(double c, unsigned long
     return __double2ull_rn(rem * 18446744073709551616.0);
 }
 
-template <int MODE, bool FASTZ = false, int PFD = 0>
-__global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
-    const BlockDesc& B = L.blocks[blockIdx.z];
+// Per-lane state of the v3 / v6 slice walk (see the v3 comment above), set up at the warp's
+// first slice plane of each direction group.
+struct Walk3 {
+    const float* src;          // FP source (the padded copy of the frame's layout)
+    float* dst;                // BP target
+    unsigned long long DX, DZ, KX, KZ;   // 64-bit plane distances and per-slice decrements
+    float ikx, ikz;            // 1 / K (crossing point u = D / K)
+    float slo, shi_last;       // COUNT: in-slice entry / exit at the lane's first / last slice
+    float Ls;                  // voxel length per unit of main-axis travel
+    float wbp;                 // BP weight per unit of main-axis travel
+    float S;                   // PROJ_BPD scale
+    unsigned o;                // voxel offset at the current slice (wraps outside the range)
+    int sxo, pstep, rowstep;   // x step (+-1), z step (+-plane), slice step (+-row)
+    int k0, nk;                // the lane's slices [k0, k0 + nk] relative to its group's start
+    int jlo_p, jhi_p, jlo_n, jhi_n;   // warp-wide slice ranges of the two direction groups
+    bool pos, neg;             // the lane's ray walks the sy > 0 / sy < 0 group
+    bool inrect;
+    int view, iu, iv;
+};
+
+// Ray setup (a2) + v3 walk state.  Returns false when the v2 companion kernel takes this
+// warp (a steep ray, or a ray starting / ending inside the box) or the CTA has no rays.
+template <int MODE>
+__device__ __forceinline__ bool walk3_setup(const ProjLaunch& L, const BlockDesc& B, Walk3& W) {
     unsigned bid = blockIdx.x;
     const int chunk = (int)(bid % (unsigned)L.n_chunks);
     bid /= (unsigned)L.n_chunks;
@@ -423,16 +433,20 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
     const int r0 = max(rc.z, band * L.rows_per_band), r1 = min(rc.w, band * L.rows_per_band + L.rows_per_band);
     const int w = rc.y - rc.x;
-    if (r0 >= r1 || w <= 0) return;
+    if (r0 >= r1 || w <= 0) return false;
     const int nrect = (r1 - r0) * w;
     const int base = chunk * (int)blockDim.x;
-    if (base >= nrect) return;                       // uniform over the CTA
+    if (base >= nrect) return false;                 // uniform over the CTA
     const int tid = base + (int)threadIdx.x;
     const bool inrect = tid < nrect;
     const int iu = rc.x + (inrect ? tid % w : 0);
     const int iv = r0 + (inrect ? tid / w : 0);
     const int view = L.views[slot];
     const double* vec = L.g.vecs + 12 * (size_t)view;
+    W.inrect = inrect;
+    W.view = view;
+    W.iu = iu;
+    W.iv = iv;
 
     double a[3], b[3];
     make_ray(L.g, vec, iu, iv, a, b);
@@ -452,16 +466,16 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     // the v2 kernel takes this warp if a lane's ray is steep or starts / ends inside the box
     // (source or detector within the block: no face to exit through, the zero border would
     // not absorb the rest of the slice)
-    if (__any_sync(0xffffffffu, hit && (lane_steep(b) || amin == 0.0 || amax == 1.0))) return;
+    if (__any_sync(0xffffffffu, hit && (lane_steep(b) || amin == 0.0 || amax == 1.0))) return false;
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     float rs = 0.f;
-    const float S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
+    W.S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
     if (is_bp(MODE)) {
         if (inrect) rs = L.scale * L.rproj[((long long)view * L.g.nv + iv) * L.g.nu + iu];
         hit = hit && (rs != 0.f);
     }
-    const float* __restrict__ src = mainX ? B.xT : B.xN;
-    float* dst = mainX ? B.outT : B.outN;
+    W.src = mainX ? B.xT : B.xN;
+    W.dst = mainX ? B.outT : B.outN;
 
     // strides of the padded copy of the frame's layout (BlockDesc): rows carry PAD_X and
     // the block PAD_Z zero cells beyond every face the slice walk can step through
@@ -481,19 +495,24 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         j1 = cell_exit(a[1] + amax * b[1], sy, lo[1], hi[1]);
         if (sy * (j1 - j0) < 0) j1 = j0;              // rounding on a sub-slice chord
     }
-    const bool pos = hit && sy > 0, neg = hit && sy < 0;
-    const int jlo_p = __reduce_min_sync(0xffffffffu, pos ? j0 : INT_MAX);
-    const int jhi_p = __reduce_max_sync(0xffffffffu, pos ? j1 : INT_MIN);
-    const int jlo_n = __reduce_min_sync(0xffffffffu, neg ? j1 : INT_MAX);
-    const int jhi_n = __reduce_max_sync(0xffffffffu, neg ? j0 : INT_MIN);
-    unsigned long long DX = 0ull, DZ = 0ull, KX = 0ull, KZ = 0ull;
-    float ikx = 0.f, ikz = 0.f, slo = 0.f, shi_last = 1.f, Ls = 0.f;
-    unsigned o = 0u;   // wraps freely outside the lane's range; exact inside it
-    int sxo = 1, pstep = plane, k0 = INT_MAX, nk = 0;
+    W.pos = hit && sy > 0;
+    W.neg = hit && sy < 0;
+    W.jlo_p = __reduce_min_sync(0xffffffffu, W.pos ? j0 : INT_MAX);
+    W.jhi_p = __reduce_max_sync(0xffffffffu, W.pos ? j1 : INT_MIN);
+    W.jlo_n = __reduce_min_sync(0xffffffffu, W.neg ? j1 : INT_MAX);
+    W.jhi_n = __reduce_max_sync(0xffffffffu, W.neg ? j0 : INT_MIN);
+    W.DX = W.DZ = W.KX = W.KZ = 0ull;
+    W.ikx = W.ikz = W.slo = W.Ls = 0.f;
+    W.shi_last = 1.f;
+    W.o = 0u;
+    W.sxo = 1;
+    W.pstep = plane;
+    W.k0 = INT_MAX;
+    W.nk = 0;
     if (hit) {
-        const int jstart = sy > 0 ? jlo_p : jhi_n;
-        k0 = sy * (j0 - jstart);
-        nk = sy * (j1 - j0);
+        const int jstart = sy > 0 ? W.jlo_p : W.jhi_n;
+        W.k0 = sy * (j0 - jstart);
+        W.nk = sy * (j1 - j0);
         const double ys = (double)(sy > 0 ? jstart : jstart + 1);   // entry plane of jstart
         const double yin0 = (double)(sy > 0 ? j0 : j0 + 1);         // entry plane of slice j0
         const double yin1 = (double)(sy > 0 ? j1 : j1 + 1);
@@ -502,29 +521,50 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         const bool mx = kx < 0.0, mz = kz < 0.0;
         const double xr = a[0] + ap * b[0] - lo[0], zr = a[2] + ap * b[2] - lo[2];
         const double xm = mx ? -xr : xr, zm = mz ? -zr : zr;
-        KX = __double2ull_rn(fabs(kx) * TWO64);
-        KZ = __double2ull_rn(fabs(kz) * TWO64);
+        W.KX = __double2ull_rn(fabs(kx) * TWO64);
+        W.KZ = __double2ull_rn(fabs(kz) * TWO64);
         int cxm, czm;
-        DX = plane_dist(xm, KX, cxm);
-        DZ = plane_dist(zm, KZ, czm);
+        W.DX = plane_dist(xm, W.KX, cxm);
+        W.DZ = plane_dist(zm, W.KZ, czm);
         const int ix = mx ? -cxm - 1 : cxm;                         // frame cell relative to lo
         const int iz = mz ? -czm - 1 : czm;
         // K = 0 (ray parallel to that axis' planes): an infinite distance, never crossed
-        if (!KX) DX = ~0ull;
-        if (!KZ) DZ = ~0ull;
-        ikx = KX ? (float)(1.0 / (double)KX) : 0.f;
-        ikz = KZ ? (float)(1.0 / (double)KZ) : 0.f;
-        sxo = mx ? -1 : 1;
-        pstep = mz ? -plane : plane;
-        o = (unsigned)iz * (unsigned)plane + (unsigned)(jstart - lo[1]) * (unsigned)bdx + (unsigned)ix;
-        slo = (float)fmin(fmax((amin - (yin0 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
-        shi_last = (float)fmin(fmax((amax - (yin1 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
-        if (j1 == j0) shi_last = fmaxf(shi_last, slo);
-        Ls = (float)(blen * ainv1);
+        if (!W.KX) W.DX = ~0ull;
+        if (!W.KZ) W.DZ = ~0ull;
+        // (K = 0: D = 2^64 - 1 and 1/K := 2^-63, so D / K = 2 saturates to "no crossing")
+        W.ikx = W.KX ? (float)(1.0 / (double)W.KX) : 1.0842022e-19f;
+        W.ikz = W.KZ ? (float)(1.0 / (double)W.KZ) : 1.0842022e-19f;
+        W.sxo = mx ? -1 : 1;
+        W.pstep = mz ? -plane : plane;
+        W.o = (unsigned)iz * (unsigned)plane + (unsigned)(jstart - lo[1]) * (unsigned)bdx + (unsigned)ix;
+        W.slo = (float)fmin(fmax((amin - (yin0 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
+        W.shi_last = (float)fmin(fmax((amax - (yin1 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
+        if (j1 == j0) W.shi_last = fmaxf(W.shi_last, W.slo);
+        W.Ls = (float)(blen * ainv1);
     }
-    const int rowstep = sy * bdx;
+    W.rowstep = sy * bdx;
+    W.wbp = W.Ls * rs;   // BP weight per unit of main-axis travel
+    return true;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
+    const BlockDesc& B = L.blocks[blockIdx.z];
+    Walk3 W;
+    if (!walk3_setup<MODE>(L, B, W)) return;
+    const float* __restrict__ src = W.src;
+    float* dst = W.dst;
+    const bool inrect = W.inrect, pos = W.pos, neg = W.neg;
+    const int jlo_p = W.jlo_p, jhi_p = W.jhi_p, jlo_n = W.jlo_n, jhi_n = W.jhi_n;
+    unsigned long long DX = W.DX, DZ = W.DZ;
+    const unsigned long long KX = W.KX, KZ = W.KZ;
+    const float ikx = W.ikx, ikz = W.ikz, slo = W.slo, shi_last = W.shi_last, Ls = W.Ls, S = W.S;
+    unsigned o = W.o;
+    const int sxo = W.sxo, pstep = W.pstep, k0 = W.k0, nk = W.nk, rowstep = W.rowstep;
+    const int view = W.view, iu = W.iu, iv = W.iv;
+    const int slot = (int)((blockIdx.x / (unsigned)L.n_chunks) % (unsigned)L.n_slots);
     const unsigned nsxo = (unsigned)(-sxo), npstep = (unsigned)(-pstep);
-    const float wbp = Ls * rs;   // BP weight per unit of main-axis travel
+    const float wbp = W.wbp;
     double acc = 0.0;
     float acc32 = 0.f;
     float pv0 = 0.f, pv1 = 0.f, pv2 = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f;   // FP: previous slice
@@ -536,78 +576,10 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
         if (jl > jh) continue;                                      // warp-uniform
         const int nsl = jh - jl + 1;
         const int kb = (pass == 0 ? pos : neg) ? k0 : INT_MAX;      // this lane's slices [kb, kb + nk]
-        if (FASTZ) {
-            // v4: z-plane crossings are rare (|kz| <= 0.08 in the cone configs) and coherent
-            // across a warp (its lanes trace adjacent pixels of ONE detector row, at nearly the
-            // same height), so a slice in which no in-range lane crosses a z plane takes a
-            // two-segment body (one gather / reduction less, no z crossing point, no ordering
-            // of two crossings); the general three-segment body (the v3 arithmetic) runs only
-            // when some lane does (a warp-uniform branch).  FP keeps the fp32 partial sum of
-            // 16 slices, then adds it into the fp64 accumulator (an outer loop, not a select).
-            const unsigned sxu = (unsigned)sxo;
-            for (int kc = 0; kc < nsl; kc += 16) {
-                const int kend = min(kc + 16, nsl);
-                for (int k = kc; k < kend; ++k) {
-                    const unsigned rel = (unsigned)(k - kb);
-                    const bool in = rel <= (unsigned)nk;
-                    // D >= K without a crossing, so the saturated D / K is 1 up to rounding
-                    // (>= 1 - 2^-23); the FP's two segments then share one voxel (o1 = o)
-                    const float fx = __saturatef(__ull2float_rn(DX) * ikx);
-                    const unsigned bx = sub_borrow(DX, KX);
-                    const unsigned bz = sub_borrow(DZ, KZ);
-                    const unsigned dox = bx & sxu, doz = bz & (unsigned)pstep;
-                    const unsigned o1 = o + dox;
-                    if (MODE == PROJ_FP && true) {   // the previous slice's gathers
-                        const float an = fmaf(pl0, pv0, fmaf(pl1, pv1, acc32));
-                        acc32 = pin ? an : acc32;
-                    }
-                    if (__any_sync(0xffffffffu, in && bz != 0u)) {
-                        const float ux = bx ? fx : 1.f;
-                        const float uz = bz ? __saturatef(__ull2float_rn(DZ + KZ) * ikz) : 1.f;
-                        const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
-                        const float l0 = m1, l1 = m2 - m1, l2 = 1.f - m2;
-                        const unsigned oa = ux <= uz ? o1 : o + doz;
-                        const unsigned o2 = o1 + doz;
-                        if (MODE == PROJ_FP) {
-                            float v0, v1, v2;
-                            gather3(rel, (unsigned)nk, src + (int)o, src + (int)oa, src + (int)o2, v0, v1, v2);
-                            if (true) {
-                                if (in) acc32 = fmaf(l2, v2, acc32);   // rare: consumed at once
-                                pv0 = v0; pv1 = v1; pl0 = l0; pl1 = l1;
-                            } else if (in) {
-                                acc32 = fmaf(l0, v0, fmaf(l1, v1, fmaf(l2, v2, acc32)));
-                            }
-                        }
-                        if (is_bp(MODE))
-                            scatter3<MODE>(in, bx | bz, bx & bz, dst, (int)o, (int)oa, (int)o2, l0 * wbp, l1 * wbp,
-                                           l2 * wbp, S);
-                    } else {
-                        if (MODE == PROJ_FP) {
-                            float v0, v1;
-                            gather2(rel, (unsigned)nk, src + (int)o, src + (int)o1, v0, v1);
-                            if (true) {
-                                pv0 = v0; pv1 = v1; pl0 = fx; pl1 = 1.f - fx;
-                            } else if (in) {
-                                acc32 = fmaf(fx, v0, fmaf(1.f - fx, v1, acc32));
-                            }
-                        }
-                        if (is_bp(MODE) && in) {
-                            const float l0 = bx ? fx : 1.f;
-                            red_acc<MODE>(dst, (int)o, l0 * wbp, S);
-                            if (bx) red_acc<MODE>(dst, (int)o1, (1.f - l0) * wbp, S);
-                        }
-                    }
-                    if (MODE == PROJ_FP && true) pin = in;
-                    o = o1 + doz + (unsigned)rowstep;
-                }
-                if (MODE == PROJ_FP) {
-                    acc += (double)acc32;
-                    acc32 = 0.f;
-                }
-            }
-            continue;
-        }
-        for (int k = 0; k < nsl; ++k) {
+        for (int kc = 0; kc < nsl; kc += 16) {     // FP: fp32 sums of 16 slices -> fp64
+          const int ke = min(kc + 16, nsl);
+#pragma unroll 4
+          for (int k = kc; k < ke; ++k) {
             const int rel = k - kb;
             const bool in = (unsigned)rel <= (unsigned)nk;
             // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
@@ -634,8 +606,11 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
                 // (through an x or z face) the part outside the block lies in the cell just
                 // beyond that face, i.e. in the padded copy's zero border (FP reads 0, BP's
                 // reduction lands in the ignored border), so no entry/exit clamping
-                ux = bx ? __saturatef(fx) : 1.f;
-                uz = bz ? __saturatef(fz) : 1.f;
+                // FP: without a crossing D >= K, so the saturated D / K is 1 up to rounding
+                // (>= 1 - 2^-23) and the segments it separates share voxel o (no select
+                // needed); BP keeps the select (its rare reductions are keyed on the borrows)
+                ux = (MODE == PROJ_FP || bx) ? __saturatef(fx) : 1.f;
+                uz = (MODE == PROJ_FP || bz) ? __saturatef(fz) : 1.f;
                 const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
                 l0 = m1;
                 l1 = m2 - m1;
@@ -651,11 +626,6 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
                 // slice's values are consumed (two slices of loads in flight per warp)
                 float v0, v1, v2;
                 gather3((unsigned)rel, (unsigned)nk, src + (int)o, src + (int)o1, src + (int)o2, v0, v1, v2);
-                // L1 prefetch of the line this lane's ray reaches PFD slices ahead (x / z drift
-                // ignored: the warp's lanes cover that line's neighbours anyway), so those
-                // gathers hit L1 instead of waiting on L2
-                if (PFD > 0 && (unsigned)(rel + PFD) <= (unsigned)nk)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(src + (int)(o + (unsigned)(PFD * rowstep))));
                 const float an = fmaf(pl0, pv0, fmaf(pl1, pv1, fmaf(pl2, pv2, acc32)));
                 acc32 = pin ? an : acc32;            // the previous slice was in range
                 pv0 = v0; pv1 = v1; pv2 = v2;
@@ -672,10 +642,11 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
                 nvis += (unsigned)(in && l0 > 1e-6f) + (unsigned)(p1 && l1 > 1e-6f) + (unsigned)(p2 && l2 > 1e-6f);
             }
             o = o2 + (unsigned)rowstep;
-            if (MODE == PROJ_FP && (k & 15) == 15) {               // warp-uniform
-                acc += (double)acc32;
-                acc32 = 0.f;
-            }
+          }
+          if (MODE == PROJ_FP) {
+              acc += (double)acc32;
+              acc32 = 0.f;
+          }
         }
     }
     if (MODE == PROJ_FP && inrect) {
@@ -688,216 +659,6 @@ __global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
     if (MODE == PROJ_COUNT && L.visits) {
         unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
         if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits + (size_t)blockIdx.z * L.n_slots + slot, (unsigned long long)s);
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// v5: two detector rows per thread.  When the detector's v step has no x / y component
-// (circular orbits, reading A19: v = pitch_v (0, 0, 1)), the rays of one detector column
-// in rows iv and iv + 1 have the same source, the same in-plane direction (b_x, b_y) and so
-// the same in-plane path: the same main axis, slice direction, x-plane crossings and x cell
-// at every slice.  One thread carries both rays: the x stepping (64-bit plane distance,
-// crossing point, x step) is computed once per slice for the pair, the z stepping and the
-// three-segment body stay per ray (the v3 arithmetic, bit for bit).  Each ray issues its
-// own gathers, so a warp keeps twice the loads in flight per slice.
-// The warp / skip decomposition is v3's per detector row (32 adjacent columns of one row;
-// the host uses v5 only when no rect width straddles warps), so the v2 companion launch
-// with the one-ray mapping takes exactly the 32-ray row groups v5 leaves.
-template <int MODE>
-__global__ void __launch_bounds__(256, 3) k_project5(const ProjLaunch L) {
-    const BlockDesc& B = L.blocks[blockIdx.z];
-    unsigned bid = blockIdx.x;
-    const int chunk = (int)(bid % (unsigned)L.pair_chunks);
-    bid /= (unsigned)L.pair_chunks;
-    const int slot = (int)(bid % (unsigned)L.n_slots);
-    const int band = B.band_lo + (int)(bid / (unsigned)L.n_slots);
-    const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
-    const int r0 = max(rc.z, band * L.rows_per_band), r1 = min(rc.w, band * L.rows_per_band + L.rows_per_band);
-    const int w = rc.y - rc.x;
-    if (r0 >= r1 || w <= 0) return;
-    const int npairs = (r1 - r0 + 1) / 2;
-    const int nrect = npairs * w;
-    const int base = chunk * (int)blockDim.x;
-    if (base >= nrect) return;                       // uniform over the CTA
-    const int tid = base + (int)threadIdx.x;
-    const bool inrect = tid < nrect;
-    const int iu = rc.x + (inrect ? tid % w : 0);
-    const int ivA = r0 + 2 * (inrect ? tid / w : 0);
-    const bool hasB = ivA + 1 < r1;
-    const int view = L.views[slot];
-    const double* vec = L.g.vecs + 12 * (size_t)view;
-
-    double a[2][3], b[2][3];
-    make_ray(L.g, vec, iu, ivA, a[0], b[0]);
-    make_ray(L.g, vec, iu, hasB ? ivA + 1 : ivA, a[1], b[1]);
-    const bool mainX = warp_main_x(b[0], inrect);    // = v3's choice for either row's warp
-    int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
-    if (mainX) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            double t = a[r][0]; a[r][0] = a[r][1]; a[r][1] = t;
-            t = b[r][0]; b[r][0] = b[r][1]; b[r][1] = t;
-        }
-        int q = lo[0]; lo[0] = lo[1]; lo[1] = q;
-        q = hi[0]; hi[0] = hi[1]; hi[1] = q;
-    }
-    double inv[2][3], amin[2], amax[2];
-    bool hit[2], take[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) inv[r][c] = (b[r][c] != 0.0) ? 1.0 / b[r][c] : 0.0;
-        const bool valid = inrect && (r == 0 || hasB);
-        hit[r] = valid && clip(a[r], b[r], inv[r], lo, hi, amin[r], amax[r]);
-        // v3's skip rule per 32-ray row group: the v2 companion takes the group
-        const bool skip = __any_sync(0xffffffffu, hit[r] && (lane_steep(b[r]) || amin[r] == 0.0 || amax[r] == 1.0));
-        take[r] = valid && !skip;
-        hit[r] = hit[r] && !skip;
-    }
-    if (!__any_sync(0xffffffffu, take[0] || take[1])) return;
-    float rs[2] = {0.f, 0.f};
-    const float S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
-    if (is_bp(MODE)) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            if (take[r]) rs[r] = L.scale * L.rproj[((long long)view * L.g.nv + ivA + r) * L.g.nu + iu];
-            hit[r] = hit[r] && (rs[r] != 0.f);
-        }
-    }
-    const float* __restrict__ src = mainX ? B.xT : B.xN;
-    float* dst = mainX ? B.outT : B.outN;
-    const int bdx = mainX ? B.rowT : B.rowN;
-    const int plane = mainX ? B.planeT : B.planeN;
-    // the in-plane direction, and so sy, |1/b_1| and the x stepping, are the pair's
-    const int sy = (b[0][1] > 0.0) ? 1 : -1;
-    const double ainv1 = fabs(inv[0][1]);
-    const double TWO64 = 18446744073709551616.0;
-    int j0[2] = {0, 0}, j1[2] = {-1, -1};
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-        if (hit[r]) {
-            j0[r] = cell_enter(a[r][1] + amin[r] * b[r][1], sy, lo[1], hi[1]);
-            j1[r] = cell_exit(a[r][1] + amax[r] * b[r][1], sy, lo[1], hi[1]);
-            if (sy * (j1[r] - j0[r]) < 0) j1[r] = j0[r];
-        }
-    const bool pos0 = hit[0] && sy > 0, pos1 = hit[1] && sy > 0;
-    const bool neg0 = hit[0] && sy < 0, neg1 = hit[1] && sy < 0;
-    const int jlo_p = __reduce_min_sync(0xffffffffu, min(pos0 ? j0[0] : INT_MAX, pos1 ? j0[1] : INT_MAX));
-    const int jhi_p = __reduce_max_sync(0xffffffffu, max(pos0 ? j1[0] : INT_MIN, pos1 ? j1[1] : INT_MIN));
-    const int jlo_n = __reduce_min_sync(0xffffffffu, min(neg0 ? j1[0] : INT_MAX, neg1 ? j1[1] : INT_MAX));
-    const int jhi_n = __reduce_max_sync(0xffffffffu, max(neg0 ? j0[0] : INT_MIN, neg1 ? j0[1] : INT_MIN));
-    const bool anyhit = hit[0] || hit[1];
-    const int jstart = sy > 0 ? jlo_p : jhi_n;
-    // shared x stepping, set up at jstart's entry plane from ray 0 (ray 1 is identical in x)
-    unsigned long long DX = 0ull, KX = 0ull;
-    float ikx = 0.f;
-    int sxo = 1, ix = 0;
-    if (anyhit) {
-        const double ys = (double)(sy > 0 ? jstart : jstart + 1);
-        const double ap = (ys - a[0][1]) * inv[0][1];
-        const double kx = b[0][0] * ainv1;
-        const bool mx = kx < 0.0;
-        const double xr = a[0][0] + ap * b[0][0] - lo[0];
-        KX = __double2ull_rn(fabs(kx) * TWO64);
-        int cxm;
-        DX = plane_dist(mx ? -xr : xr, KX, cxm);
-        ix = mx ? -cxm - 1 : cxm;
-        if (!KX) DX = ~0ull;
-        ikx = KX ? (float)(1.0 / (double)KX) : 0.f;
-        sxo = mx ? -1 : 1;
-    }
-    unsigned long long DZ[2] = {0ull, 0ull}, KZ[2] = {0ull, 0ull};
-    float ikz[2] = {0.f, 0.f}, Ls[2] = {0.f, 0.f};
-    unsigned o[2] = {0u, 0u};
-    int pstep[2] = {plane, plane}, k0[2] = {INT_MAX, INT_MAX}, nk[2] = {0, 0};
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-        if (hit[r]) {
-            k0[r] = sy * (j0[r] - jstart);
-            nk[r] = sy * (j1[r] - j0[r]);
-            const double ys = (double)(sy > 0 ? jstart : jstart + 1);
-            const double ap = (ys - a[r][1]) * inv[r][1];
-            const double kz = b[r][2] * ainv1;
-            const bool mz = kz < 0.0;
-            const double zr = a[r][2] + ap * b[r][2] - lo[2];
-            KZ[r] = __double2ull_rn(fabs(kz) * TWO64);
-            int czm;
-            DZ[r] = plane_dist(mz ? -zr : zr, KZ[r], czm);
-            const int iz = mz ? -czm - 1 : czm;
-            if (!KZ[r]) DZ[r] = ~0ull;
-            ikz[r] = KZ[r] ? (float)(1.0 / (double)KZ[r]) : 0.f;
-            pstep[r] = mz ? -plane : plane;
-            o[r] = (unsigned)iz * (unsigned)plane + (unsigned)(jstart - lo[1]) * (unsigned)bdx + (unsigned)ix;
-            const double blen = sqrt(b[r][0] * b[r][0] + b[r][1] * b[r][1] + b[r][2] * b[r][2]);
-            Ls[r] = (float)(blen * ainv1);
-        }
-    const int rowstep = sy * bdx;
-    const unsigned nsxo = (unsigned)(-sxo);
-    const unsigned npstep[2] = {(unsigned)(-pstep[0]), (unsigned)(-pstep[1])};
-    const float wbp[2] = {Ls[0] * rs[0], Ls[1] * rs[1]};
-    double acc[2] = {0.0, 0.0};
-    float acc32[2] = {0.f, 0.f};
-    float pv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}}, pl[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-    bool pin[2] = {false, false};
-    const int jl = sy > 0 ? jlo_p : jlo_n, jh = sy > 0 ? jhi_p : jhi_n;
-    // (one direction group per warp: sy is the pair's, and a warp whose lanes disagree on sy
-    // walks each group in its own pass, as in v3)
-    for (int pass = 0; pass < 2; ++pass) {
-        const int pjl = pass == 0 ? jlo_p : jlo_n, pjh = pass == 0 ? jhi_p : jhi_n;
-        if (pjl > pjh) continue;                                    // warp-uniform
-        const int nsl = pjh - pjl + 1;
-        const bool mine = pass == 0 ? sy > 0 : sy < 0;
-        const int kb0 = (mine && hit[0]) ? k0[0] : INT_MAX, kb1 = (mine && hit[1]) ? k0[1] : INT_MAX;
-        for (int k = 0; k < nsl; ++k) {
-            const float fx = __ull2float_rn(DX) * ikx;
-            const unsigned bx = sub_borrow(DX, KX);
-            const float ux = bx ? __saturatef(fx) : 1.f;
-            const unsigned dox = bx * nsxo;
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int rel = k - (r == 0 ? kb0 : kb1);
-                const bool in = (unsigned)rel <= (unsigned)nk[r];
-                const float fz = __ull2float_rn(DZ[r]) * ikz[r];
-                const unsigned bz = sub_borrow(DZ[r], KZ[r]);
-                const float uz = bz ? __saturatef(fz) : 1.f;
-                const float m1 = fminf(ux, uz), m2 = fmaxf(ux, uz);
-                const float l0 = m1, l1 = m2 - m1, l2 = 1.f - m2;
-                const unsigned doz = bz * npstep[r];
-                const unsigned o1 = o[r] + (ux <= uz ? dox : doz);
-                const unsigned o2 = doz + (dox + o[r]);
-                if (MODE == PROJ_FP) {
-                    float v0, v1, v2;
-                    gather3((unsigned)rel, (unsigned)nk[r], src + (int)o[r], src + (int)o1, src + (int)o2, v0, v1, v2);
-                    const float an = fmaf(pl[r][0], pv[r][0], fmaf(pl[r][1], pv[r][1], fmaf(pl[r][2], pv[r][2], acc32[r])));
-                    acc32[r] = pin[r] ? an : acc32[r];
-                    pv[r][0] = v0; pv[r][1] = v1; pv[r][2] = v2;
-                    pl[r][0] = l0; pl[r][1] = l1; pl[r][2] = l2;
-                    pin[r] = in;
-                }
-                if (is_bp(MODE))
-                    scatter3<MODE>(in, bx | bz, bx & bz, dst, (int)o[r], (int)o1, (int)o2, l0 * wbp[r], l1 * wbp[r],
-                                   l2 * wbp[r], S);
-                o[r] = o2 + (unsigned)rowstep;
-            }
-            if (MODE == PROJ_FP && (k & 15) == 15) {                // warp-uniform
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    acc[r] += (double)acc32[r];
-                    acc32[r] = 0.f;
-                }
-            }
-        }
-    }
-    (void)jl; (void)jh;
-    if (MODE == PROJ_FP) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            if (!take[r]) continue;
-            if (pin[r]) acc32[r] = fmaf(pl[r][0], pv[r][0], fmaf(pl[r][1], pv[r][1], fmaf(pl[r][2], pv[r][2], acc32[r])));
-            double v = (acc[r] + (double)acc32[r]) * (double)Ls[r];
-            float* zp = zaddr(B, L.g, view, iu, ivA + r);
-            *zp = L.accumulate ? (*zp + (float)v) : (float)v;
-        }
     }
 }
 
@@ -945,7 +706,7 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
     if (L.n_slots == 0 || L.n_blocks == 0 || L.max_rect_rays == 0) return;
     static const int version = [] {
         const char* e = getenv("BSGD_PROJECTOR");
-        return e ? atoi(e) : 5;
+        return e ? atoi(e) : 3;
     }();
     const dim3 grid((unsigned)((long long)L.n_bands * L.n_slots * L.n_chunks), 1, (unsigned)L.n_blocks);
     if (grid.x == 0) return;
@@ -958,33 +719,12 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
         note_launch();
         return;
     }
-    // v4 (default): the v3 traversal with the two-segment fast path for slices without a z
-    // crossing (FASTZ); v3 (BSGD_PROJECTOR=3): the three-segment body throughout.  Then the
-    // v2 traversal for the warps either skipped (same launch geometry, same predicate).
-    // The COUNT traversal (visit table) always takes the v3 body (exact clamps).
-    if (version >= 5 && L.pair_chunks > 0 && mode != PROJ_COUNT) {
-        const dim3 g5((unsigned)((long long)L.n_bands * L.n_slots * L.pair_chunks), 1, (unsigned)L.n_blocks);
-        if (mode == PROJ_FP) k_project5<PROJ_FP><<<g5, 256, 0, st>>>(L);
-        else if (mode == PROJ_BP) k_project5<PROJ_BP><<<g5, 256, 0, st>>>(L);
-        else k_project5<PROJ_BPD><<<g5, 256, 0, st>>>(L);
-    } else if (version >= 4 && mode != PROJ_COUNT) {
-        static const int pfd = [] {
-            const char* e = getenv("BSGD_FP_PREFETCH");
-            return e ? atoi(e) : 0;
-        }();
-        if (mode == PROJ_FP && pfd == 4) k_project3<PROJ_FP, false, 4><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_FP && pfd == 8) k_project3<PROJ_FP, false, 8><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_FP && pfd == 16) k_project3<PROJ_FP, false, 16><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_FP && pfd == -1) k_project3<PROJ_FP, true><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_FP) k_project3<PROJ_FP><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_BP) k_project3<PROJ_BP, true><<<grid, 256, 0, st>>>(L);
-        else k_project3<PROJ_BPD, true><<<grid, 256, 0, st>>>(L);
-    } else {
-        if (mode == PROJ_FP) k_project3<PROJ_FP><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_BP) k_project3<PROJ_BP><<<grid, 256, 0, st>>>(L);
-        else if (mode == PROJ_BPD) k_project3<PROJ_BPD><<<grid, 256, 0, st>>>(L);
-        else k_project3<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
-    }
+    // v3 (default), then the v2 traversal for the warps v3 skipped (same launch geometry,
+    // same predicate)
+    if (mode == PROJ_FP) k_project3<PROJ_FP><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BP) k_project3<PROJ_BP><<<grid, 256, 0, st>>>(L);
+    else if (mode == PROJ_BPD) k_project3<PROJ_BPD><<<grid, 256, 0, st>>>(L);
+    else k_project3<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
     if (mode == PROJ_FP) k_project2<PROJ_FP, true><<<grid, 256, 0, st>>>(L);

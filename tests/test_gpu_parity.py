@@ -98,14 +98,21 @@ def _fp_bp_check(bs, g, blocks, M, views, block_ids, rects=None, seed=0):
     ("cfg1", 90, None),        # all views, all 2x2 blocks (ties at 0/90 degrees)
     ("cfg2", 48, None),        # 48 of 360 views, all 16 blocks
     ("cfg3", 24, None),        # 24 of 360 views, all 8 z-slabs
-    ("cfg4", 3, [0, 3]),       # full size, sampled views, edge + inner slab
-    ("cfg5", 2, [0, 4]),       # full size, sampled views, edge + inner slab
+    ("cfg4", 4, [0, 3]),       # full size, sampled views, edge + inner slab
+    ("cfg5", 4, [0, 4]),       # full size, sampled views, edge + inner slab
 ])
 def test_operator_parity(bs, name, nviews, blocks_sel):
     p = synth.PRESETS[name]
     g = p.geometry()
-    views = np.linspace(0, g.n_views - 1, nviews).round().astype(int)
-    views = np.unique(np.concatenate([views, [0, g.n_views // 4]]))[:max(nviews, 2)]
+    if name in ("cfg4", "cfg5"):
+        # full size: an axis-aligned view (ties on voxel planes), the two diagonal views
+        # (45 / 135 deg: the most visits per ray, the main-axis switch inside the fan and the
+        # steep-ray companion kernel) and one seeded random view
+        rv = int(np.random.default_rng(7 + p.dims[0]).integers(0, g.n_views))
+        views = np.array(sorted({0, g.n_views // 8, 3 * g.n_views // 8, rv}))
+    else:
+        views = np.linspace(0, g.n_views - 1, nviews).round().astype(int)
+        views = np.unique(np.concatenate([views, [0, g.n_views // 4]]))[:max(nviews, 2)]
     bsel = list(range(p.N)) if blocks_sel is None else blocks_sel
     wf, wb = _fp_bp_check(bs, g, p.blocks, p.M, views, bsel)
     print(f"{name}: worst FP |d|/tol {wf:.3g}, worst BP |d|/tol {wb:.3g}")
@@ -391,8 +398,11 @@ def test_full_size_engine_step_cfg5(bs):
     xd = torch.from_numpy(x0).cuda()
     ctx.reset(yd)
     ctx.step(yd, xd, [0], list(range(8)), mu=0.0)
-    sv = [views[0], views[len(views) // 2]]
-    rects = [(0, 1024, 300, 302), (0, 1024, 700, 701)]
+    # two random views of the row block and its views nearest 45 and 135 deg (oblique:
+    # the most visits per ray, steep-ray companion warps near the fan's edges)
+    near = [int(min(views, key=lambda v: abs(v - a))) for a in (g.n_views // 8, 3 * g.n_views // 8)]
+    sv = sorted({views[0], views[len(views) // 2], *near})
+    rects = [(0, 1024, 37, 38), (0, 1024, 300, 302), (0, 1024, 511, 513), (0, 1024, 700, 701), (0, 1024, 990, 991)]
     xb = x0.reshape(8, -1)
     for j in range(8):
         zg = ctx.get_state(0, j).astype(np.float64)

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of projector variants on the cfg5 bench (device time only); run under gpurun.
-# usage: tools/ab_proj.sh TAG "ENV1" "ENV2" ...
+# usage: tools/ab_proj.sh TAG "ENV1" "ENV2" ...   (each ENV: space-separated VAR=value list)
 tag=$1; shift
 mkdir -p gpurun_out
 for e in "$@"; do
