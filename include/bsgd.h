@@ -260,7 +260,10 @@ typedef struct {
 /* Run params->epochs epochs of BSGD (Algo 1) or its variants selected by
  * flags, sampling with the counter RNG from params->seed.  y, x_owned, x_true
  * may be host or device pointers (host: copied in / x copied back).
- * Synchronises `stream` before returning (the log is host memory).           */
+ * Synchronises `stream` before returning (the log is host memory).
+ * Errors: BSGD_E_CONTRACT for bad parameters (unknown flags, mu0 <= 0, negative lambda or
+ * tv_iters with BSGD_TV, bad strata); BSGD_E_PARTITION for BSGD_TV when world > 1 and a
+ * rank would own part of a z-layer of the block grid (see bsgd_tv_prox).              */
 bsgd_status bsgd_run(bsgd_ctx ctx, const float* y, float* x_owned, const float* x_true,
                      const bsgd_run_params* params, bsgd_run_log* log, void* stream);
 
@@ -290,22 +293,35 @@ bsgd_status bsgd_power_iteration(bsgd_ctx ctx, int32_t iters, uint64_t seed, dou
  * BSGD_FORCE_NCCL), count < 1 or count > n_rays, iters < 1.                      */
 bsgd_status bsgd_allreduce_time(bsgd_ctx ctx, int64_t count, int32_t iters, void* stream, double* ms_out);
 
+/* Residual exchange accounting (the ALLREDUCE of PAPER.md:99), cumulative since
+ * bsgd_create, host-side counters of what this rank SENT for line 7 of the epochs it ran:
+ * band mode (world > 1, default): the partial projection sums on the detector rows where this
+ * rank's band (the rows its blocks project into) overlaps a peer's, one message per (peer,
+ * view); full mode (environment BSGD_EXCHANGE=full): the ring allreduce's 2 (G-1)/G of the
+ * selected rows' buffer per epoch.  *band_mode (nullable) = 1 in band mode.  In band mode the
+ * residual r is formed on this rank's band rows only (bsgd_get_state's r is valid there;
+ * rows no band covers keep r = y).  Errors: BSGD_E_CONTRACT for NULL outputs.            */
+bsgd_status bsgd_comm_stats(bsgd_ctx ctx, uint64_t* bytes_sent, uint64_t* messages, int32_t* band_mode);
+
 /* TV proximal step (Algo 4 line 16; TV of Eq. 5-6):
  * x_owned <- argmin_t 1/2 ||t - x_owned||^2 + w TV(t), by `iters` cold-start FGP iterations
  * on the dual (reading A16; the same call bsgd_run makes every tv_period epochs, with
  * w = mu lambda).  TV is the isotropic backward-difference TV of Eq. 6 over the WHOLE volume
  * (zero difference at index 0).  x_owned: device, this rank's owned blocks, block-major (the
  * layout of bsgd_run's x_owned), modified in place; enqueued on `stream`.  Collective when
- * world > 1 (z-slab halo planes by ncclSend/Recv; every rank calls it).  w = 0 or iters = 0
+ * world > 1 (z-plane halos by ncclSend/Recv; every rank calls it).  w = 0 or iters = 0
  * leaves x unchanged.  method: 0 = FGP (default of bsgd_run), 1 = Chambolle 2004 (tau = 1/8
  * in 2D, 1/12 in 3D; SURVEY §8c step 7's flag; bsgd_run with BSGD_TV_CHAMBOLLE).
  * Errors: BSGD_E_CONTRACT for NULL x, w < 0 or not finite, iters < 0 or an unknown method;
- * BSGD_E_PARTITION when world > 1 and the block grid is not z-slabs (1, 1, N).          */
+ * BSGD_E_PARTITION when world > 1 and a rank would own part of a z-layer of the block grid
+ * (N / world not a multiple of bx * by): the stencil's only cross-rank neighbours must lie
+ * in z.  z-slabs (1, 1, N) always qualify; so do the paper's 2x2x2 cubes at world = 2.    */
 bsgd_status bsgd_tv_prox(bsgd_ctx ctx, float* x_owned, double w, int32_t iters, int32_t method,
                          void* stream);
 /* TV(x) = sum over voxels of |grad x|_2 (isotropic backward differences, zero at index 0;
  * Eq. 6) of the whole volume: x_owned device (owned blocks, block-major),
- * *out host.  Collective when world > 1 (one halo plane + a 1-double allreduce).  Synchronous. */
+ * *out host.  Collective when world > 1 (one halo plane + a 1-double allreduce).  Synchronous.
+ * Errors: as bsgd_tv_prox (BSGD_E_PARTITION for partial z-layers per rank).               */
 bsgd_status bsgd_tv_value(bsgd_ctx ctx, const float* x_owned, double* out, void* stream);
 
 /* Comparison solvers on the same operators (the methods the paper

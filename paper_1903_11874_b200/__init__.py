@@ -142,6 +142,7 @@ SIGS = {
     "bsgd_set_state": ([_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_allreduce_time": ([_ctx, C.c_int64, C.c_int32, C.c_void_p, P(C.c_double)], C.c_int),
+    "bsgd_comm_stats": ([_ctx, P(C.c_uint64), P(C.c_uint64), P(C.c_int32)], C.c_int),
     "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "bsgd_tv_value": ([_ctx, C.c_void_p, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
@@ -495,6 +496,13 @@ class Context:
         out = C.c_double()
         self._c(_lib.bsgd_allreduce_time(self.h, int(count), int(iters), _stream(stream), C.byref(out)))
         return out.value
+
+    def comm_stats(self) -> dict:
+        """Residual-exchange bytes / messages this rank sent so far and the mode
+        (bsgd_comm_stats)."""
+        b, m, band = C.c_uint64(), C.c_uint64(), C.c_int32()
+        self._c(_lib.bsgd_comm_stats(self.h, C.byref(b), C.byref(m), C.byref(band)))
+        return {"bytes_sent": int(b.value), "messages": int(m.value), "mode": "band" if band.value else "full"}
 
     def power_iteration(self, iters=30, seed=0, stream=None) -> float:
         out = C.c_double()

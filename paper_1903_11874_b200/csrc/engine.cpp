@@ -88,6 +88,18 @@ struct bsgd_ctx_s {
     bsgd_vgroup vg = nullptr;   // virtual rank: collectives through the in-process group
     void* vg_tmp = nullptr;
     double* d_rpart = nullptr;   // k_residual per-CTA partials of ||r||^2
+    // N2 band exchange (world > 1).  Rank h's partial sum p_h = sum of its owned
+    // z^j is zero outside the detector rows its blocks project into (band_h(view): the union
+    // of the footprint rows of its blocks), and its BP reads r only there.  So instead of an
+    // allreduce of the whole detector, each rank receives the peers' p on the rows where their
+    // bands overlap its own and forms r on its band rows only (r is then valid on the band;
+    // rows no band covers stay r = y).  ||r_I||^2: each row counted by the lowest rank whose
+    // band covers it, one M-double allreduce.  BSGD_EXCHANGE=full keeps the full allreduce.
+    bool band = false;
+    std::vector<int2> bands;         // [world][n_views] (lo, hi)
+    std::vector<float*> rbuf;        // [world] peers' partial sums, compact like pc (overlap rows)
+    double* d_npart = nullptr;       // [M] this rank's partial ||r_I||^2
+    unsigned long long comm_bytes = 0, comm_msgs = 0;   // residual exchange, sent by this rank
     float* gap_proj = nullptr;   // BSGD_LOG_TRUE_OBJ: A x (full length)
     float* tvv_halo = nullptr;   // tv_value: x plane z0-1 from the previous rank
     double* d_tvv = nullptr;     // per-epoch TV(x) (BSGD_LOG_TRUE_OBJ with log->tv)
@@ -119,7 +131,7 @@ struct bsgd_ctx_s {
     float *accN = nullptr, *accT = nullptr, *pc = nullptr;
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
-          *tv_q2 = nullptr, *tv_hp = nullptr;
+          *tv_q2 = nullptr, *tv_hp = nullptr, *tv_pk = nullptr;
     float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
@@ -487,6 +499,106 @@ struct bsgd_ctx_s {
         BSGD_CUDA(cudaMemcpyAsync(p, vg_tmp, bytes, cudaMemcpyDeviceToDevice, st));
     }
 
+    // Rows [lo, hi) of the detector that owned blocks [h s, (h+1) s) project into, per view.
+    void compute_bands() {
+        bands.assign((size_t)world * n_views, make_int2(0, 0));
+        for (int h = 0; h < world; ++h)
+            for (int v = 0; v < n_views; ++v) {
+                int lo_ = nv, hi_ = 0;
+                for (int b = 0; b < s; ++b) {
+                    int lo[3], hi[3];
+                    box(h * s + b, lo, hi);
+                    const int4 f = footprint(lo, hi, v);
+                    if (f.x >= f.y || f.z >= f.w) continue;
+                    lo_ = std::min(lo_, f.z);
+                    hi_ = std::max(hi_, f.w);
+                }
+                bands[(size_t)h * n_views + v] = lo_ < hi_ ? make_int2(lo_, hi_) : make_int2(0, 0);
+            }
+    }
+    int2 band_of(int h, int v) const { return bands[(size_t)h * n_views + v]; }
+    static int2 isect(int2 a, int2 b) { return make_int2(std::max(a.x, b.x), std::min(a.y, b.y)); }
+
+    // Send this rank's pc on the overlap rows to every peer whose band overlaps, receive theirs
+    // into rbuf[h] (same compact offsets).  Symmetric: the overlap is the same set of rows
+    // seen from either side.
+    void band_exchange(const std::vector<int>& vsel, cudaStream_t st) {
+        const int V = (int)vsel.size();
+        struct Chunk { long long off, cnt; };
+        std::vector<std::vector<Chunk>> ch(world);
+        for (int h = 0; h < world; ++h) {
+            if (h == rank) continue;
+            for (int k = 0; k < V; ++k) {
+                const int2 o = isect(band_of(rank, vsel[k]), band_of(h, vsel[k]));
+                if (o.x >= o.y) continue;
+                ch[h].push_back({(long long)k * per + (long long)o.x * nu, (long long)(o.y - o.x) * nu});
+            }
+            if (!ch[h].empty() && !rbuf[h]) rbuf[h] = dnew<float>(n_rays, false);
+            for (auto& c : ch[h]) {
+                comm_bytes += 4ull * (unsigned long long)c.cnt;
+                ++comm_msgs;
+            }
+        }
+        if (vg) {
+            vg_offer(pc, st);
+            for (int h = 0; h < world; ++h) {
+                if (ch[h].empty()) continue;
+                BSGD_CUDA(cudaStreamWaitEvent(st, vg->ev1[h], 0));
+                const float* src = (const float*)vg->src[h];
+                for (auto& c : ch[h])
+                    BSGD_CUDA(cudaMemcpyAsync(rbuf[h] + c.off, src + c.off, sizeof(float) * c.cnt,
+                                              cudaMemcpyDeviceToDevice, st));
+            }
+            vg_release(st);
+            return;
+        }
+        BSGD_NCCL(ncclGroupStart());
+        for (int h = 0; h < world; ++h)
+            for (auto& c : ch[h]) {
+                BSGD_NCCL(ncclSend(pc + c.off, (size_t)c.cnt, ncclFloat, h, comm, st));
+                BSGD_NCCL(ncclRecv(rbuf[h] + c.off, (size_t)c.cnt, ncclFloat, h, comm, st));
+            }
+        BSGD_NCCL(ncclGroupEnd());
+    }
+
+    // line 7 with the band exchange (Rl: the k_residual launch of this epoch, pc filled):
+    // r on this rank's band rows and ||r_I||^2 of the selected row blocks (into d_normsq)
+    void band_residual(ResLaunch& Rl, const std::vector<int>& vsel, const std::vector<int>& sel_rows,
+                       const int* drows, std::vector<char>& staging, size_t& off, cudaStream_t st) {
+        const int V = (int)vsel.size();
+        band_exchange(vsel, st);
+        std::vector<int2> bt((size_t)V * world), rg(V);
+        for (int k = 0; k < V; ++k) {
+            for (int h = 0; h < world; ++h) bt[(size_t)k * world + h] = band_of(h, vsel[k]);
+            rg[k] = rank == 0 ? make_int2(0, nv) : band_of(rank, vsel[k]);
+        }
+        std::vector<const float*> dp(world, nullptr);
+        for (int h = 0; h < world; ++h) dp[h] = h == rank ? pc : rbuf[h];
+        const size_t start = off;
+        BandLaunch B;
+        B.n_slots = V;
+        B.per = (int)per;
+        B.nu = nu;
+        B.G = world;
+        B.me = rank;
+        B.views = Rl.views;
+        B.bands = tab_put(off, bt, staging);
+        B.range = tab_put(off, rg, staging);
+        B.data = tab_put(off, dp, staging);
+        if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
+        BSGD_CUDA(cudaMemcpyAsync(d_tab + start, staging.data() + start, off - start, cudaMemcpyHostToDevice, st));
+        B.y = Rl.y;
+        B.r = Rl.r;
+        B.part = d_rpart;
+        launch_residual_band(B, st);
+        ResLaunch Rn = Rl;
+        Rn.normsq = d_npart;
+        launch_zero_rows(d_npart, drows, (int)sel_rows.size(), st);
+        launch_normsq_final(Rn, RES_GX, st);
+        allreduce_d(d_npart, (size_t)M, st);
+        launch_copy_rows(d_normsq, d_npart, drows, (int)sel_rows.size(), st);
+    }
+
     // ------------------------------------------------------------ one epoch
     // Algo 1 / Algo 2 / Eq. 4 with an explicit selection.  tiles: [n_cols][V_sel] or empty.
     // Host-buffer runs (bsgd_run with y / x in host memory) overlap the uploads with the
@@ -597,10 +709,18 @@ struct bsgd_ctx_s {
             if (!coll) {
                 Rl.mode = 0;
                 launch_residual(Rl, st);
+            } else if (band) {
+                Rl.mode = 1;
+                launch_residual(Rl, st);
+                band_residual(Rl, vsel, sel_rows, drows, staging, off, st);
             } else {
                 Rl.mode = 1;
                 launch_residual(Rl, st);
                 allreduce_f(pc, (size_t)V * per, st);
+                if (world > 1) {   // ring allreduce: 2 (G-1)/G of the buffer sent per rank
+                    comm_bytes += (unsigned long long)(8.0 * (double)V * per * (world - 1) / world);
+                    ++comm_msgs;
+                }
                 Rl.mode = 2;
                 launch_residual(Rl, st);
             }
@@ -963,6 +1083,34 @@ struct bsgd_ctx_s {
         epoch = 0;
     }
 
+    // Sharded TV (the stencil's only cross-rank neighbours are in z) needs every rank to own
+    // whole z-layers of the block grid: z-slabs, or any bx x by x bz grid with N/G a multiple
+    // of bx*by (e.g. the paper's 2x2x2 octants at G = 2).  The owned region is then the global
+    // z-range [z0, z1) and the halos are whole z-planes.
+    bool tv_shardable() const {
+        return world == 1 || (bgrid[0] == 1 && bgrid[1] == 1) || s % (bgrid[0] * bgrid[1]) == 0;
+    }
+    int owned_z0() const { return (first / (bgrid[0] * bgrid[1])) * bd[2]; }
+    int owned_z1() const { return ((first + s) / (bgrid[0] * bgrid[1])) * bd[2]; }
+    // Global plane z (inside the owned z-range) of an owned block-major field as a contiguous
+    // [y][x] plane: in place for z-slab layouts, else gathered from the bx*by blocks of its
+    // layer into tv_pk (stream-ordered: the previous exchange reading tv_pk is complete).
+    const float* plane_of(const float* owned, int z, cudaStream_t st) {
+        const long long plane = (long long)dims[0] * dims[1];
+        if (bgrid[0] == 1 && bgrid[1] == 1) return owned + (long long)(z - owned_z0()) * plane;
+        if (!tv_pk) tv_pk = dnew<float>(plane, false);
+        TvLaunch T{};
+        for (int c = 0; c < 3; ++c) {
+            T.dims[c] = dims[c];
+            T.bdims[c] = bd[c];
+            T.bgrid[c] = bgrid[c];
+        }
+        T.block0 = first;
+        T.n = (long long)s * bsize;
+        launch_pack_plane(T, owned, z, tv_pk, st);
+        return tv_pk;
+    }
+
     // method 0: FGP (Beck-Teboulle, reading A16); 1: Chambolle 2004 (tau = 1/L), the flag of
     // one dual field (tv_q, double-buffered on the fused path)
     void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st, int method = 0) {
@@ -1008,8 +1156,8 @@ struct bsgd_ctx_s {
         int axes = (dims[0] > 1) + (dims[1] > 1) + (dims[2] > 1);
         Tl.L = 4.0 * axes;
         Tl.n = n;
-        Tl.z0 = first * bd[2];
-        Tl.z1 = (first + s) * bd[2];
+        Tl.z0 = owned_z0();
+        Tl.z1 = owned_z1();
         Tl.chambolle = method == 1;
         double sk = 1.0;
         if (fused) {
@@ -1044,15 +1192,15 @@ struct bsgd_ctx_s {
             const double sk1 = (1.0 + sqrt(1.0 + 4.0 * sk * sk)) / 2.0;
             Tl.beta = (sk - 1.0) / sk1;
             // u = b - w grad^T q   (needs q_z of plane z1 from the next rank)
-            halo_exchange(tv_q + 2 * n, tv_hq, plane, /*send first plane down*/ true, st);
+            if (world > 1) halo_exchange(plane_of(tv_q + 2 * n, Tl.z0, st), tv_hq, plane, /*down*/ true, st);
             launch_tv_u(Tl, tv_q, tv_u, st);
             // p, q update (needs u of plane z0-1 from the previous rank)
-            halo_exchange(tv_u + n - plane, tv_hu, plane, false, st);
+            if (world > 1) halo_exchange(plane_of(tv_u, Tl.z1 - 1, st), tv_hu, plane, false, st);
             launch_tv_pq(Tl, st);
             sk = sk1;
         }
         float* pf = method == 1 ? tv_q : tv_p;                // Chambolle updates q in place
-        halo_exchange(pf + 2 * n, tv_hq, plane, true, st);
+        if (world > 1) halo_exchange(plane_of(pf + 2 * n, Tl.z0, st), tv_hq, plane, true, st);
         launch_tv_u(Tl, pf, x_owned, st);
     }
 
@@ -1073,8 +1221,8 @@ struct bsgd_ctx_s {
     // TV(x) (Eq. 6) of the whole volume into *d_out (device; summed over ranks)
     void tv_value(const float* x_owned, double* d_out, cudaStream_t st) {
         const long long n = (long long)s * bsize, plane = (long long)dims[0] * dims[1];
-        if (world > 1 && (bgrid[0] != 1 || bgrid[1] != 1))
-            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        if (!tv_shardable())
+            fail(BSGD_E_PARTITION, "sharded TV needs whole z-layers of blocks per rank (N/G divisible by bx*by)");
         if (!tvv_halo) tvv_halo = dnew<float>(plane);
         TvLaunch Tl{};
         for (int c = 0; c < 3; ++c) {
@@ -1084,10 +1232,10 @@ struct bsgd_ctx_s {
         }
         Tl.block0 = first;
         Tl.n = n;
-        Tl.z0 = first * bd[2];
-        Tl.z1 = (first + s) * bd[2];
+        Tl.z0 = owned_z0();
+        Tl.z1 = owned_z1();
         Tl.halo_u_prev = tvv_halo;
-        halo_exchange(x_owned + n - plane, tvv_halo, plane, false, st);   // x of plane z0-1
+        if (world > 1) halo_exchange(plane_of(x_owned, Tl.z1 - 1, st), tvv_halo, plane, false, st);   // x of plane z0-1
         BSGD_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), st));
         launch_tv_value(Tl, x_owned, d_out, st);
         allreduce_d(d_out, 1, st);
@@ -1382,11 +1530,21 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         if (const char* e = getenv("BSGD_FORCE_NCCL")) c->coll = atoi(e) != 0;   // test hook
         if (c->world > 1) c->coll = true;
         c->pc = c->coll ? c->dnew<float>(c->n_rays) : nullptr;
+        if (c->world > 1) {
+            const char* e = getenv("BSGD_EXCHANGE");
+            c->band = !(e && std::string(e) == "full");
+            if (c->band) {
+                c->compute_bands();
+                c->rbuf.assign(c->world, nullptr);
+                c->d_npart = c->dnew<double>(c->M);
+            }
+        }
         c->d_normsq = c->dnew<double>(c->M);
         c->d_rpart = c->dnew<double>((long long)c->n_views * RES_GX);
         c->d_red = c->dnew<double>(16);
         c->d_visits = c->dnew<unsigned long long>(1);
-        c->tab_bytes = 2 * (size_t)(64 + 16 * ((size_t)c->n_views * (2 + 4LL * c->s + 1) + 64LL * c->s + c->M) + 4096);
+        c->tab_bytes = 2 * (size_t)(64 + 16 * ((size_t)c->n_views * (2 + 4LL * c->s + 1 + c->world) + 64LL * c->s +
+                                              c->M + c->world) + 4096);
         c->d_tab = (char*)c->dalloc(c->tab_bytes);
         c->h_normsq.assign(c->M, 0.0);
         if (c->vg) {
@@ -1592,8 +1750,8 @@ bsgd_status bsgd_solve(bsgd_ctx c, const float* y, float* x_owned, const bsgd_so
         if (!isfinite(P->lambda) || P->lambda < 0.0 || P->tv_iters < 0 || P->svrg_m < 0)
             fail(BSGD_E_CONTRACT, "bad lambda / tv_iters / svrg_m");
         const bool tv = (P->solver == BSGD_SOLVER_ISTA || P->solver == BSGD_SOLVER_FISTA) && P->lambda > 0.0;
-        if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
-            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        if (tv && !c->tv_shardable())
+            fail(BSGD_E_PARTITION, "sharded TV needs whole z-layers of blocks per rank (N/G divisible by bx*by)");
         Ordered order_(c, S(stream));
         c->solve(P->solver, y, x_owned, P->iters, P->mu0, tv ? P->lambda : 0.0, P->tv_iters, P->svrg_m, P->seed,
                  obj, mu, S(stream));
@@ -1628,8 +1786,8 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         const int strata = P->strata > 0 ? P->strata : c->world;
         if (strat && (P->strata < 0 || c->N % strata || gN % strata))
             fail(BSGD_E_CONTRACT, "BSGD_STRATIFIED: strata must divide N and cols_per_epoch");
-        if (tv && c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
-            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        if (tv && !c->tv_shardable())
+            fail(BSGD_E_PARTITION, "sharded TV needs whole z-layers of blocks per rank (N/G divisible by bx*by)");
         if (tv && (P->tv_iters < 0 || !isfinite(P->lambda) || P->lambda < 0.0))
             fail(BSGD_E_CONTRACT, "bad TV parameters (lambda must be finite and >= 0, tv_iters >= 0)");
         if (!(P->mu0 > 0.0)) fail(BSGD_E_CONTRACT, "mu0 must be > 0");
@@ -1988,8 +2146,8 @@ bsgd_status bsgd_tv_prox(bsgd_ctx c, float* x_owned, double w, int32_t iters, in
     return guard(c, [&] {
         if (!c || !x_owned || !(w >= 0.0) || !isfinite(w) || iters < 0 || method < 0 || method > 1)
             fail(BSGD_E_CONTRACT, "bad arguments");
-        if (c->world > 1 && (c->bgrid[0] != 1 || c->bgrid[1] != 1))
-            fail(BSGD_E_PARTITION, "sharded TV needs a z-slab block grid (1,1,N)");
+        if (!c->tv_shardable())
+            fail(BSGD_E_PARTITION, "sharded TV needs whole z-layers of blocks per rank (N/G divisible by bx*by)");
         Ordered order_(c, S(stream));
         c->tv_prox(x_owned, w, iters, S(stream), method);
     });
@@ -2027,6 +2185,15 @@ bsgd_status bsgd_allreduce_time(bsgd_ctx c, int64_t count, int32_t iters, void* 
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         *ms_out = (double)ms / iters;
+    });
+}
+
+bsgd_status bsgd_comm_stats(bsgd_ctx c, uint64_t* bytes_sent, uint64_t* messages, int32_t* band_mode) {
+    return guard(c, [&] {
+        if (!c || !bytes_sent || !messages) fail(BSGD_E_CONTRACT, "bad arguments");
+        *bytes_sent = c->comm_bytes;
+        *messages = c->comm_msgs;
+        if (band_mode) *band_mode = c->band ? 1 : 0;
     });
 }
 

@@ -143,6 +143,25 @@ struct ResLaunch {
 };
 constexpr int RES_GX = 64;   // max CTAs per view slot of k_residual
 void launch_residual(const ResLaunch& R, cudaStream_t st);
+// N2 band exchange (world > 1): the residual on the detector rows this rank's
+// blocks project into.  Row v of slot k: covered_by = {h : bands[k][h] contains v}; if this
+// rank is in it, r = y - sum_{h in covered_by, ascending} data[h][k][v][.] (the same sum, in
+// the same order, on every rank sharing the row) and ||r||^2 counts it iff this rank is the
+// lowest h; rows no band covers keep r = y and rank 0 counts them.
+struct BandLaunch {
+    int n_slots, per, nu, G, me;
+    const int* views;           // [n_slots]
+    const int2* bands;          // [n_slots][G] (lo, hi) detector rows of every rank's band
+    const int2* range;          // [n_slots] rows this rank visits
+    const float* const* data;   // [G] compact [n_slots * per] partial sums (own pc / received)
+    const float* y;
+    float* r;
+    double* part;               // [n_slots][RES_GX] per-CTA partial ||r||^2
+};
+void launch_residual_band(const BandLaunch& B, cudaStream_t st);
+void launch_copy_rows(double* dst, const double* src, const int* rows, int n, cudaStream_t st);
+// R.normsq[i] = fixed-order sum of R.part over the slots of row block i (gx CTAs per slot)
+void launch_normsq_final(const ResLaunch& R, int gx, cudaStream_t st);
 // deterministic BP: S (power of two) from max|r| over n rays, V views and rpc (an upper bound on
 // the rays of one view crossing one cell); out += a / S
 void launch_det_scale(const float* r, long long n, int V, double rpc, float scale, unsigned* mx, float* S,
@@ -201,6 +220,9 @@ struct TvLaunch {
 };
 void launch_tv_u(const TvLaunch& T, const float* src_q, float* dst, cudaStream_t st);
 void launch_tv_pq(const TvLaunch& T, cudaStream_t st);
+// out[y * nx + x] = owned[(x, y, z)] for global plane z inside the owned range (block-major
+// owned field; T: dims, bdims, bgrid, block0, n) -- a z-plane halo of a non-slab block grid
+void launch_pack_plane(const TvLaunch& T, const float* owned, int z, float* out, cudaStream_t st);
 // *out += TV(x) over the owned voxels (T: dims, bdims, bgrid, block0, n, halo_u_prev = x of plane z0-1)
 void launch_tv_value(const TvLaunch& T, const float* x, double* out, cudaStream_t st);
 // out[i] = sum_{g = 0..G-1} ptrs[g][i] in ascending g (virtual-rank allreduce), G <= 8

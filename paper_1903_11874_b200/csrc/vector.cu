@@ -264,6 +264,70 @@ __global__ void __launch_bounds__(256) k_residual(const ResLaunch R) {
     }
 }
 
+// N2 band residual (BandLaunch): r = y - sum over the ranks whose band covers the row, in
+// ascending rank order; fp64 ||r||^2 partials of the rows this rank owns (per CTA)
+__global__ void __launch_bounds__(256) k_residual_band(const BandLaunch B) {
+    const int slot = blockIdx.y;
+    const int view = B.views[slot];
+    const int2 rg = B.range[slot];
+    const int2* bd = B.bands + (size_t)slot * B.G;
+    const long long base = (long long)view * B.per, cbase = (long long)slot * B.per;
+    double ss = 0.0;
+    const bool v4 = (B.nu & 3) == 0;
+    const int W = v4 ? B.nu / 4 : B.nu;
+    const long long n = (long long)(rg.y - rg.x) * W;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int v = rg.x + (int)(q / W), u = (int)(q % W) * (v4 ? 4 : 1);
+        int first = -1;
+        bool mine = false;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const long long e = (long long)v * B.nu + u;
+        for (int h = 0; h < B.G; ++h) {          // ascending ranks: one order everywhere
+            const int2 b = bd[h];
+            if (v < b.x || v >= b.y) continue;
+            if (first < 0) first = h;
+            mine |= h == B.me;
+            const float* d = B.data[h];
+            if (!d) continue;                    // a band not overlapping this rank's
+            if (v4) {
+                const float4 t = *reinterpret_cast<const float4*>(d + cbase + e);
+                acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+            } else {
+                acc.x += d[cbase + e];
+            }
+        }
+        if (mine) {
+            if (v4) {
+                const float4 yy = __ldg(reinterpret_cast<const float4*>(B.y + base + e));
+                const float4 rr = make_float4(yy.x - acc.x, yy.y - acc.y, yy.z - acc.z, yy.w - acc.w);
+                *reinterpret_cast<float4*>(B.r + base + e) = rr;
+                if (first == B.me)
+                    ss += (double)rr.x * rr.x + (double)rr.y * rr.y + (double)rr.z * rr.z + (double)rr.w * rr.w;
+            } else {
+                const float rr = B.y[base + e] - acc.x;
+                B.r[base + e] = rr;
+                if (first == B.me) ss += (double)rr * rr;
+            }
+        } else if (first < 0 && B.me == 0) {     // no band: r = y, never changed
+            if (v4) {
+                const float4 yy = __ldg(reinterpret_cast<const float4*>(B.y + base + e));
+                ss += (double)yy.x * yy.x + (double)yy.y * yy.y + (double)yy.z * yy.z + (double)yy.w * yy.w;
+            } else {
+                const float yy = B.y[base + e];
+                ss += (double)yy * yy;
+            }
+        }
+    }
+    ss = block_sum(ss);
+    if (threadIdx.x == 0) B.part[(size_t)slot * RES_GX + blockIdx.x] = ss;
+}
+
+__global__ void k_copy_rows(double* dst, const double* src, const int* rows, int n) {
+    const int i = threadIdx.x;
+    if (i < n) dst[rows[i]] = src[rows[i]];
+}
+
 // normsq[i] = sum of the partials of the slots of row block i (CTA i; fixed assignment of
 // partials to threads and a fixed reduction tree: deterministic).  Rows without slots keep
 // their value.
@@ -482,6 +546,18 @@ __global__ void __launch_bounds__(256) k_tv_value(const TvLaunch T, const float*
     }
     acc = block_sum(acc);
     if (threadIdx.x == 0) atomicAdd(out, acc);
+}
+
+// one global z-plane of an owned block-major field, gathered into [y][x] (halo exchange of
+// block grids whose ranks own whole z-layers of blocks)
+__global__ void __launch_bounds__(256) k_pack_plane(const TvLaunch T, const float* owned, int z, float* out) {
+    const long long plane = (long long)T.dims[0] * T.dims[1];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % T.dims[0]), y = (int)(i / T.dims[0]);
+        const long long o = owned_index(T, x, y, z);
+        out[i] = o >= 0 ? owned[o] : 0.f;
+    }
 }
 
 // p_new = P(q + grad(u)/(L w)); q = p_new + beta (p_new - p); p = p_new
@@ -869,6 +945,12 @@ void launch_residual(const ResLaunch& R, cudaStream_t st) {
     }
 }
 
+void launch_normsq_final(const ResLaunch& R, int gx, cudaStream_t st) {
+    k_normsq_final<<<R.M, 256, 0, st>>>(R, gx);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
 void launch_zero_rects(float* proj, const int* views, const int4* rects, int n, int nu, int nv, cudaStream_t st) {
     if (n == 0) return;
     k_zero_rects<<<dim3(64, (unsigned)n), 256, 0, st>>>(proj, views, rects, nu, nv);
@@ -941,6 +1023,26 @@ void launch_fill_random(float* v, long long n, uint64_t seed, cudaStream_t st) {
 
 void launch_scale(float* v, long long n, const double* nrm, cudaStream_t st) {
     k_scale<<<grid_for(n, 4), 256, 0, st>>>(v, n, nrm);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_residual_band(const BandLaunch& B, cudaStream_t st) {
+    if (B.n_slots == 0) return;
+    k_residual_band<<<dim3(RES_GX, (unsigned)B.n_slots), 256, 0, st>>>(B);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_copy_rows(double* dst, const double* src, const int* rows, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_copy_rows<<<1, 1024, 0, st>>>(dst, src, rows, n);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_pack_plane(const TvLaunch& T, const float* owned, int z, float* out, cudaStream_t st) {
+    k_pack_plane<<<grid_for((long long)T.dims[0] * T.dims[1], 1), 256, 0, st>>>(T, owned, z, out);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

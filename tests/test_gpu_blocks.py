@@ -1,0 +1,217 @@
+"""Sharded TV on non-slab block grids (the paper's "8 cubic blocks",
+PAPER.md:449): with G virtual ranks on one GPU (bsgd_vgroup), every rank owning whole
+z-layers of a bx x by x bz grid, BSGD-TV (Algo 4) + Algo 3 against the oracle, the TV prox
+(Algo 4 line 16) and TV(x) (Eq. 6) per voxel, and the E_PARTITION contract for grids whose
+ranks would own partial layers."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import bsgd as ob
+from oracle.projector import BlockGrid, Projector
+
+from _problems import problem
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1903_11874_b200 as m
+    return m
+
+
+def _ranks(bs, G, fn):
+    """Run fn(r, stream) on G threads (one per virtual rank); re-raise the first error."""
+    out, errs = [None] * G, []
+
+    def main(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(r, s)
+                s.synchronize()
+        except Exception as e:          # noqa: BLE001 -- surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("blocks,G", [((2, 2, 2), 2), ((2, 2, 4), 4), ((2, 1, 4), 2)])
+def test_virtual_ranks_block_grid_tv_trajectory(bs, blocks, G):
+    p, g, vol32, y = problem("cfg3", K=48, n_views=40)
+    P = Projector(g, BlockGrid(g.dims, blocks))
+    mu = float(np.float32(2.0 / ob.power_iteration(P, 30, seed=1)))
+    E, M, N = 24, p.M, P.grid.N
+    xtb = P.grid.to_blocks(vol32)
+    prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=N // 2, total_epochs=E, tv=True,
+                    auto_mu=True, lam=0.1, tv_period=3)
+    o = ob.OracleBSGD(g, blocks, M, y.astype(np.float64), prm, row_kind="random", row_seed=11,
+                      x_true=xtb.astype(np.float64))
+    for _ in range(E):
+        o.epoch()
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, blocks, M, kind="random", row_seed=11, rank=r, world=G, vgroup=group)
+            for r in range(G)]
+    nb = N // G
+
+    def run(r, s):
+        yd = torch.from_numpy(y).cuda()
+        xd = torch.zeros(nb * P.grid.bsize, device="cuda")
+        xt = torch.from_numpy(xtb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+        res = ctxs[r].run(yd, xd, epochs=E, mu0=mu, seed=3, x_true=xt, rows_per_epoch=1, cols_per_epoch=N // 2,
+                          flags=bs.TV | bs.AUTO_MU, lam=0.1, tv_iters=20, tv_period=3, stream=s)
+        s.synchronize()
+        return res, xd.cpu().numpy().astype(np.float64)
+
+    out = _ranks(bs, G, run)
+    for c in ctxs:
+        c.close()
+    group.close()
+    res0 = out[0][0]
+    for r in range(1, G):
+        assert np.array_equal(out[r][0].obj, res0.obj)
+        assert np.array_equal(out[r][0].mu, res0.mu)
+    assert [r_["rows"] for r_ in o.log] == res0.sel_rows.tolist()
+    assert [r_["cols"] for r_ in o.log] == res0.sel_cols.tolist()
+    obj = np.array([r_["obj"] for r_ in o.log])
+    rmse = np.array([r_["rmse"] for r_ in o.log])
+    assert np.allclose(res0.mu, [r_["mu"] for r_ in o.log], rtol=1e-12)
+    x = np.concatenate([out[r][1] for r in range(G)])
+    e_obj = float(np.max(np.abs(res0.obj - obj) / obj))
+    e_rmse = float(np.max(np.abs(res0.rmse - rmse) / rmse))
+    e_x = float(np.max(np.abs(x - o.x.ravel())) / np.max(np.abs(o.x)))
+    print(f"blocks {blocks} G={G}: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}")
+    assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (e_obj, e_rmse, e_x)
+
+
+@pytest.mark.parametrize("blocks,G", [((2, 2, 2), 2), ((3, 2, 4), 4)])
+def test_virtual_ranks_block_grid_tv_prox_and_value(bs, blocks, G):
+    """bsgd_tv_prox / bsgd_tv_value with the halo planes gathered from the bx*by blocks of a
+    layer: per voxel against the oracle's whole-volume FGP prox and TV(x)."""
+    dims = (36, 28, 24)
+    rng = np.random.default_rng(5)
+    vol = rng.random((dims[2], dims[1], dims[0])).astype(np.float32)
+    import synth
+    vecs = synth.circular("cone", 8, 360.0, 100.0, 60.0, 40, 30, 1.4, 1.3)
+    g = synth.Geometry(synth.CONE, vecs, 40, 30, dims)
+    grid = BlockGrid(dims, blocks)
+    xb = grid.to_blocks(vol)
+    N = grid.N
+    nb = N // G
+    w = 0.07
+    ref = ob.tv_prox(vol.astype(np.float64), w, 20)
+    tv_ref = ob.tv_value(vol.astype(np.float64))
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, blocks, 2, rank=r, world=G, vgroup=group) for r in range(G)]
+
+    def run(r, s):
+        xd = torch.from_numpy(xb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+        tv = ctxs[r].tv_value(xd, stream=s)
+        ctxs[r].tv_prox(xd, w, 20, stream=s)
+        s.synchronize()
+        return tv, xd.cpu().numpy().astype(np.float64)
+
+    out = _ranks(bs, G, run)
+    for c in ctxs:
+        c.close()
+    group.close()
+    got = grid.from_blocks(np.concatenate([o[1] for o in out]).reshape(N, -1))
+    err = float(np.max(np.abs(got - ref)))
+    print(f"blocks {blocks} G={G}: prox max |d| {err:.3g}, TV rel {abs(out[0][0] - tv_ref) / tv_ref:.3g}")
+    assert err < 1e-5 * max(1.0, float(np.max(np.abs(ref))))
+    for r in range(G):
+        assert abs(out[r][0] - tv_ref) <= 1e-9 * tv_ref
+
+
+def test_partial_layer_ownership_is_rejected(bs):
+    """(2,2,2) over 4 ranks: each rank would own half a z-layer (cross-rank x / y neighbours):
+    the TV calls fail with E_PARTITION before any device work; plain BSGD still runs."""
+    import synth
+    dims = (16, 16, 16)
+    vecs = synth.circular("cone", 6, 360.0, 60.0, 40.0, 24, 20, 1.3, 1.3)
+    g = synth.Geometry(synth.CONE, vecs, 24, 20, dims)
+    G = 4
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, (2, 2, 2), 2, rank=r, world=G, vgroup=group) for r in range(G)]
+    codes = []
+    for c in ctxs:
+        x = torch.ones(c.owned_count * c.block_voxels, device="cuda")
+        with pytest.raises(bs.BsgdError) as e:
+            c.tv_prox(x, 0.1, 5)
+        codes.append(e.value.code)
+        assert torch.all(x == 1.0)
+    assert codes == [2] * G                      # BSGD_E_PARTITION
+    for c in ctxs:
+        c.close()
+    group.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
+    """N2: the residual formed from the peers' partial sums on overlapping
+    detector bands only (default for world > 1) reproduces the oracle's Algo 1 + Algo 3
+    trajectory, and the full-allreduce mode (BSGD_EXCHANGE=full), on G virtual ranks of a
+    scaled cfg5-shaped cone problem (8 z-slabs); it sends >= 4x fewer bytes."""
+    p, g, vol32, y = problem("cfg5", K=64, n_views=36)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = float(np.float32(1.5 / ob.power_iteration(P, 20, seed=1)))
+    E = 20
+    xtb = P.grid.to_blocks(vol32)
+    prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=8, total_epochs=E, auto_mu=True)
+    o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11,
+                      x_true=xtb.astype(np.float64))
+    for _ in range(E):
+        o.epoch()
+    nb = p.N // G
+    runs = {}
+    for mode in ("band", "full"):
+        monkeypatch.setenv("BSGD_EXCHANGE", mode)
+        group = bs.VirtualGroup(G)
+        ctxs = [bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, rank=r, world=G,
+                                         vgroup=group) for r in range(G)]
+
+        def run(r, s):
+            yd = torch.from_numpy(y).cuda()
+            xd = torch.zeros(nb * P.grid.bsize, device="cuda")
+            xt = torch.from_numpy(xtb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+            res = ctxs[r].run(yd, xd, epochs=E, mu0=mu, seed=3, x_true=xt, rows_per_epoch=1, cols_per_epoch=8,
+                              flags=bs.AUTO_MU, stream=s)
+            s.synchronize()
+            return res, xd.cpu().numpy().astype(np.float64), ctxs[r].comm_stats()
+
+        out = _ranks(bs, G, run)
+        for c in ctxs:
+            c.close()
+        group.close()
+        assert all(o_[2]["mode"] == mode for o_ in out)
+        for r in range(1, G):
+            assert np.array_equal(out[r][0].obj, out[0][0].obj)
+            assert np.array_equal(out[r][0].mu, out[0][0].mu)
+        runs[mode] = out
+    for mode, out in runs.items():
+        res0 = out[0][0]
+        x = np.concatenate([o_[1] for o_ in out])
+        obj = np.array([r_["obj"] for r_ in o.log])
+        rmse = np.array([r_["rmse"] for r_ in o.log])
+        assert [r_["cols"] for r_ in o.log] == res0.sel_cols.tolist()
+        assert np.allclose(res0.mu, [r_["mu"] for r_ in o.log], rtol=1e-12)
+        e_obj = float(np.max(np.abs(res0.obj - obj) / obj))
+        e_rmse = float(np.max(np.abs(res0.rmse - rmse) / rmse))
+        e_x = float(np.max(np.abs(x - o.x.ravel())) / np.max(np.abs(o.x)))
+        sent = sum(o_[2]["bytes_sent"] for o_ in out)
+        print(f"G={G} {mode}: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}; sent {sent / 1e6:.2f} MB")
+        assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (mode, e_obj, e_rmse, e_x)
+    band = sum(o_[2]["bytes_sent"] for o_ in runs["band"])
+    full = sum(o_[2]["bytes_sent"] for o_ in runs["full"])
+    assert 0 < band and 4 * band <= full, (band, full)
