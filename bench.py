@@ -340,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
     # warm-up epochs (untimed; also builds/initialises everything)
     ctx.run(y, x, epochs=args.warmup, mu0=mu0, seed=7, rows_per_epoch=aM, cols_per_epoch=gN, flags=sched, lam=lam)
     launches0 = bs.kernel_launches()
+    comm0 = ctx.comm_stats()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -416,6 +417,29 @@ def run_ours(args, rank, world, local_rank):
                              "(72 views x 1024^2 rays), 5 back-to-back calls timed with CUDA events on the launch "
                              "stream, max over ranks; busbw = S/t x 2(G-1)/G",
                      "residual_phase_ms": res_ms}
+    # N2: the residual exchange.  world > 1: the bytes all ranks sent in the timed
+    # epochs (bsgd_comm_stats, band mode by default); always: the library's host plan of one
+    # epoch's exchange at G = 2, 4, 8 for this config (band overlap rows vs the ring allreduce),
+    # averaged over the M row blocks
+    exchange = {"plan_per_epoch": {}}
+    try:
+        for G in (2, 4, 8):
+            if p.N % G:
+                continue
+            bb = fb = 0
+            for i in range(p.M):
+                pl = ctx.exchange_plan(G, ctx.row_block_views(i))
+                bb += pl["band_bytes"]
+                fb += pl["full_bytes"]
+            exchange["plan_per_epoch"][str(G)] = {"band_bytes": bb / p.M, "full_allreduce_bytes": fb / p.M,
+                                                   "reduction": (fb / bb) if bb else None}
+        if world > 1:
+            cs = ctx.comm_stats()
+            sent = torch.tensor([float(cs["bytes_sent"] - comm0["bytes_sent"])], dtype=torch.float64, device="cuda")
+            dist.all_reduce(sent)
+            exchange.update({"mode": cs["mode"], "timed_bytes_per_epoch_all_ranks": float(sent.item()) / args.steps})
+    except Exception as exc:   # noqa: BLE001 -- auxiliary
+        exchange["error"] = f"{type(exc).__name__}: {exc}"[:300]
     tv = None
     if not args.no_tv:   # an auxiliary measurement: never lose the main line over it
         try:
@@ -455,6 +479,7 @@ def run_ours(args, rank, world, local_rank):
                    "fp64": "ray parameters fp64, values fp32"},
         "phase_ms": {"fp": fp_ms, "residual_allreduce": res_ms, "bp": bp_ms, "step": st_ms},
         "allreduce": allreduce,
+        "exchange": exchange,
         "roofline": {"bound": "hbm",
                      "kernel": "projector pair k_project3<FP> + k_project3<BP> (+ k_project2 steep-only companions)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

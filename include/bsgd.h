@@ -303,6 +303,16 @@ bsgd_status bsgd_allreduce_time(bsgd_ctx ctx, int64_t count, int32_t iters, void
  * rows no band covers keep r = y).  Errors: BSGD_E_CONTRACT for NULL outputs.            */
 bsgd_status bsgd_comm_stats(bsgd_ctx ctx, uint64_t* bytes_sent, uint64_t* messages, int32_t* band_mode);
 
+/* Host-only plan of the residual exchange for a hypothetical ownership of this ctx's block
+ * grid by `world` ranks (rank g owns blocks [g N/world, (g+1) N/world)), for one epoch whose
+ * selected row blocks hold the n_sel views `views` (host int32): *band_bytes = bytes all
+ * ranks together send in band mode (the same band / overlap computation the band exchange
+ * uses), *full_bytes = the ring allreduce's world x 2 (world-1)/world x n_sel x rays-per-view
+ * x 4 B.  Pure host work; no collective.  Errors: BSGD_E_CONTRACT (NULL outputs, views out of
+ * range), BSGD_E_PARTITION (N % world != 0).                                             */
+bsgd_status bsgd_exchange_plan(bsgd_ctx ctx, int32_t world, int32_t n_sel, const int32_t* views,
+                               uint64_t* band_bytes, uint64_t* full_bytes);
+
 /* TV proximal step (Algo 4 line 16; TV of Eq. 5-6):
  * x_owned <- argmin_t 1/2 ||t - x_owned||^2 + w TV(t), by `iters` cold-start FGP iterations
  * on the dual (reading A16; the same call bsgd_run makes every tv_period epochs, with

@@ -143,6 +143,7 @@ SIGS = {
     "bsgd_power_iteration": ([_ctx, C.c_int32, C.c_uint64, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_allreduce_time": ([_ctx, C.c_int64, C.c_int32, C.c_void_p, P(C.c_double)], C.c_int),
     "bsgd_comm_stats": ([_ctx, P(C.c_uint64), P(C.c_uint64), P(C.c_int32)], C.c_int),
+    "bsgd_exchange_plan": ([_ctx, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_uint64), P(C.c_uint64)], C.c_int),
     "bsgd_tv_prox": ([_ctx, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
     "bsgd_tv_value": ([_ctx, C.c_void_p, P(C.c_double), C.c_void_p], C.c_int),
     "bsgd_solve": ([_ctx, C.c_void_p, C.c_void_p, P(SolveParams), P(C.c_double), P(C.c_double), C.c_void_p],
@@ -503,6 +504,14 @@ class Context:
         b, m, band = C.c_uint64(), C.c_uint64(), C.c_int32()
         self._c(_lib.bsgd_comm_stats(self.h, C.byref(b), C.byref(m), C.byref(band)))
         return {"bytes_sent": int(b.value), "messages": int(m.value), "mode": "band" if band.value else "full"}
+
+    def exchange_plan(self, world, views) -> dict:
+        """Bytes one epoch's residual exchange would send over `world` ranks for the given
+        selected views: band mode vs the full ring allreduce (bsgd_exchange_plan)."""
+        v, vp = _i32(views)
+        b, f = C.c_uint64(), C.c_uint64()
+        self._c(_lib.bsgd_exchange_plan(self.h, int(world), len(v), vp, C.byref(b), C.byref(f)))
+        return {"band_bytes": int(b.value), "full_bytes": int(f.value)}
 
     def power_iteration(self, iters=30, seed=0, stream=None) -> float:
         out = C.c_double()

@@ -23,6 +23,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 namespace bsgd {
@@ -54,6 +56,13 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
 using namespace bsgd;
 
 // Virtual-rank group (bsgd_vgroup_create): `world` contexts of one process share it.
+// NVTX range per phase of an epoch (host-side markers for nsys / ncu --nvtx; header-only
+// NVTX 3, a no-op unless a tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct bsgd_vgroup_s {
     int world = 1;
     std::mutex m;
@@ -499,23 +508,26 @@ struct bsgd_ctx_s {
         BSGD_CUDA(cudaMemcpyAsync(p, vg_tmp, bytes, cudaMemcpyDeviceToDevice, st));
     }
 
-    // Rows [lo, hi) of the detector that owned blocks [h s, (h+1) s) project into, per view.
-    void compute_bands() {
-        bands.assign((size_t)world * n_views, make_int2(0, 0));
-        for (int h = 0; h < world; ++h)
+    // Rows [lo, hi) of the detector that the blocks [h s_, (h+1) s_) of rank h of a G_-rank
+    // ownership project into, per view ([G_][n_views]).
+    std::vector<int2> rank_bands(int G_, int s_) const {
+        std::vector<int2> out((size_t)G_ * n_views, make_int2(0, 0));
+        for (int h = 0; h < G_; ++h)
             for (int v = 0; v < n_views; ++v) {
                 int lo_ = nv, hi_ = 0;
-                for (int b = 0; b < s; ++b) {
+                for (int b = 0; b < s_; ++b) {
                     int lo[3], hi[3];
-                    box(h * s + b, lo, hi);
+                    box(h * s_ + b, lo, hi);
                     const int4 f = footprint(lo, hi, v);
                     if (f.x >= f.y || f.z >= f.w) continue;
                     lo_ = std::min(lo_, f.z);
                     hi_ = std::max(hi_, f.w);
                 }
-                bands[(size_t)h * n_views + v] = lo_ < hi_ ? make_int2(lo_, hi_) : make_int2(0, 0);
+                out[(size_t)h * n_views + v] = lo_ < hi_ ? make_int2(lo_, hi_) : make_int2(0, 0);
             }
+        return out;
     }
+    void compute_bands() { bands = rank_bands(world, s); }
     int2 band_of(int h, int v) const { return bands[(size_t)h * n_views + v]; }
     static int2 isect(int2 a, int2 b) { return make_int2(std::max(a.x, b.x), std::min(a.y, b.y)); }
 
@@ -647,7 +659,9 @@ struct bsgd_ctx_s {
                              (int)((long long)tv * nv / tiles_v), (int)((long long)(tv + 1) * nv / tiles_v));
         };
         if (ev) BSGD_CUDA(cudaEventRecord(ev[0], st));
+        NvtxRange nv_epoch("bsgd epoch");
         // ---- lines 4-6: z^j_{I_i} = A_{I_i}^{J_j} x_{J_j}  (IM: tile rows only)
+        std::unique_ptr<NvtxRange> nv_phase(new NvtxRange("fp (Algo 1 l.5)"));
         if (up && up->xev) {   // block by block as the x upload lands
             for (int b = 0; b < s; ++b) {
                 BSGD_CUDA(cudaStreamWaitEvent(st, (*up->xev)[b], 0));
@@ -680,6 +694,7 @@ struct bsgd_ctx_s {
             }
         }
         if (ev) BSGD_CUDA(cudaEventRecord(ev[1], st));
+        nv_phase.reset(new NvtxRange("residual + exchange (Algo 1 l.7)"));
         // ---- line 7: r = y - sum_j z^j on the selected rows (+ allreduce of the partials)
         {
             std::vector<char> staging(tab_bytes / 2);
@@ -726,6 +741,7 @@ struct bsgd_ctx_s {
             }
         }
         if (ev) BSGD_CUDA(cudaEventRecord(ev[2], st));
+        nv_phase.reset(new NvtxRange("bp + step (Algo 1 l.9-14)"));
         // ---- lines 8-10: g_hat^i_{J_j} = 2 (A_{I_i}^{J_j})^T r_{I_i}, then lines 11-14
         std::vector<float*> oN, oT;
         std::vector<const float*> none;
@@ -1114,6 +1130,7 @@ struct bsgd_ctx_s {
     // method 0: FGP (Beck-Teboulle, reading A16); 1: Chambolle 2004 (tau = 1/L), the flag of
     // one dual field (tv_q, double-buffered on the fused path)
     void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st, int method = 0) {
+        NvtxRange nv_("tv prox (Algo 4 l.16)");
         const long long n = (long long)s * bsize;
         // z-slab layouts (the owned volume is one [z][y][x] array) take the fused iteration
         const bool fused = bgrid[0] == 1 && bgrid[1] == 1;
@@ -2185,6 +2202,29 @@ bsgd_status bsgd_allreduce_time(bsgd_ctx c, int64_t count, int32_t iters, void* 
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         *ms_out = (double)ms / iters;
+    });
+}
+
+bsgd_status bsgd_exchange_plan(bsgd_ctx c, int32_t world, int32_t n_sel, const int32_t* views,
+                               uint64_t* band_bytes, uint64_t* full_bytes) {
+    return guard(c, [&] {
+        if (!c || world < 1 || n_sel < 0 || (n_sel > 0 && !views) || !band_bytes || !full_bytes)
+            fail(BSGD_E_CONTRACT, "bad arguments");
+        if (c->N % world) fail(BSGD_E_PARTITION, "N must be divisible by world");
+        for (int k = 0; k < n_sel; ++k)
+            if (views[k] < 0 || views[k] >= c->n_views) fail(BSGD_E_CONTRACT, "view out of range");
+        const std::vector<int2> bd = c->rank_bands(world, c->N / world);
+        unsigned long long band = 0;
+        for (int g = 0; g < world; ++g)
+            for (int h = 0; h < world; ++h) {
+                if (h == g) continue;
+                for (int k = 0; k < n_sel; ++k) {
+                    const int2 o = bsgd_ctx_s::isect(bd[(size_t)g * c->n_views + views[k]], bd[(size_t)h * c->n_views + views[k]]);
+                    if (o.x < o.y) band += 4ull * (unsigned long long)(o.y - o.x) * (unsigned long long)c->nu;
+                }
+            }
+        *band_bytes = band;
+        *full_bytes = world > 1 ? (uint64_t)(8.0 * (double)n_sel * c->per * (world - 1)) : 0;   // G ranks x 2(G-1)/G
     });
 }
 

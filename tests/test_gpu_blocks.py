@@ -191,10 +191,17 @@ def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
             return res, xd.cpu().numpy().astype(np.float64), ctxs[r].comm_stats()
 
         out = _ranks(bs, G, run)
+        # the host plan (bsgd_exchange_plan) predicts the bytes the ranks sent
+        plan = 0
+        for e in range(E):
+            views = [v for i in out[0][0].sel_rows[e] for v in ctxs[0].row_block_views(int(i))]
+            pl = ctxs[0].exchange_plan(G, views)
+            plan += pl["band_bytes"] if mode == "band" else pl["full_bytes"]
         for c in ctxs:
             c.close()
         group.close()
         assert all(o_[2]["mode"] == mode for o_ in out)
+        assert abs(sum(o_[2]["bytes_sent"] for o_ in out) - plan) <= 8 * G * E, (mode, plan)
         for r in range(1, G):
             assert np.array_equal(out[r][0].obj, out[0][0].obj)
             assert np.array_equal(out[r][0].mu, out[0][0].mu)
