@@ -794,36 +794,38 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
     const int nx = T.dims[0], ny = T.dims[1];
     const float w = T.wf;
     const TvPlane P = tv_plane(T, z);
-    if (warp > TV4_TY) {                           // halo column x0 - 1 (scalars), rows y0 .. y0+TY-1
-        const int y = y0 + lane;
-        if (lane < TV4_TY && x0 >= 1 && y < ny) su[lane + 1][3] = tv_u_at(T, P, x0 - 1, y, z, w);
-        __syncthreads();
-        return;
-    }
-    const int row = warp;                          // 0 = halo row y0 - 1, 1.. = output rows
-    const int y = y0 + row - 1, x = x0 + 4 * lane;
-    const bool act = y >= 0 && y < ny && x < nx;
+    // the last warp is the helper of the halo column x0 - 1 (scalars, rows y0 .. y0+TY-1);
+    // every thread of the CTA reaches the one barrier below (no divergent barriers)
+    const bool helper = warp > TV4_TY;
+    const int row = helper ? 0 : warp;             // 0 = halo row y0 - 1, 1.. = output rows
+    const int y = helper ? y0 + lane : y0 + row - 1, x = x0 + 4 * lane;
+    const bool act = !helper && y >= 0 && y < ny && x < nx;
     const bool out = act && row >= 1;
-    float u[4], uz[4] = {0.f, 0.f, 0.f, 0.f};
-    tv_u4(T, P, x, y, z, act, w, u);
+    float u[4] = {0.f, 0.f, 0.f, 0.f}, uz[4] = {0.f, 0.f, 0.f, 0.f};
     const long long plane = (long long)nx * ny;
     const long long i = (long long)(z - T.z0) * plane + (long long)y * nx + x;
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0, p0 = q0, p1 = q0, p2 = q0;
-    if (row >= 1) {
-        if (z >= 1) tv_u4(T, tv_plane(T, z - 1), x, y, z - 1, out, w, uz);
-        if (out && !T.first) {
-            q0 = ld4(T.q + i);
-            q1 = ld4(T.q + T.n + i);
-            q2 = ld4(T.q + 2 * T.n + i);
-            if (!T.chambolle) {
-                p0 = ld4(T.p + i);
-                p1 = ld4(T.p + T.n + i);
-                p2 = ld4(T.p + 2 * T.n + i);
+    float ul = 0.f;
+    if (helper) {
+        if (lane < TV4_TY && x0 >= 1 && y < ny) su[lane + 1][3] = tv_u_at(T, P, x0 - 1, y, z, w);
+    } else {                                       // warp-uniform branch: whole warps
+        tv_u4(T, P, x, y, z, act, w, u);
+        if (row >= 1) {
+            if (z >= 1) tv_u4(T, tv_plane(T, z - 1), x, y, z - 1, out, w, uz);
+            if (out && !T.first) {
+                q0 = ld4(T.q + i);
+                q1 = ld4(T.q + T.n + i);
+                q2 = ld4(T.q + 2 * T.n + i);
+                if (!T.chambolle) {
+                    p0 = ld4(T.p + i);
+                    p1 = ld4(T.p + T.n + i);
+                    p2 = ld4(T.p + 2 * T.n + i);
+                }
             }
         }
+        if (act) *reinterpret_cast<float4*>(&su[row][4 + 4 * lane]) = make_float4(u[0], u[1], u[2], u[3]);
+        ul = __shfl_up_sync(0xffffffffu, u[3], 1);
     }
-    if (act) *reinterpret_cast<float4*>(&su[row][4 + 4 * lane]) = make_float4(u[0], u[1], u[2], u[3]);
-    const float ul = __shfl_up_sync(0xffffffffu, u[3], 1);
     __syncthreads();
     if (!out) return;
     const float uxm = lane > 0 ? ul : su[row][3];   // u(x - 1)
