@@ -257,29 +257,46 @@ def _band_sample(seconds):
     return {"vps_per_core": visits / timed, "bands": n, "threads": 1}
 
 
-def run_reference(args, rank, world):
-    if rank != 0:
-        return 0
-    # rank 0 alone does the work: all host cores (torch.distributed.run exports
-    # OMP_NUM_THREADS=1 to every rank; BENCH_OMP_THREADS overrides)
+def oracle_env():
+    """Both CPU legs run the oracle on all host cores with OMP_PROC_BIND=close (set before
+    liboracle.so, and so its OpenMP runtime, is first loaded; torch.distributed.run exports
+    OMP_NUM_THREADS=1 to every rank; BENCH_OMP_THREADS overrides)."""
     os.environ["OMP_NUM_THREADS"] = os.environ.get("BENCH_OMP_THREADS", str(os.cpu_count() or 1))
-    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ["OMP_PROC_BIND"] = os.environ.get("BENCH_OMP_PROC_BIND", "close")
+
+
+def measure_oracle(steps, warmup):
+    """The one CPU measurement both legs report (the --impl reference arm and our line's
+    cpu_baseline): each step = FP + BP of one whole sampled cfg5 view through the 8 slabs
+    (views taken in SAMPLE_VIEWS order after the warm-up ones); value = median visits/s over
+    the steps / (FP + BP visits of one epoch, from the oracle's own per-view counts)."""
+    oracle_env()
     _oracle_setup()
     per_step, vps_all, views = [], [], []
-    for it in range(args.warmup + args.steps):
+    for it in range(warmup + steps):
         r = oracle_sample(target_s=4.0, max_views=1, first=it)
-        if it >= args.warmup:
+        if it >= warmup:
             per_step.append(r["seconds"])
             vps_all.append(r["vps"])
             views += r["views"]
     p, g, projs, counts, epoch_fp, _ = _oracle_setup()
     vps = float(np.median(vps_all))
-    value = vps / (2.0 * epoch_fp)
     cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or (os.cpu_count() or 1)
     sample = (f"each step = one whole cfg5 view (1024x1024 rays) FP+BP through all 8 z-slabs, fp64 merged-alpha "
-              f"Siddon, OpenMP on {cores} host threads ({_cpu_model()}); views {views}; visits from the "
-              f"oracle's own per-view count; epoch = {g.n_views // p.M} views x the mean visits per view of "
-              f"the quarter-orbit sample {list(SAMPLE_VIEWS)} = {epoch_fp:.4g} FP visits")
+              f"Siddon, OpenMP on {cores} host threads ({_cpu_model()}, OMP_PROC_BIND="
+              f"{os.environ['OMP_PROC_BIND']}); views {views}; visits from the oracle's own per-view count; "
+              f"epoch = {g.n_views // p.M} views x the mean visits per view of the quarter-orbit sample "
+              f"{list(SAMPLE_VIEWS)} = {epoch_fp:.4g} FP visits; value = median over the steps")
+    return {"value": vps / (2.0 * epoch_fp), "vps": vps, "cores": cores, "sample": sample,
+            "ms_per_step": 1e3 * float(np.mean(per_step)), "epoch_fp_visits": epoch_fp}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    m = measure_oracle(args.steps, args.warmup)
+    value, vps, cores, sample = m["value"], m["vps"], m["cores"], m["sample"]
+    per_step = [m["ms_per_step"] / 1e3]
     line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "epochs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(per_step)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -451,17 +468,12 @@ def run_ours(args, rank, world, local_rank):
         return 0
     cpu = None
     if world == 1 and not args.no_cpu and args.config == "cfg5":
-        r = oracle_sample(target_s=args.cpu_seconds)
+        # the same measurement as the --impl reference arm (measure_oracle), fewer steps
+        r = measure_oracle(steps=3, warmup=1)
         one = oracle_one_thread()
-        cpu = {"value": r["epochs_per_s"], "unit": "epochs/s", "cores": r["threads"], "kind": "oracle",
-               "sample": (f"{len(r['views'])} whole cfg5 view(s) {r['views']} (1024x1024 rays each) FP+BP through all "
-                          f"8 z-slabs, fp64 merged-alpha Siddon, OpenMP on {r['threads']} host threads; "
-                          f"{r['visits']:.4g} visits (the oracle's own per-view counts, outside the timing) in "
-                          f"{r['seconds']:.1f} s; epoch = {g.n_views // p.M} views x the mean visits per view of "
-                          f"the quarter-orbit sample {list(SAMPLE_VIEWS)} = {r['epoch_fp_visits']:.4g} FP visits "
-                          f"(this run's GPU epochs: {vis_ep:.4g})"),
-               "intersections_per_s": r["vps"], "cpu_model": _cpu_model(),
-               "one_thread": one}
+        cpu = {"value": r["value"], "unit": "epochs/s", "cores": r["cores"], "kind": "oracle",
+               "sample": r["sample"] + f" (this run's GPU epochs: {vis_ep:.4g} FP visits)",
+               "intersections_per_s": r["vps"], "cpu_model": _cpu_model(), "one_thread": one}
     line = {
         "metric": METRIC, "value": epochs_per_s, "unit": "epochs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -579,7 +591,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-tv", action="store_true", help="skip the separate TV-prox timing")
     ap.add_argument("--det", action="store_true", help="BSGD_DETERMINISTIC (fixed-point BP reductions)")
     ap.add_argument("--eq8", action="store_true",
