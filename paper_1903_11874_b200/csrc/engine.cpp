@@ -140,7 +140,7 @@ struct bsgd_ctx_s {
     float *accN = nullptr, *accT = nullptr, *pc = nullptr;
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
-          *tv_q2 = nullptr, *tv_hp = nullptr, *tv_pk = nullptr;
+          *tv_q2 = nullptr, *tv_hp = nullptr, *tv_pk = nullptr, *tvz_hp = nullptr, *tvz_hn = nullptr;
     float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
@@ -1177,6 +1177,58 @@ struct bsgd_ctx_s {
         Tl.z1 = owned_z1();
         Tl.chambolle = method == 1;
         double sk = 1.0;
+        if (fused && method == 0 && dims[0] % 4 == 0 && !getenv("BSGD_TV_PLANEWISE")) {
+            // z-marching FGP (k_tv_fgp_z): p_{k-1}, p_{k-2}, p_k rotate through tv_q, tv_q2, tv_p
+            if (!tvz_hp) {
+                tvz_hp = dnew<float>(7 * plane);
+                tvz_hn = dnew<float>(2 * plane);
+            }
+            float* buf[3] = {tv_q, tv_q2, tv_p};
+            TvzLaunch Z{};
+            Z.nx = dims[0];
+            Z.ny = dims[1];
+            Z.nz = dims[2];
+            Z.z0 = Tl.z0;
+            Z.z1 = Tl.z1;
+            Z.n = n;
+            Z.b = x_owned;
+            Z.halo_prev = tvz_hp;
+            Z.halo_next = tvz_hn;
+            Z.w = (float)wgt;
+            Z.s = (float)(1.0 / (Tl.L * wgt));
+            Z.zc = std::max(1, std::min(16, (Tl.z1 - Tl.z0) / 4));
+            if (world > 1) halo_exchange(x_owned + n - plane, tvz_hp + 6 * plane, plane, false, st);   // b of z0-1
+            double s_prev = 1.0;                             // s_{k-1}
+            for (int k = 1; k <= iters; ++k) {
+                double beta = 0.0;                           // beta_{k-1} = (s_{k-1} - 1) / s_k
+                if (k >= 2) {
+                    const double s_k = (1.0 + sqrt(1.0 + 4.0 * s_prev * s_prev)) / 2.0;
+                    beta = (s_prev - 1.0) / s_k;
+                    s_prev = s_k;
+                }
+                Z.P1 = buf[(k + 2) % 3];                     // p_{k-1}
+                Z.P2 = buf[(k + 1) % 3];                     // p_{k-2}
+                Z.Pn = buf[k % 3];                           // p_k
+                Z.stage = k == 1 ? 1 : (k == 2 ? 2 : 0);
+                Z.beta = (float)beta;
+                if (world > 1 && k >= 2) {
+                    for (int c = 0; c < 3; ++c) {            // P1, P2 of plane z0-1 from the previous rank
+                        halo_exchange(Z.P1 + c * n + n - plane, tvz_hp + c * plane, plane, false, st);
+                        halo_exchange(Z.P2 + c * n + n - plane, tvz_hp + (3 + c) * plane, plane, false, st);
+                    }
+                    halo_exchange(Z.P1 + 2 * n, tvz_hn, plane, true, st);           // z components of
+                    halo_exchange(Z.P2 + 2 * n, tvz_hn + plane, plane, true, st);   // plane z1
+                }
+                launch_tv_fgp_z(Z, st);
+            }
+            float* pf = buf[iters % 3];                      // p_K
+            Tl.first = 0;
+            if (world > 1) halo_exchange(pf + 2 * n, tv_hq, plane, true, st);
+            Tl.q = pf;
+            Tl.wf = (float)wgt;
+            launch_tv_out(Tl, x_owned, st);
+            return;
+        }
         if (fused) {
             Tl.halo_prev = tv_hp;
             halo_exchange(x_owned + n - plane, tv_hp + 3 * plane, plane, false, st);   // b of plane z0-1

@@ -232,5 +232,24 @@ void launch_sum_ptrs(void* out, const void* const* ptrs, int G, long long n, boo
 void launch_tv_fgp(const TvLaunch& T, cudaStream_t st);
 // x = b - w grad^T q (T.q = the final p) for z-slab layouts
 void launch_tv_out(const TvLaunch& T, float* out, cudaStream_t st);
+// z-marching FGP iteration (z-slab layouts, nx % 4 == 0; the default FGP path): the dual
+// state is (p_{k-1}, p_{k-2}) in three rotating buffers -- q_k = p_{k-1} + beta (p_{k-1} -
+// p_{k-2}) is formed where it is read, p_k is written to the third buffer -- and each CTA
+// walks a column of ZC planes of one x-y tile, carrying u(z-1) in registers.
+struct TvzLaunch {
+    int nx, ny, nz;            // global volume dims
+    int z0, z1;                // owned planes
+    long long n;               // owned voxels (component stride of the P buffers)
+    const float* b;            // owned b = x (prox input), [z][y][x] from plane z0
+    const float* P1;           // p_{k-1} (3 components)
+    const float* P2;           // p_{k-2}
+    float* Pn;                 // p_k (output)
+    const float* halo_prev;    // plane z0-1: P1x, P1y, P1z, P2x, P2y, P2z, b (7 planes) or NULL
+    const float* halo_next;    // plane z1: P1z, P2z (2 planes) or NULL
+    float w, s, beta;          // w = mu lambda, s = 1/(L w), beta = beta_{k-1}
+    int stage;                 // 1: k = 1 (q = 0); 2: k = 2 (q = p_1, p_0 = 0 not read); 0: k >= 3
+    int zc;                    // planes per CTA
+};
+void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st);
 
 }  // namespace bsgd

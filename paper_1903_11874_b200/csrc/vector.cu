@@ -864,6 +864,178 @@ __global__ void __launch_bounds__((TV4_TY + 2) * 32, MINB) k_tv_fgp4(const TvLau
     }
 }
 
+// ---- z-marching FGP (TvzLaunch) -------------------------------------------------------
+// Per plane z, component c (0..2) of P1 / P2 and b: owned planes from the buffers, plane
+// z0-1 from halo_prev, plane z1 (z components only) from halo_next.
+struct ZPlane {
+    const float* p1[3];
+    const float* p2[3];
+    const float* b;
+};
+__device__ __forceinline__ ZPlane zplane(const TvzLaunch& T, int z) {
+    const long long plane = (long long)T.nx * T.ny;
+    ZPlane P;
+    if (z < T.z0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            P.p1[c] = T.halo_prev + c * plane;
+            P.p2[c] = T.halo_prev + (3 + c) * plane;
+        }
+        P.b = T.halo_prev + 6 * plane;
+    } else if (z >= T.z1) {           // only the z components are read there
+        P.p1[0] = P.p1[1] = P.p1[2] = T.halo_next;
+        P.p2[0] = P.p2[1] = P.p2[2] = T.halo_next + plane;
+        P.b = nullptr;
+    } else {
+        const long long off = (long long)(z - T.z0) * plane;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            P.p1[c] = T.P1 + c * T.n + off;
+            P.p2[c] = T.P2 + c * T.n + off;
+        }
+        P.b = T.b + off;
+    }
+    return P;
+}
+// q = p1 + beta (p1 - p2) as the fused kernel formed it (stage 1: q = 0, stage 2: q = p1)
+__device__ __forceinline__ float4 zq4(const TvzLaunch& T, const float* p1, const float* p2, long long i) {
+    if (T.stage == 1) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 a = ld4(p1 + i);
+    if (T.stage == 2) return a;
+    const float4 c = ld4(p2 + i);
+    return make_float4(a.x + T.beta * (a.x - c.x), a.y + T.beta * (a.y - c.y), a.z + T.beta * (a.z - c.z),
+                       a.w + T.beta * (a.w - c.w));
+}
+__device__ __forceinline__ float zq1(const TvzLaunch& T, const float* p1, const float* p2, long long i) {
+    if (T.stage == 1) return 0.f;
+    const float a = p1[i];
+    if (T.stage == 2) return a;
+    return a + T.beta * (a - p2[i]);
+}
+
+// u = b - w grad^T q at (x..x+3, y) of plane z (x % 4 == 0; all lanes of the warp call it),
+// with q own (3 components) returned for the p update
+__device__ __forceinline__ void zu4(const TvzLaunch& T, int x, int y, int z, bool act, float u[4], float4 q[3]) {
+    const int nx = T.nx;
+    const long long i = (long long)y * nx + x;
+    const ZPlane P = zplane(T, z);
+    float4 qyn = make_float4(0.f, 0.f, 0.f, 0.f), qz1 = qyn, b = qyn;
+    q[0] = q[1] = q[2] = qyn;
+    float qxe = 0.f;
+    if (act) {
+        q[0] = zq4(T, P.p1[0], P.p2[0], i);
+        q[1] = zq4(T, P.p1[1], P.p2[1], i);
+        q[2] = zq4(T, P.p1[2], P.p2[2], i);
+        if (y + 1 < T.ny) qyn = zq4(T, P.p1[1], P.p2[1], i + nx);
+        if (z + 1 < T.nz) {
+            const ZPlane Q = zplane(T, z + 1);
+            qz1 = zq4(T, Q.p1[2], Q.p2[2], i);
+        }
+        b = ld4(P.b + i);
+        if ((threadIdx.x & 31) == 31 && x + 4 < nx) qxe = zq1(T, P.p1[0], P.p2[0], i + 4);
+    }
+    float qx4 = __shfl_down_sync(0xffffffffu, q[0].x, 1);
+    if ((threadIdx.x & 31) == 31) qx4 = qxe;
+    if (!act) {
+        u[0] = u[1] = u[2] = u[3] = 0.f;
+        return;
+    }
+    const float qxa[5] = {q[0].x, q[0].y, q[0].z, q[0].w, x + 4 < nx ? qx4 : 0.f};
+    const float qya[4] = {q[1].x, q[1].y, q[1].z, q[1].w}, qyb[4] = {qyn.x, qyn.y, qyn.z, qyn.w};
+    const float qza[4] = {q[2].x, q[2].y, q[2].z, q[2].w}, qzb[4] = {qz1.x, qz1.y, qz1.z, qz1.w};
+    const float ba[4] = {b.x, b.y, b.z, b.w};
+    const float cy = y >= 1 ? 1.f : 0.f, cz = z >= 1 ? 1.f : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float t = (x + k >= 1 ? qxa[k] : 0.f) - qxa[k + 1];
+        t += cy * qya[k] - qyb[k] + cz * qza[k] - qzb[k];
+        u[k] = fmaf(-T.w, t, ba[k]);
+    }
+}
+// scalar u at (x, y) of plane z (the helper lanes' halo column x0 - 1)
+__device__ __forceinline__ float zu1(const TvzLaunch& T, int x, int y, int z) {
+    const int nx = T.nx;
+    const long long i = (long long)y * nx + x;
+    const ZPlane P = zplane(T, z);
+    float t = 0.f;
+    if (x >= 1) t += zq1(T, P.p1[0], P.p2[0], i);
+    if (x + 1 < nx) t -= zq1(T, P.p1[0], P.p2[0], i + 1);
+    if (y >= 1) t += zq1(T, P.p1[1], P.p2[1], i);
+    if (y + 1 < T.ny) t -= zq1(T, P.p1[1], P.p2[1], i + nx);
+    if (z >= 1) t += zq1(T, P.p1[2], P.p2[2], i);
+    if (z + 1 < T.nz) {
+        const ZPlane Q = zplane(T, z + 1);
+        t -= zq1(T, Q.p1[2], Q.p2[2], i);
+    }
+    return fmaf(-T.w, t, P.b[i]);
+}
+
+// CTA: warp 0 = the halo row y0 - 1, warps 1..TY = output rows y0..y0+TY-1 (4 x voxels per
+// lane, 128 per row), warp TY + 1 = helper lanes for the halo column x0 - 1; the CTA walks
+// planes zs..zs+zc-1 with u(z-1) of its output rows in registers (a prologue evaluates
+// u(zs-1)).  Per plane: every warp evaluates u on its row, one barrier, the output rows
+// project q + s grad u onto the unit ball and write p_k, a second barrier before the shared
+// u rows are overwritten.
+template <int TY>
+__global__ void __launch_bounds__((TY + 2) * 32, 4) k_tv_fgp_z(const TvzLaunch T) {
+    constexpr int RS = TV4_TX + 8;
+    __shared__ __align__(16) float su[TY + 1][RS];   // slot 4 + (x - x0) <-> x; slot 3 <-> x0 - 1
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x0 = blockIdx.x * TV4_TX, y0 = blockIdx.y * TY;
+    const int zs = T.z0 + blockIdx.z * T.zc, ze = min(zs + T.zc, T.z1);
+    const bool helper = warp > TY;
+    const int row = helper ? 0 : warp;
+    const int y = helper ? y0 + lane : y0 + row - 1, x = x0 + 4 * lane;
+    const bool act = !helper && y >= 0 && y < T.ny && x < T.nx;
+    const bool out = act && row >= 1;
+    const long long plane = (long long)T.nx * T.ny;
+    float uprev[4] = {0.f, 0.f, 0.f, 0.f};
+    if (!helper && row >= 1 && zs >= 1) {          // u(zs - 1) of the output rows
+        float4 qd[3];
+        zu4(T, x, y, zs - 1, out, uprev, qd);
+    }
+    for (int z = zs; z < ze; ++z) {
+        float u[4] = {0.f, 0.f, 0.f, 0.f};
+        float4 q[3];
+        float ul = 0.f;
+        if (helper) {
+            if (lane < TY && x0 >= 1 && y < T.ny) su[lane + 1][3] = zu1(T, x0 - 1, y, z);
+        } else {
+            zu4(T, x, y, z, act, u, q);
+            if (act) *reinterpret_cast<float4*>(&su[row][4 + 4 * lane]) = make_float4(u[0], u[1], u[2], u[3]);
+            ul = __shfl_up_sync(0xffffffffu, u[3], 1);
+        }
+        __syncthreads();
+        if (out) {
+            const float uxm = lane > 0 ? ul : su[row][3];
+            const float4 up = *reinterpret_cast<const float4*>(&su[row - 1][4 + 4 * lane]);
+            const float upa[4] = {up.x, up.y, up.z, up.w};
+            const float qa[3][4] = {{q[0].x, q[0].y, q[0].z, q[0].w}, {q[1].x, q[1].y, q[1].z, q[1].w},
+                                    {q[2].x, q[2].y, q[2].z, q[2].w}};
+            float po[3][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float left = k == 0 ? uxm : u[k - 1];
+                const float gx = x + k >= 1 ? u[k] - left : 0.f;
+                const float gy = y >= 1 ? u[k] - upa[k] : 0.f;
+                const float gz = z >= 1 ? u[k] - uprev[k] : 0.f;
+                const float a0 = qa[0][k] + gx * T.s, a1 = qa[1][k] + gy * T.s, a2 = qa[2][k] + gz * T.s;
+                const float n2 = a0 * a0 + a1 * a1 + a2 * a2;
+                const float inv = n2 > 1.f ? rsqrtf(n2) : 1.f;
+                po[0][k] = a0 * inv;
+                po[1][k] = a1 * inv;
+                po[2][k] = a2 * inv;
+            }
+            const long long i = (long long)(z - T.z0) * plane + (long long)y * T.nx + x;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) st4(T.Pn + c * T.n + i, po[c][0], po[c][1], po[c][2], po[c][3]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) uprev[k] = u[k];
+        __syncthreads();
+    }
+}
+
 // float4 form of k_tv_out (nx % 4 == 0): 4 x voxels per lane, in place (b = x is read only at
 // the lane's own voxels)
 __global__ void __launch_bounds__(256) k_tv_out4(const TvLaunch T, float* out) {
@@ -1127,6 +1299,16 @@ void launch_tv_fgp(const TvLaunch& T, cudaStream_t st) {
                         (unsigned)(T.z1 - T.z0));
         k_tv_fgp<1><<<grid, TV_THREADS, 0, st>>>(T);
     }
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st) {
+    constexpr int TY = 4;
+    const int nzl = T.z1 - T.z0;
+    const dim3 g((unsigned)((T.nx + TV4_TX - 1) / TV4_TX), (unsigned)((T.ny + TY - 1) / TY),
+                 (unsigned)((nzl + T.zc - 1) / T.zc));
+    k_tv_fgp_z<TY><<<g, (TY + 2) * 32, 0, st>>>(T);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }

@@ -563,6 +563,9 @@ def test_trajectory_fuzz(bs, seed):
 @pytest.mark.parametrize("dims,blocks,w,iters", [
     ((45, 20, 36), (1, 1, 4), 0.3, 20),     # fused scalar path (nx % 4 != 0): ragged tiles, 9-plane slabs
     ((64, 64, 64), (1, 1, 2), 0.2, 20),     # fused float4 path: partial 128-wide x tile
+    ((64, 64, 64), (1, 1, 2), 0.2, 1),      # z-marching FGP: k = 1 (q = 0) only
+    ((64, 64, 64), (1, 1, 2), 0.2, 2),      # ... k = 2 (q = p_1; p_0 never read)
+    ((128, 40, 70), (1, 1, 2), 0.3, 3),     # ... k = 3 (first momentum step); 35-plane slabs
     ((136, 20, 24), (1, 1, 3), 0.3, 20),    # fused float4 path: ragged x / y tiles, 3 slabs
     ((64, 48, 1), (1, 1, 1), 0.5, 50),      # fused 2D (nz = 1, L = 8)
     ((24, 16, 20), (2, 2, 2), 0.3, 20),     # octants: the generic two-kernel path
