@@ -1,4 +1,3 @@
-#include <cstdlib>
 // HBM-streaming kernels of the hot path:
 //  * k_block_update: g_hat / g / x step of Algo 1 lines 11-14
 //    fused with the combination of the two BP accumulators (normal + transposed
@@ -8,6 +7,7 @@
 //  * small reductions (EUD of Algo 3, dot products, RMSE) and the FGP TV prox
 //    stencil of Algo 4 line 16 (Eq. 6 backward differences).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -976,8 +976,8 @@ __device__ __forceinline__ float zu1(const TvzLaunch& T, int x, int y, int z) {
 // u(zs-1)).  Per plane: every warp evaluates u on its row, one barrier, the output rows
 // project q + s grad u onto the unit ball and write p_k, a second barrier before the shared
 // u rows are overwritten.
-template <int TY>
-__global__ void __launch_bounds__((TY + 2) * 32, 4) k_tv_fgp_z(const TvzLaunch T) {
+template <int TY, int MINB>
+__global__ void __launch_bounds__((TY + 2) * 32, MINB) k_tv_fgp_z(const TvzLaunch T) {
     constexpr int RS = TV4_TX + 8;
     __shared__ __align__(16) float su[TY + 1][RS];   // slot 4 + (x - x0) <-> x; slot 3 <-> x0 - 1
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1308,7 +1308,12 @@ void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st) {
     const int nzl = T.z1 - T.z0;
     const dim3 g((unsigned)((T.nx + TV4_TX - 1) / TV4_TX), (unsigned)((T.ny + TY - 1) / TY),
                  (unsigned)((nzl + T.zc - 1) / T.zc));
-    k_tv_fgp_z<TY><<<g, (TY + 2) * 32, 0, st>>>(T);
+    static const int minb = [] {
+        const char* e = getenv("BSGD_TV_MINB");
+        return e ? atoi(e) : 4;
+    }();
+    if (minb >= 6) k_tv_fgp_z<TY, 6><<<g, (TY + 2) * 32, 0, st>>>(T);
+    else k_tv_fgp_z<TY, 4><<<g, (TY + 2) * 32, 0, st>>>(T);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
