@@ -1197,7 +1197,9 @@ struct bsgd_ctx_s {
             Z.w = (float)wgt;
             Z.s = (float)(1.0 / (Tl.L * wgt));
             Z.zc = std::max(1, std::min(16, (Tl.z1 - Tl.z0) / 4));
-            if (const char* e = getenv("BSGD_TV_ZC")) Z.zc = std::max(1, atoi(e));   // A/B hook
+            if (const char* e = getenv("BSGD_TV_ZC")) Z.zc = std::max(1, atoi(e));   // A/B hooks
+            Z.pf = 2;
+            if (const char* e = getenv("BSGD_TV_PF")) Z.pf = std::max(0, atoi(e));
             if (world > 1) halo_exchange(x_owned + n - plane, tvz_hp + 6 * plane, plane, false, st);   // b of z0-1
             double s_prev = 1.0;                             // s_{k-1}
             for (int k = 1; k <= iters; ++k) {

@@ -249,6 +249,7 @@ struct TvzLaunch {
     float w, s, beta;          // w = mu lambda, s = 1/(L w), beta = beta_{k-1}
     int stage;                 // 1: k = 1 (q = 0); 2: k = 2 (q = p_1, p_0 = 0 not read); 0: k >= 3
     int zc;                    // planes per CTA
+    int pf;                    // L2 prefetch distance in planes (0 = none)
 };
 void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st);
 

@@ -998,6 +998,19 @@ __global__ void __launch_bounds__((TY + 2) * 32, MINB) k_tv_fgp_z(const TvzLaunc
         float u[4] = {0.f, 0.f, 0.f, 0.f};
         float4 q[3];
         float ul = 0.f;
+        // L2 prefetch of this thread's lines of plane z + pf (the DRAM latency of the next
+        // planes overlaps this plane's work; each plane's own loads then hit L2)
+        const int zp = z + T.pf;
+        if (T.pf > 0 && act && zp < T.z1) {
+            const ZPlane Q = zplane(T, zp);
+            const long long ip = (long long)y * T.nx + x;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (T.stage != 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(Q.p1[c] + ip));
+                if (T.stage == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(Q.p2[c] + ip));
+            }
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(Q.b + ip));
+        }
         if (helper) {
             if (lane < TY && x0 >= 1 && y < T.ny) su[lane + 1][3] = zu1(T, x0 - 1, y, z);
         } else {
