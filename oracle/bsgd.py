@@ -301,9 +301,9 @@ class OracleBSGD:
     (or the given x0)."""
 
     def __init__(self, geom, blocks, M, y, params: Params, row_kind="random",
-                 row_seed=None, tiles=(1, 1), x0=None, x_true=None):
+                 row_seed=None, tiles=(1, 1), x0=None, x_true=None, z_splits=None):
         self.geom = geom
-        self.grid = BlockGrid(geom.dims, blocks)
+        self.grid = BlockGrid(geom.dims, blocks, z_splits)
         self.P = Projector(geom, self.grid)
         self.M, self.N = M, self.grid.N
         self.p = params
@@ -424,8 +424,8 @@ class OracleBSGD:
                    obj=0.5 * float(self.r @ self.r))
         if tiles is not None:
             rec["tiles"] = dict(tiles)
-        if self.x_true is not None:
-            rec["rmse"] = float(np.sqrt(np.mean((self.x - self.x_true) ** 2)))
+        if self.x_true is not None:   # over the volume's voxels (block tails are zero in both)
+            rec["rmse"] = float(np.sqrt(np.sum((self.x - self.x_true) ** 2) / self.grid.n_vox))
         self.log.append(rec)
         return rec
 
@@ -470,7 +470,7 @@ def power_iteration(P: Projector, iters: int = 50, seed: int = 0) -> float:
     with the factor-2 gradient, GD is stable iff mu < 1/sigma_max^2, reading A1)."""
     rng = np.random.default_rng(seed)
     N = P.grid.N
-    v = rng.standard_normal((N, P.grid.bsize))
+    v = rng.standard_normal((N, P.grid.bsize)) * P.grid.mask()
     v /= np.linalg.norm(v)
     views = np.arange(P.g.n_views)
     lam = 0.0
@@ -578,6 +578,6 @@ class OracleBSGDLean:
             for j in range(self.N):
                 d = self.x[j] - self.x_true[j]
                 s += float(d @ d)
-            rec["rmse"] = math.sqrt(s / (self.N * self.grid.bsize))
+            rec["rmse"] = math.sqrt(s / self.grid.n_vox)
         self.log.append(rec)
         return rec

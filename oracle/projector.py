@@ -42,31 +42,49 @@ def _p(a, ct):
 
 
 class BlockGrid:
-    """Equal boxes of a bx x by x bz block grid over the (nx, ny, nz) volume."""
+    """Boxes of a bx x by x bz block grid over the (nx, ny, nz) volume: equal boxes, or, for
+    z-slab grids (1, 1, N), slabs between the given z_splits (0 = s_0 < ... < s_N = nz; the
+    column partition J of Eq. 3, need not be uniform).
+    Block-major arrays are (N, bsize) with bsize the LARGEST block's voxel count: block j's
+    [z][y][x] values fill the first bsizes[j] entries of its row, the rest are zero."""
 
-    def __init__(self, dims, blocks):
+    def __init__(self, dims, blocks, z_splits=None):
         self.dims = tuple(int(v) for v in dims)
         self.blocks = tuple(int(v) for v in blocks)
-        for n, b in zip(self.dims, self.blocks):
-            if b < 1 or n % b:
-                raise ValueError("volume dims must be divisible by the block grid")
-        self.bdims = tuple(n // b for n, b in zip(self.dims, self.blocks))
         self.N = self.blocks[0] * self.blocks[1] * self.blocks[2]
+        if z_splits is None:
+            for n, b in zip(self.dims, self.blocks):
+                if b < 1 or n % b:
+                    raise ValueError("volume dims must be divisible by the block grid")
+            self.z_splits = None
+            self.bdims = tuple(n // b for n, b in zip(self.dims, self.blocks))
+        else:
+            zs = [int(v) for v in z_splits]
+            if self.blocks[:2] != (1, 1) or len(zs) != self.blocks[2] + 1 or zs[0] != 0 or zs[-1] != self.dims[2] \
+                    or any(b <= a for a, b in zip(zs, zs[1:])):
+                raise ValueError("z_splits: a z-slab grid and 0 = s_0 < ... < s_N = nz")
+            self.z_splits = zs
+            self.bdims = (self.dims[0], self.dims[1], max(b - a for a, b in zip(zs, zs[1:])))
         self.bsize = self.bdims[0] * self.bdims[1] * self.bdims[2]
+        self.bsizes = [int(np.prod(self.box(j)[1] - self.box(j)[0])) for j in range(self.N)]
+        self.n_vox = self.dims[0] * self.dims[1] * self.dims[2]
 
     def box(self, j):
+        if self.z_splits is not None:
+            lo = np.array([0, 0, self.z_splits[j]], dtype=np.int32)
+            return lo, np.array([self.dims[0], self.dims[1], self.z_splits[j + 1]], dtype=np.int32)
         bx, by, _ = self.blocks
         jx, jy, jz = j % bx, (j // bx) % by, j // (bx * by)
         lo = np.array([jx * self.bdims[0], jy * self.bdims[1], jz * self.bdims[2]], dtype=np.int32)
         return lo, lo + np.array(self.bdims, dtype=np.int32)
 
     def to_blocks(self, vol):
-        """(nz, ny, nx) volume -> (N, bsize) block-major."""
+        """(nz, ny, nx) volume -> (N, bsize) block-major (zero tail for smaller blocks)."""
         vol = np.asarray(vol).reshape(self.dims[2], self.dims[1], self.dims[0])
-        out = np.empty((self.N, self.bsize), dtype=vol.dtype)
+        out = np.zeros((self.N, self.bsize), dtype=vol.dtype)
         for j in range(self.N):
             lo, hi = self.box(j)
-            out[j] = vol[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]].ravel()
+            out[j, :self.bsizes[j]] = vol[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]].ravel()
         return out
 
     def from_blocks(self, blk):
@@ -74,9 +92,16 @@ class BlockGrid:
         vol = np.empty((self.dims[2], self.dims[1], self.dims[0]), dtype=blk.dtype)
         for j in range(self.N):
             lo, hi = self.box(j)
-            vol[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = blk[j].reshape(
-                self.bdims[2], self.bdims[1], self.bdims[0])
+            vol[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = blk[j, :self.bsizes[j]].reshape(
+                hi[2] - lo[2], hi[1] - lo[1], hi[0] - lo[0])
         return vol
+
+    def mask(self):
+        """(N, bsize) 1.0 on block voxels, 0.0 on the tails of smaller blocks."""
+        m = np.zeros((self.N, self.bsize))
+        for j in range(self.N):
+            m[j, :self.bsizes[j]] = 1.0
+        return m
 
 
 class Projector:
@@ -178,12 +203,10 @@ class Projector:
             views = np.arange(self.g.n_views)
         nrows = len(views) * self.nu * self.nv
         A = np.zeros((nrows, self.g.n_vox))
-        gidx = self.grid.from_blocks(np.arange(self.g.n_vox).reshape(self.grid.N, -1)).ravel()
-        # gidx[global] = block-major flat index; invert
-        inv = np.empty_like(gidx)
-        inv[gidx] = np.arange(gidx.size)
+        # global [z][y][x] index of every block voxel
+        gidx = self.grid.to_blocks(np.arange(self.g.n_vox).reshape(self.g.dims[::-1]))
         for j in range(self.grid.N):
             Aj = self.csr(views, j).toarray()
-            cols = inv[j * self.grid.bsize + np.arange(self.grid.bsize)]
-            A[:, cols] += Aj
+            nb = self.grid.bsizes[j]
+            A[:, gidx[j, :nb]] += Aj[:, :nb]
         return A

@@ -524,3 +524,29 @@ def test_lean_algo1_equals_dense_state(tmp_path, aM, gN):
         assert abs(a["obj"] - b["obj"]) <= 1e-12 * a["obj"]
         assert abs(a["rmse"] - b["rmse"]) <= 1e-12 * a["rmse"]
     assert np.max(np.abs(d.x - lean.x)) <= 1e-13 * np.max(np.abs(d.x))
+
+
+def test_unequal_slabs_gd_closed_form():
+    """alpha = gamma = 1 BSGD over unequal z-slabs is still GD (the partition does not
+    change the full-gradient step): SVD closed form to 1e-10; the RMSE is
+    over the volume's voxels."""
+    p = synth.scaled(synth.PRESETS["cfg3"], 8, n_views=12)
+    g = p.geometry()
+    zs = [0, 1, 4, 5, 8]
+    grid = BlockGrid(g.dims, (1, 1, 4), zs)
+    P = Projector(g, grid)
+    A = P.dense()
+    x_true = synth.rasterise(synth.ellipsoids_world("shepp3d", g.dims), g.dims)
+    y = A @ x_true.ravel()
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    mu = 0.5 / s[0] ** 2
+    o = ob.OracleBSGD(g, (1, 1, 4), 3, y, ob.Params(seed=2, mu=mu, rows_per_epoch=3, cols_per_epoch=4),
+                      x_true=grid.to_blocks(x_true), z_splits=zs)
+    keep = s > 1e-10 * s[0]
+    uy = U.T @ y
+    for k in range(1, 11):
+        rec = o.epoch()
+        xk = (Vt[keep].T * ((1 - (1 - 2 * mu * s[keep] ** 2) ** k) / s[keep])) @ uy[keep]
+        xg = grid.from_blocks(o.x).ravel()
+        assert np.max(np.abs(xg - xk)) <= 1e-10 * np.max(np.abs(xk))
+        assert abs(rec["rmse"] - np.sqrt(np.mean((xg - x_true.ravel()) ** 2))) <= 1e-12
