@@ -323,8 +323,16 @@ def run_ours(args, rank, world, local_rank):
         r, w, nid = bs.dist_from_process_group()
     else:
         r, w, nid = 0, 1, None
+    z_splits = None
+    if args.balanced:   # slab thicknesses with equal ray-voxel intersections
+        fine_n = max(p.N, p.dims[2] // 4)
+        fine = bs.Context.from_geometry(g, (1, 1, fine_n), 1)   # 4-plane candidate slabs, exact visits
+        z_splits = fine.balanced_z_splits(p.N)
+        fine.close()
+        del fine
+        torch.cuda.empty_cache()
     ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=1, tiles=p.tiles,
-                                   rank=r, world=w, nccl_id=nid)
+                                   rank=r, world=w, nccl_id=nid, z_splits=z_splits)
     n_owned = ctx.owned_count * ctx.block_voxels
     # synthetic data shaped like the paper's workload: analytic projections of 32
     # seeded random ellipsoids (replicated y), x0 = 0 (Algo 1 line 1)
@@ -438,6 +446,20 @@ def run_ours(args, rank, world, local_rank):
     # epochs (bsgd_comm_stats, band mode by default); always: the library's host plan of one
     # epoch's exchange at G = 2, 4, 8 for this config (band overlap rows vs the ring allreduce),
     # averaged over the M row blocks
+    # per-slab ray-voxel intersections over all views (the exact COUNT traversal): the load
+    # balance of a G-rank z-slab sharding (N3); balanced slabs with --balanced
+    balance = None
+    try:
+        if world == 1 and p.blocks[:2] == (1, 1):
+            v = ctx.visit_table().sum(axis=(1, 2)).astype(np.float64)
+            shares = v / v.sum()
+            balance = {"z_splits": [int(ctx.block_box(j)[0][2]) for j in range(p.N)] + [int(p.dims[2])],
+                       "slab_visit_shares": [round(float(x), 5) for x in shares],
+                       "visit_spread": float((v.max() - v.min()) / v.mean()),
+                       "ideal_speedup": {str(G): float(1.0 / max(shares.reshape(G, -1).sum(axis=1)))
+                                         for G in (2, 4, 8) if p.N % G == 0}}
+    except Exception as exc:   # noqa: BLE001 -- auxiliary
+        balance = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     exchange = {"plan_per_epoch": {}}
     try:
         for G in (2, 4, 8):
@@ -482,7 +504,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": workload(p) + (f" [Eq. 8 schedule at NodeNum = {world}: alpha*M = "
                                               f"{res.sel_rows.shape[1]}, gamma*N = {res.sel_cols.shape[1]}, "
                                               "columns stratified by owner]" if args.eq8 else "")
-                   + (" [BSGD_DETERMINISTIC: fixed-point BP]" if args.det else ""),
+                   + (" [BSGD_DETERMINISTIC: fixed-point BP]" if args.det else "")
+                   + (" [work-balanced slab thicknesses]" if args.balanced else ""),
                    "global_batch": int(res.sel_rows.shape[1]) * (g.n_views // p.M),
                    "parallelism": f"z-slab{world}" if p.blocks[:2] == (1, 1) else f"blocks{world}",
                    "l2": ("inputs larger than L2 (537 MB slabs, 3.0 GB y); no flush needed" if p.name == "cfg5"
@@ -492,6 +515,7 @@ def run_ours(args, rank, world, local_rank):
         "phase_ms": {"fp": fp_ms, "residual_allreduce": res_ms, "bp": bp_ms, "step": st_ms},
         "allreduce": allreduce,
         "exchange": exchange,
+        "balance": balance,
         "roofline": {"bound": "hbm",
                      "kernel": "projector pair k_project3<FP> + k_project3<BP> (+ k_project2 steep-only companions)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -596,6 +620,8 @@ def main():
     ap.add_argument("--eq8", action="store_true",
                     help="Eq. 8 schedule (gamma N = G, alpha M from Eq. 8), stratified by owner: weak scaling")
     ap.add_argument("--cheap-data", action="store_true", help="uniform random y instead of analytic projections")
+    ap.add_argument("--balanced", action="store_true",
+                    help="work-balanced z-slab thicknesses (bsgd_balanced_z_splits; SURVEY §8f N3)")
     ap.add_argument("--dry-run", action="store_true", help="multi-rank launch check on CPU (gloo), no GPU work")
     ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="workload (cfg5 = the BASELINE.json headline; the others for DESIGN tables)")

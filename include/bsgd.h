@@ -140,6 +140,31 @@ bsgd_status bsgd_nccl_unique_id(uint8_t* out128);
 bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks,
                         bsgd_row_grid rows, const bsgd_dist* dist /* NULL = single GPU */,
                         const bsgd_alloc* alloc /* NULL = cudaMalloc */, bsgd_ctx* out);
+/* Options of bsgd_create_ex.
+ * z_splits: host [bz + 1] plane indices 0 = s_0 < s_1 < ... < s_bz = nz, or NULL.  Column
+ *   blocks J_j of Eq. 3 need not be equal: with a z-slab grid (1, 1, bz),
+ *   block j is the slab of planes [s_j, s_{j+1}) (slab thicknesses chosen so
+ *   every rank traverses the same number of ray-voxel intersections, bsgd_balanced_z_splits).
+ *   Block-major buffers (x_owned, x_true, g-hat / g of bsgd_get_state) then keep the stride of
+ *   the THICKEST slab (bsgd_info.block_voxels): block j's [z][y][x] values, then zeros to the
+ *   end of its row (inputs must carry zero tails; outputs keep them).                      */
+typedef struct {
+    const int32_t* z_splits;
+} bsgd_create_opts;
+/* bsgd_create with options (NULL opts = bsgd_create).  Errors as bsgd_create, plus
+ * BSGD_E_PARTITION for z_splits on a non-slab grid, not running 0..nz or not increasing.   */
+bsgd_status bsgd_create_ex(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks,
+                           bsgd_row_grid rows, const bsgd_dist* dist, const bsgd_alloc* alloc,
+                           const bsgd_create_opts* opts, bsgd_ctx* out);
+/* Box of column block j in grid coordinates: lo [3], hi [3] (half-open).                  */
+bsgd_status bsgd_block_box(bsgd_ctx ctx, int32_t j, int32_t* lo, int32_t* hi);
+/* Work-balanced z-splits: ctx must be a one-rank z-slab context whose slabs
+ * are the candidate boundaries (e.g. nz/8 slabs of 8 planes); from its exact visit table (the
+ * COUNT traversal of every view, bsgd_visit_table) it picks splits [n_slabs + 1] so that the
+ * cumulative ray-voxel intersections of slab k end nearest to (k+1)/n_slabs of the total.
+ * Synchronises the stream.  Errors: BSGD_E_PARTITION (non-slab grid, world > 1, n_slabs > N),
+ * BSGD_E_CONTRACT (NULL, n_slabs < 1).                                                    */
+bsgd_status bsgd_balanced_z_splits(bsgd_ctx ctx, int32_t n_slabs, int32_t* splits, void* stream);
 void bsgd_destroy(bsgd_ctx ctx);
 
 typedef struct {

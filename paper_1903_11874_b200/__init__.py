@@ -60,6 +60,10 @@ class RowGrid(C.Structure):
                 ("tiles_v", C.c_int32)]
 
 
+class CreateOpts(C.Structure):
+    _fields_ = [("z_splits", C.POINTER(C.c_int32))]
+
+
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.POINTER(C.c_uint8)),
                 ("vgroup", C.c_void_p)]
@@ -123,6 +127,9 @@ SIGS = {
     "bsgd_owned_blocks": ([C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
     "bsgd_nccl_unique_id": ([P(C.c_uint8)], C.c_int),
     "bsgd_create": ([P(Geometry), Dims, BlockGrid, RowGrid, P(Dist), P(Alloc), P(_ctx)], C.c_int),
+    "bsgd_create_ex": ([P(Geometry), Dims, BlockGrid, RowGrid, P(Dist), P(Alloc), P(CreateOpts), P(_ctx)], C.c_int),
+    "bsgd_block_box": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+    "bsgd_balanced_z_splits": ([_ctx, C.c_int32, P(C.c_int32), C.c_void_p], C.c_int),
     "bsgd_destroy": ([_ctx], None),
     "bsgd_vgroup_create": ([C.c_int32, P(C.c_void_p)], C.c_int),
     "bsgd_vgroup_destroy": ([C.c_void_p], None),
@@ -324,7 +331,7 @@ class Context:
     """One BSGD problem on this process's GPU (bsgd_create ... bsgd_destroy)."""
 
     def __init__(self, beam, vecs, det, dims, blocks, M, kind=0, row_seed=0, tiles=(1, 1),
-                 rank=0, world=1, nccl_id=None, torch_alloc=True, device=None, vgroup=None):
+                 rank=0, world=1, nccl_id=None, torch_alloc=True, device=None, vgroup=None, z_splits=None):
         import torch
         self.device = torch.cuda.current_device() if device is None else device
         self.vecs = np.ascontiguousarray(vecs, dtype=np.float64)
@@ -342,10 +349,15 @@ class Context:
         self._alloc = _TorchAllocator(self.device) if torch_alloc else None
         h = _ctx()
         with torch.cuda.device(self.device):
-            _check(_lib.bsgd_create(C.byref(g), Dims(*dims), BlockGrid(*blocks),
-                                    RowGrid(M, int(kind), row_seed, int(tiles[0]), int(tiles[1])),
-                                    C.byref(dist) if dist else None,
-                                    C.byref(self._alloc.struct) if self._alloc else None, C.byref(h)))
+            opts = None
+            if z_splits is not None:   # unequal z-slabs (bsgd_create_opts.z_splits)
+                self._zsp, zp = _i32(z_splits)
+                opts = CreateOpts(zp)
+            _check(_lib.bsgd_create_ex(C.byref(g), Dims(*dims), BlockGrid(*blocks),
+                                       RowGrid(M, int(kind), row_seed, int(tiles[0]), int(tiles[1])),
+                                       C.byref(dist) if dist else None,
+                                       C.byref(self._alloc.struct) if self._alloc else None,
+                                       C.byref(opts) if opts else None, C.byref(h)))
         self.h = h
         inf = Info()
         _check(_lib.bsgd_get_info(self.h, C.byref(inf)), self.h)
@@ -375,6 +387,19 @@ class Context:
 
     def _c(self, code):
         _check(code, self.h)
+
+    def block_box(self, j):
+        """(lo, hi) of column block j in grid coordinates (bsgd_block_box)."""
+        lo, hi = (C.c_int32 * 3)(), (C.c_int32 * 3)()
+        self._c(_lib.bsgd_block_box(self.h, int(j), lo, hi))
+        return tuple(lo), tuple(hi)
+
+    def balanced_z_splits(self, n_slabs, stream=None):
+        """Work-balanced z-splits for n_slabs slabs from this (one-rank, z-slab) context's
+        exact visit table (bsgd_balanced_z_splits)."""
+        out = (C.c_int32 * (int(n_slabs) + 1))()
+        self._c(_lib.bsgd_balanced_z_splits(self.h, int(n_slabs), out, _stream(stream)))
+        return list(out)
 
     def row_block_views(self, i) -> list[int]:
         n = C.c_int32()

@@ -90,6 +90,11 @@ struct bsgd_ctx_s {
     int beam = 0, n_views = 0, nu = 0, nv = 0;
     std::vector<double> vecs;
     int dims[3] = {0, 0, 0}, bgrid[3] = {1, 1, 1}, bd[3] = {0, 0, 0};
+    // Unequal z-slabs (work-balanced slabs): block j spans planes
+    // [zsp[j], zsp[j+1]); bd[2] is then the thickest slab and every block-major buffer keeps
+    // the stride bsize of that slab (a thinner slab's row ends in zeros nobody reads).
+    bool zsplit = false;
+    std::vector<int> zsp;
     int N = 1, M = 1, kind = 0, tiles_u = 1, tiles_v = 1, T = 1;
     uint64_t row_seed = 0;
     int rank = 0, world = 1, first = 0, s = 1;
@@ -140,7 +145,8 @@ struct bsgd_ctx_s {
     float *accN = nullptr, *accT = nullptr, *pc = nullptr;
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
-          *tv_q2 = nullptr, *tv_hp = nullptr, *tv_pk = nullptr, *tvz_hp = nullptr, *tvz_hn = nullptr;
+          *tv_q2 = nullptr, *tv_hp = nullptr, *tv_pk = nullptr, *tvz_hp = nullptr, *tvz_hn = nullptr,
+          *tv_xc = nullptr;
     float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
@@ -275,7 +281,17 @@ struct bsgd_ctx_s {
         k.R = R;
         return k;
     }
+    int nz_of(int j) const { return zsplit ? zsp[j + 1] - zsp[j] : bd[2]; }
+    long long vox_of(int j) const { return (long long)bd[0] * bd[1] * nz_of(j); }
     void box(int j, int lo[3], int hi[3]) const {
+        if (zsplit) {
+            lo[0] = lo[1] = 0;
+            lo[2] = zsp[j];
+            hi[0] = dims[0];
+            hi[1] = dims[1];
+            hi[2] = zsp[j + 1];
+            return;
+        }
         int jx = j % bgrid[0], jy = (j / bgrid[0]) % bgrid[1], jz = j / (bgrid[0] * bgrid[1]);
         lo[0] = jx * bd[0]; lo[1] = jy * bd[1]; lo[2] = jz * bd[2];
         for (int c = 0; c < 3; ++c) hi[c] = lo[c] + bd[c];
@@ -451,7 +467,7 @@ struct bsgd_ctx_s {
                 cudaStream_t st, float* accN_ = nullptr, float* accT_ = nullptr, float* xT_ = nullptr,
                 int ghat_i = 0, float* xN_ = nullptr) {
         UpdLaunch U;
-        U.bd[0] = bd[0]; U.bd[1] = bd[1]; U.bd[2] = bd[2];
+        U.bd[0] = bd[0]; U.bd[1] = bd[1]; U.bd[2] = nz_of(first + b);
         U.rowN = rowN; U.planeN = planeN; U.rowT = rowT; U.planeT = planeT;
         U.accN = accN_ ? accN_ : pN(accN, b);
         U.accT = accT_ ? accT_ : pT(accT, b);
@@ -1106,8 +1122,20 @@ struct bsgd_ctx_s {
     bool tv_shardable() const {
         return world == 1 || (bgrid[0] == 1 && bgrid[1] == 1) || s % (bgrid[0] * bgrid[1]) == 0;
     }
-    int owned_z0() const { return (first / (bgrid[0] * bgrid[1])) * bd[2]; }
-    int owned_z1() const { return ((first + s) / (bgrid[0] * bgrid[1])) * bd[2]; }
+    int owned_z0() const { return zsplit ? zsp[first] : (first / (bgrid[0] * bgrid[1])) * bd[2]; }
+    int owned_z1() const { return zsplit ? zsp[first + s] : ((first + s) / (bgrid[0] * bgrid[1])) * bd[2]; }
+    // Unequal slabs: the TV stencil runs on the owned planes packed contiguously (tv_xc);
+    // copy the blocks' rows in / out (their real parts; the zero tails stay as they are)
+    void zsplit_pack(const float* x_owned, float* xc, bool in, cudaStream_t st) {
+        long long o = 0;
+        for (int b = 0; b < s; ++b) {
+            const long long nb = vox_of(first + b);
+            if (in) BSGD_CUDA(cudaMemcpyAsync(xc + o, x_owned + b * bsize, sizeof(float) * nb, cudaMemcpyDeviceToDevice, st));
+            else BSGD_CUDA(cudaMemcpyAsync((float*)x_owned + b * bsize, xc + o, sizeof(float) * nb, cudaMemcpyDeviceToDevice, st));
+            o += nb;
+        }
+    }
+    long long owned_real() const { return (long long)dims[0] * dims[1] * (owned_z1() - owned_z0()); }
     // Global plane z (inside the owned z-range) of an owned block-major field as a contiguous
     // [y][x] plane: in place for z-slab layouts, else gathered from the bx*by blocks of its
     // layer into tv_pk (stream-ordered: the previous exchange reading tv_pk is complete).
@@ -1131,7 +1159,18 @@ struct bsgd_ctx_s {
     // one dual field (tv_q, double-buffered on the fused path)
     void tv_prox(float* x_owned, double wgt, int iters, cudaStream_t st, int method = 0) {
         NvtxRange nv_("tv prox (Algo 4 l.16)");
-        const long long n = (long long)s * bsize;
+        if (wgt == 0.0 || iters <= 0) return;
+        if (zsplit) {
+            if (!tv_xc) tv_xc = dnew<float>(owned_real(), false);
+            zsplit_pack(x_owned, tv_xc, true, st);
+            tv_prox_on(tv_xc, owned_real(), wgt, iters, st, method);
+            zsplit_pack(x_owned, tv_xc, false, st);
+            return;
+        }
+        tv_prox_on(x_owned, (long long)s * bsize, wgt, iters, st, method);
+    }
+    // the prox on an owned volume whose blocks are stored back to back (n voxels)
+    void tv_prox_on(float* x_owned, long long n, double wgt, int iters, cudaStream_t st, int method) {
         // z-slab layouts (the owned volume is one [z][y][x] array) take the fused iteration
         const bool fused = bgrid[0] == 1 && bgrid[1] == 1;
         const long long plane = (long long)dims[0] * dims[1];
@@ -1292,7 +1331,12 @@ struct bsgd_ctx_s {
 
     // TV(x) (Eq. 6) of the whole volume into *d_out (device; summed over ranks)
     void tv_value(const float* x_owned, double* d_out, cudaStream_t st) {
-        const long long n = (long long)s * bsize, plane = (long long)dims[0] * dims[1];
+        if (zsplit) {
+            if (!tv_xc) tv_xc = dnew<float>(owned_real(), false);
+            zsplit_pack(x_owned, tv_xc, true, st);
+            x_owned = tv_xc;
+        }
+        const long long n = zsplit ? owned_real() : (long long)s * bsize, plane = (long long)dims[0] * dims[1];
         if (!tv_shardable())
             fail(BSGD_E_PARTITION, "sharded TV needs whole z-layers of blocks per rank (N/G divisible by bx*by)");
         if (!tvv_halo) tvv_halo = dnew<float>(plane);
@@ -1487,8 +1531,15 @@ bsgd_status bsgd_nccl_unique_id(uint8_t* out128) {
 
 bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks, bsgd_row_grid rowg,
                         const bsgd_dist* dist, const bsgd_alloc* alloc, bsgd_ctx* out) {
+    return bsgd_create_ex(geom, dims, blocks, rowg, dist, alloc, nullptr, out);
+}
+
+bsgd_status bsgd_create_ex(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks, bsgd_row_grid rowg,
+                           const bsgd_dist* dist, const bsgd_alloc* alloc, const bsgd_create_opts* opts,
+                           bsgd_ctx* out) {
     std::unique_ptr<bsgd_ctx_s> c(new bsgd_ctx_s());
     bsgd_status st = guard(nullptr, [&] {
+        const int32_t* zsp_in = opts ? opts->z_splits : nullptr;
         if (!geom || !out || !geom->vecs) fail(BSGD_E_GEOMETRY, "NULL geometry");
         if (geom->n_views < 1 || geom->det_u < 1 || geom->det_v < 1) fail(BSGD_E_GEOMETRY, "bad counts");
         if (geom->beam < 0 || geom->beam > 2) fail(BSGD_E_GEOMETRY, "unknown beam");
@@ -1496,8 +1547,14 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
             if (!isfinite(geom->vecs[k])) fail(BSGD_E_GEOMETRY, "non-finite geometry vector");
         if (dims.nx < 1 || dims.ny < 1 || dims.nz < 1) fail(BSGD_E_PARTITION, "bad volume dims");
         if (blocks.bx < 1 || blocks.by < 1 || blocks.bz < 1 || dims.nx % blocks.bx || dims.ny % blocks.by ||
-            dims.nz % blocks.bz)
+            (!zsp_in && dims.nz % blocks.bz))
             fail(BSGD_E_PARTITION, "volume dims must be divisible by the block grid");
+        if (zsp_in) {
+            if (blocks.bx != 1 || blocks.by != 1) fail(BSGD_E_PARTITION, "z_splits need a z-slab grid (1, 1, N)");
+            if (zsp_in[0] != 0 || zsp_in[blocks.bz] != dims.nz) fail(BSGD_E_PARTITION, "z_splits must run from 0 to nz");
+            for (int k = 0; k < blocks.bz; ++k)
+                if (zsp_in[k + 1] <= zsp_in[k]) fail(BSGD_E_PARTITION, "z_splits must increase strictly");
+        }
         if (rowg.M < 1 || rowg.M > geom->n_views) fail(BSGD_E_PARTITION, "M must be in [1, n_views]");
         if (rowg.kind < 0 || rowg.kind > 2) fail(BSGD_E_PARTITION, "unknown row partition kind");
         if (rowg.tiles_u < 1 || rowg.tiles_v < 1 || rowg.tiles_u > geom->det_u || rowg.tiles_v > geom->det_v)
@@ -1510,6 +1567,12 @@ bsgd_status bsgd_create(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_gr
         c->dims[0] = dims.nx; c->dims[1] = dims.ny; c->dims[2] = dims.nz;
         c->bgrid[0] = blocks.bx; c->bgrid[1] = blocks.by; c->bgrid[2] = blocks.bz;
         for (int k = 0; k < 3; ++k) c->bd[k] = c->dims[k] / c->bgrid[k];
+        if (zsp_in) {   // unequal z-slabs: blocks keep the stride of the thickest one
+            c->zsplit = true;
+            c->zsp.assign(zsp_in, zsp_in + blocks.bz + 1);
+            c->bd[2] = 0;
+            for (int k = 0; k < blocks.bz; ++k) c->bd[2] = std::max(c->bd[2], c->zsp[k + 1] - c->zsp[k]);
+        }
         c->N = blocks.bx * blocks.by * blocks.bz;
         c->M = rowg.M;
         c->kind = rowg.kind;
@@ -2122,7 +2185,7 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
         if (!htv.empty()) BSGD_CUDA(cudaMemcpyAsync(htv.data(), c->d_tvv, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
         BSGD_CUDA(cudaStreamSynchronize(st));
         if (log) {
-            const double nvox = (double)c->bsize * c->N;
+            const double nvox = (double)c->dims[0] * c->dims[1] * c->dims[2];   // the volume's voxels
             for (int e = 0; e < E; ++e) {
                 if (log->obj) log->obj[e] = hl[2 * e];
                 if (log->rmse) log->rmse[e] = xt ? sqrt(hl[2 * e + 1] / nvox) : NAN;
@@ -2283,6 +2346,53 @@ bsgd_status bsgd_exchange_plan(bsgd_ctx c, int32_t world, int32_t n_sel, const i
     });
 }
 
+bsgd_status bsgd_block_box(bsgd_ctx c, int32_t j, int32_t* lo, int32_t* hi) {
+    return guard(c, [&] {
+        if (!c || !lo || !hi || j < 0 || j >= c->N) fail(BSGD_E_CONTRACT, "bad arguments");
+        int l[3], h[3];
+        c->box(j, l, h);
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = l[k];
+            hi[k] = h[k];
+        }
+    });
+}
+
+bsgd_status bsgd_balanced_z_splits(bsgd_ctx c, int32_t n_slabs, int32_t* splits, void* stream) {
+    return guard(c, [&] {
+        if (!c || !splits || n_slabs < 1) fail(BSGD_E_CONTRACT, "bad arguments");
+        if (c->bgrid[0] != 1 || c->bgrid[1] != 1 || c->world != 1)
+            fail(BSGD_E_PARTITION, "needs a one-rank z-slab context (its slabs are the candidate boundaries)");
+        if (n_slabs > c->N) fail(BSGD_E_PARTITION, "more slabs than the context's slabs");
+        cudaStream_t st = S(stream);
+        Ordered order_(c, st);
+        c->ensure_visit_table(st);
+        // visits of every view through each of the context's slabs (the COUNT traversal)
+        std::vector<double> cum(c->N + 1, 0.0);
+        for (int b = 0; b < c->N; ++b) {
+            double v = 0.0;
+            for (size_t k = (size_t)b * c->n_views * c->T; k < (size_t)(b + 1) * c->n_views * c->T; ++k)
+                v += (double)c->vtab[k];
+            cum[b + 1] = cum[b] + v;
+        }
+        // split k at the slab boundary whose cumulative visit count is nearest to k/n of the
+        // total (each slab at least one of the context's slabs)
+        int lo_b = 0;
+        splits[0] = 0;
+        for (int k = 1; k < n_slabs; ++k) {
+            const double target = cum[c->N] * k / n_slabs;
+            int best = lo_b + 1;
+            for (int b = lo_b + 1; b <= c->N - (n_slabs - k); ++b)
+                if (fabs(cum[b] - target) < fabs(cum[best] - target)) best = b;
+            int l[3], h[3];
+            c->box(best, l, h);
+            splits[k] = l[2];
+            lo_b = best;
+        }
+        splits[n_slabs] = c->dims[2];
+    });
+}
+
 bsgd_status bsgd_comm_stats(bsgd_ctx c, uint64_t* bytes_sent, uint64_t* messages, int32_t* band_mode) {
     return guard(c, [&] {
         if (!c || !bytes_sent || !messages) fail(BSGD_E_CONTRACT, "bad arguments");
@@ -2305,6 +2415,12 @@ bsgd_status bsgd_power_iteration(bsgd_ctx c, int32_t iters, uint64_t seed, doubl
             c->pw_proj = c->dnew<float>(c->n_rays, false);
         }
         launch_fill_random(c->pw_v, sb, seed + 1000003ull * (uint64_t)c->rank, st);
+        if (c->zsplit)   // the tails of thinner slabs are not voxels
+            for (int b = 0; b < c->s; ++b) {
+                const long long nb = c->vox_of(c->first + b);
+                if (nb < c->bsize)
+                    BSGD_CUDA(cudaMemsetAsync(c->pw_v + b * c->bsize + nb, 0, sizeof(float) * (c->bsize - nb), st));
+            }
         BSGD_CUDA(cudaMemsetAsync(c->d_red, 0, 3 * sizeof(double), st));
         launch_dot3(c->pw_v, c->pw_v, sb, c->d_red, st);
         c->allreduce_d(c->d_red, 1, st);

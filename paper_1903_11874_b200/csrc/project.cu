@@ -380,9 +380,13 @@ __device__ __forceinline__ void scatter3(bool in, unsigned m_or, unsigned m_and,
 }
 
 // D -= K on the 64-bit plane distance; returns ~0u when it borrows (a plane is crossed).
+// The result goes to a new register (Dn) rather than back into D: the caller still reads D
+// (the crossing point D / K), and an in-place subtraction made ptxas copy D every slice.
 __device__ __forceinline__ unsigned sub_borrow(unsigned long long& D, unsigned long long K) {
     unsigned m;
-    asm("sub.cc.u64 %0, %0, %2;\n\tsubc.u32 %1, 0, 0;" : "+l"(D), "=r"(m) : "l"(K));
+    unsigned long long Dn;
+    asm("sub.cc.u64 %0, %2, %3;\n\tsubc.u32 %1, 0, 0;" : "=l"(Dn), "=r"(m) : "l"(D), "l"(K));
+    D = Dn;
     return m;
 }
 

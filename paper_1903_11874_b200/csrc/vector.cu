@@ -480,6 +480,11 @@ struct Vox {
 };
 
 __device__ __forceinline__ Vox owned_coords(const TvLaunch& T, long long o) {
+    if (T.bgrid[0] == 1 && T.bgrid[1] == 1) {   // z-slabs (any thicknesses): planes z0.. back to back
+        const long long plane = (long long)T.dims[0] * T.dims[1];
+        const long long l = o % plane;
+        return {(int)(l % T.dims[0]), (int)(l / T.dims[0]), T.z0 + (int)(o / plane)};
+    }
     const long long bs = (long long)T.bdims[0] * T.bdims[1] * T.bdims[2];
     const long long blk = T.block0 + o / bs;
     const long long l = o % bs;
@@ -492,6 +497,10 @@ __device__ __forceinline__ Vox owned_coords(const TvLaunch& T, long long o) {
 
 // owned index of global voxel (x,y,z); -1 if outside the owned range
 __device__ __forceinline__ long long owned_index(const TvLaunch& T, int x, int y, int z) {
+    if (T.bgrid[0] == 1 && T.bgrid[1] == 1) {   // z-slabs: the owned planes [z0, z1) back to back
+        if (z < T.z0 || z >= T.z1) return -1;
+        return ((long long)(z - T.z0) * T.dims[1] + y) * T.dims[0] + x;
+    }
     const int jx = x / T.bdims[0], jy = y / T.bdims[1], jz = z / T.bdims[2];
     const long long blk = ((long long)jz * T.bgrid[1] + jy) * T.bgrid[0] + jx;
     const long long rel = blk - T.block0;

@@ -222,3 +222,119 @@ def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
     band = sum(o_[2]["bytes_sent"] for o_ in runs["band"])
     full = sum(o_[2]["bytes_sent"] for o_ in runs["full"])
     assert 0 < band and 4 * band <= full, (band, full)
+
+
+# ----------------------------------------------------------------- unequal z-slabs (N3)
+def _zs_problem(K=48, n_views=40):
+    return problem("cfg4", K=K, n_views=n_views)
+
+
+def test_unequal_slabs_operator_parity(bs):
+    """FP per ray / BP per voxel on unequal z-slabs (bsgd_create_ex z_splits) against the
+    oracle's operators on the same slabs (thin, thick and one-plane slabs)."""
+    p, g, vol32, y = _zs_problem()
+    zs = [0, 5, 6, 20, 33, 48]
+    grid = BlockGrid(g.dims, (1, 1, 5), zs)
+    P = Projector(g, grid)
+    ctx = bs.Context.from_geometry(g, (1, 1, 5), 2, z_splits=zs)
+    assert [ctx.block_box(j) for j in range(5)] == [((0, 0, zs[j]), (48, 48, zs[j + 1])) for j in range(5)]
+    assert ctx.block_voxels == grid.bsize
+    rng = np.random.default_rng(4)
+    views = np.arange(0, 40, 3)
+    rows = P.rows_of(views)
+    for j in range(5):
+        x = (rng.random(grid.bsize) * grid.mask()[j]).astype(np.float32)
+        proj = torch.zeros(g.n_rays, device="cuda")
+        ctx.forward(views, j, torch.from_numpy(x).cuda(), proj)
+        got = proj.cpu().numpy().astype(np.float64)[rows]
+        ref = P.fp(views, j, x.astype(np.float64))[rows]
+        assert np.all(np.abs(got - ref) <= 1e-5 * ref + 1e-7 * float(x.max())), j
+        r = np.zeros(g.n_rays, dtype=np.float32)
+        r[rows] = rng.standard_normal(len(rows)).astype(np.float32)
+        gb = torch.zeros(grid.bsize, device="cuda")
+        ctx.back(views, j, torch.from_numpy(r).cuda(), gb, scale=1.0)
+        gg = gb.cpu().numpy().astype(np.float64)
+        gref = P.bp(views, j, r.astype(np.float64))
+        gabs = P.bp(views, j, np.abs(r).astype(np.float64))
+        assert np.all(np.abs(gg - gref) <= 1e-5 * gabs + 1e-7 * float(np.abs(r).max())), j
+        assert np.all(gg[grid.bsizes[j]:] == 0.0)                  # nothing in the row's tail
+    ctx.close()
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_unequal_slabs_trajectory(bs, G):
+    """BSGD-TV (Algo 4) + Algo 3 + IM (Algo 2) on unequal z-slabs vs the oracle on the same
+    partition, on one rank and on 2 virtual ranks (band exchange, TV halos of the packed
+    owned planes)."""
+    p, g, vol32, y = _zs_problem()
+    zs = [0, 7, 15, 22, 26, 31, 36, 41, 48]
+    grid = BlockGrid(g.dims, (1, 1, 8), zs)
+    P = Projector(g, grid)
+    mu = float(np.float32(2.0 / ob.power_iteration(P, 30, seed=1)))
+    E = 24
+    xtb = grid.to_blocks(vol32)
+    prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=3, total_epochs=E, tv=True, auto_mu=True,
+                    lam=0.1, tv_period=3, im=True)
+    o = ob.OracleBSGD(g, (1, 1, 8), p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11,
+                      tiles=p.tiles, x_true=xtb.astype(np.float64), z_splits=zs)
+    for _ in range(E):
+        o.epoch()
+    group = bs.VirtualGroup(G) if G > 1 else None
+    ctxs = [bs.Context.from_geometry(g, (1, 1, 8), p.M, kind="random", row_seed=11, tiles=p.tiles, rank=r, world=G,
+                                     vgroup=group, z_splits=zs) for r in range(G)]
+    nb = 8 // G
+
+    def run(r, s):
+        yd = torch.from_numpy(y).cuda()
+        xd = torch.zeros(nb * grid.bsize, device="cuda")
+        xt = torch.from_numpy(xtb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+        res = ctxs[r].run(yd, xd, epochs=E, mu0=mu, seed=3, x_true=xt, rows_per_epoch=1, cols_per_epoch=3,
+                          flags=bs.TV | bs.AUTO_MU | bs.IS, lam=0.1, tv_iters=20, tv_period=3, stream=s)
+        s.synchronize()
+        return res, xd.cpu().numpy().astype(np.float64)
+
+    out = _ranks(bs, G, run)
+    for c in ctxs:
+        c.close()
+    if group:
+        group.close()
+    res0 = out[0][0]
+    assert [r_["cols"] for r_ in o.log] == res0.sel_cols.tolist()
+    obj = np.array([r_["obj"] for r_ in o.log])
+    rmse = np.array([r_["rmse"] for r_ in o.log])
+    assert np.allclose(res0.mu, [r_["mu"] for r_ in o.log], rtol=1e-12)
+    x = np.concatenate([o_[1] for o_ in out]).reshape(8, -1)
+    assert np.all(x * (1 - grid.mask()) == 0)                      # tails untouched
+    e_obj = float(np.max(np.abs(res0.obj - obj) / obj))
+    e_rmse = float(np.max(np.abs(res0.rmse - rmse) / rmse))
+    e_x = float(np.max(np.abs(x - o.x)) / np.max(np.abs(o.x)))
+    print(f"unequal slabs G={G}: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}")
+    assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (e_obj, e_rmse, e_x)
+
+
+def test_balanced_z_splits(bs):
+    """bsgd_balanced_z_splits: from a one-plane-slab context's exact visit table, 8 slabs
+    whose visit counts (measured again by the COUNT traversal of the balanced context) are
+    within the one-plane granularity of equal, and much closer than equal-thickness slabs."""
+    p, g, vol32, y = problem("cfg5", K=64, n_views=36)
+    fine = bs.Context.from_geometry(g, (1, 1, 64), 1)
+    zs = fine.balanced_z_splits(8)
+    vt = fine.visit_table().sum(axis=(1, 2)).astype(np.float64)     # visits per plane
+    fine.close()
+    assert zs[0] == 0 and zs[-1] == 64 and all(b > a for a, b in zip(zs, zs[1:]))
+
+    def spread(splits):
+        ctx = bs.Context.from_geometry(g, (1, 1, 8), 1, z_splits=splits)
+        v = ctx.visit_table().sum(axis=(1, 2)).astype(np.float64)
+        ctx.close()
+        return (v.max() - v.min()) / v.mean(), v
+
+    s_bal, v_bal = spread(zs)
+    s_eq, _ = spread(list(range(0, 65, 8)))
+    gran = vt.max() / (vt.sum() / 8)                                  # one plane, relative to a slab
+    print(f"balanced splits {zs}: visit spread {s_bal:.4f} (equal slabs {s_eq:.4f}; one-plane granularity {gran:.4f})")
+    assert s_bal <= gran + 1e-12 and s_bal < 0.5 * s_eq
+    # the balanced context's visits are the same planes' visits regrouped (the exact COUNT
+    # traversal is additive over slabs up to boundary slivers)
+    for k in range(8):
+        assert abs(v_bal[k] - vt[zs[k]:zs[k + 1]].sum()) <= 2e-4 * v_bal[k]
