@@ -1768,6 +1768,15 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
         }
         const int b = col_block - c->first;
         cudaStream_t st = S(stream);
+        if (c->zsplit && c->nz_of(col_block) < c->bd[2]) {
+            // the scratch copies are shared by all blocks: the planes past a thinner slab
+            // (its zero border first) must not hold a thicker slab's values
+            const int nzj = c->nz_of(col_block);
+            BSGD_CUDA(cudaMemsetAsync(c->fp_scratchN - PAD_X + (long long)nzj * c->planeN, 0,
+                                      sizeof(float) * (size_t)(c->bd[2] - nzj) * c->planeN, st));
+            BSGD_CUDA(cudaMemsetAsync(c->fp_scratchT - PAD_X + (long long)nzj * c->planeT, 0,
+                                      sizeof(float) * (size_t)(c->bd[2] - nzj) * c->planeT, st));
+        }
         c->update(UPD_XT, b, const_cast<float*>(x_block), 0.f, 1, nullptr, 0, st, nullptr, nullptr,
                   c->fp_scratchT, 0, c->fp_scratchN);
         std::vector<int> vv(views, views + n);

