@@ -1058,164 +1058,6 @@ __global__ void __launch_bounds__((TY + 2) * 32, MINB) k_tv_fgp_z(const TvzLaunc
     }
 }
 
-// ---- z-marching FGP through a 3-stage cp.async ring (the default) -------------------------
-// The same iteration as k_tv_fgp_z, with every operand of plane z staged in shared memory by
-// asynchronous copies issued two planes ahead: a stage holds P1 (x, y, z), P2 (x, y, z) and b on
-// rows y0-1 .. y0+TY (TY + 2 rows) and columns x0-4 .. x0+131 (the halo column x0 - 1, the
-// q_x(x0 + 128) neighbour), zero-filled outside the volume; plane z's step reads stage z and
-// the z components of stage z + 1, so a CTA keeps two planes in flight while it computes.
-constexpr int TVP_C = TV4_TX + 8;          // staged columns x0-4 .. x0+131
-constexpr int TVP_F = 7;                   // P1x P1y P1z P2x P2y P2z b
-
-__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool ok) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(ok ? 16 : 0) : "memory");
-}
-
-template <int TY>
-__device__ __forceinline__ void tvp_issue(const TvzLaunch& T, float* stage, int zz, int zlo, int zhi, int x0, int y0) {
-    if (zz >= zlo && zz <= zhi) {
-        const ZPlane P = zplane(T, zz);
-        constexpr int R = TY + 2, C4 = TVP_C / 4, N = TVP_F * R * C4;
-        for (int k = threadIdx.x; k < N; k += blockDim.x) {
-            const int f = k / (R * C4), rem = k % (R * C4), r = rem / C4, c4 = rem % C4;
-            const int y = y0 - 1 + r, x = x0 - 4 + 4 * c4;
-            const float* base = f < 3 ? P.p1[f] : (f < 6 ? P.p2[f - 3] : P.b);
-            const bool ok = base && y >= 0 && y < T.ny && x >= 0 && x < T.nx;
-            cp_async16(stage + (f * R + r) * TVP_C + 4 * c4, ok ? base + (long long)y * T.nx + x : T.b, ok);
-        }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-// q_k = p1 + beta (p1 - p2) of component c at stage (row r, column cl), float4 / scalar
-__device__ __forceinline__ float4 tvp_q4(const TvzLaunch& T, const float* st, int c, int r, int cl, int R) {
-    if (T.stage == 1) return make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 a = *reinterpret_cast<const float4*>(st + (c * R + r) * TVP_C + cl);
-    if (T.stage == 2) return a;
-    const float4 b = *reinterpret_cast<const float4*>(st + ((3 + c) * R + r) * TVP_C + cl);
-    return make_float4(a.x + T.beta * (a.x - b.x), a.y + T.beta * (a.y - b.y), a.z + T.beta * (a.z - b.z),
-                       a.w + T.beta * (a.w - b.w));
-}
-__device__ __forceinline__ float tvp_q1(const TvzLaunch& T, const float* st, int c, int r, int cl, int R) {
-    if (T.stage == 1) return 0.f;
-    const float a = st[(c * R + r) * TVP_C + cl];
-    if (T.stage == 2) return a;
-    return a + T.beta * (a - st[((3 + c) * R + r) * TVP_C + cl]);
-}
-
-// u at (x..x+3, row r) of plane z from stage s (own) and stage s1 (plane z + 1: q_z), plus q own
-template <int TY>
-__device__ __forceinline__ void tvp_u4(const TvzLaunch& T, const float* s, const float* s1, int x, int y, int z, int r,
-                                       int cl, float u[4], float4 q[3]) {
-    constexpr int R = TY + 2;
-    q[0] = tvp_q4(T, s, 0, r, cl, R);
-    q[1] = tvp_q4(T, s, 1, r, cl, R);
-    q[2] = tvp_q4(T, s, 2, r, cl, R);
-    const float4 qyn = tvp_q4(T, s, 1, r + 1, cl, R);                       // row y + 1 (0 past ny)
-    const float4 qz1 = z + 1 < T.nz ? tvp_q4(T, s1, 2, r, cl, R) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float qx4 = tvp_q1(T, s, 0, r, cl + 4, R);                        // x + 4 (0 past nx)
-    const float4 b = *reinterpret_cast<const float4*>(s + (6 * R + r) * TVP_C + cl);
-    const float qxa[5] = {q[0].x, q[0].y, q[0].z, q[0].w, x + 4 < T.nx ? qx4 : 0.f};
-    const float qya[4] = {q[1].x, q[1].y, q[1].z, q[1].w}, qyb[4] = {qyn.x, qyn.y, qyn.z, qyn.w};
-    const float qza[4] = {q[2].x, q[2].y, q[2].z, q[2].w}, qzb[4] = {qz1.x, qz1.y, qz1.z, qz1.w};
-    const float ba[4] = {b.x, b.y, b.z, b.w};
-    const float cy = y >= 1 ? 1.f : 0.f, cz = z >= 1 ? 1.f : 0.f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        float t = (x + k >= 1 ? qxa[k] : 0.f) - qxa[k + 1];
-        t += cy * qya[k] - qyb[k] + cz * qza[k] - qzb[k];
-        u[k] = fmaf(-T.w, t, ba[k]);
-    }
-}
-
-template <int TY>
-__global__ void __launch_bounds__((TY + 2) * 32, 3) k_tv_fgp_zp(const TvzLaunch T) {
-    extern __shared__ __align__(16) float tvp_smem[];
-    constexpr int R = TY + 2, SS = TVP_F * R * TVP_C;
-    float* const su = tvp_smem + 3 * SS;           // u rows y0-1 .. y0+TY-1: slot 4 + (x - x0), 3 = x0 - 1
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x0 = blockIdx.x * TV4_TX, y0 = blockIdx.y * TY;
-    const int zs = T.z0 + blockIdx.z * T.zc, ze = min(zs + T.zc, T.z1);
-    const bool helper = warp > TY;
-    const int row = helper ? 0 : warp;
-    const int y = helper ? y0 + lane : y0 + row - 1, x = x0 + 4 * lane;
-    const bool act = !helper && y >= 0 && y < T.ny && x < T.nx;
-    const bool out = act && row >= 1;
-    const long long plane = (long long)T.nx * T.ny;
-    const int F = zs >= 1 ? zs - 1 : zs;           // first staged plane
-    const int zhi = min(ze, T.nz - 1);             // last staged plane (z comps of plane ze)
-    auto stage = [&](int zz) { return tvp_smem + ((zz - F) % 3) * SS; };
-    tvp_issue<TY>(T, stage(F), F, F, zhi, x0, y0);
-    tvp_issue<TY>(T, stage(F + 1), F + 1, F, zhi, x0, y0);
-    tvp_issue<TY>(T, stage(F + 2), F + 2, F, zhi, x0, y0);
-    float uprev[4] = {0.f, 0.f, 0.f, 0.f};
-    if (zs >= 1) {                                 // u(zs - 1) of the output rows
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-        if (out) {
-            float4 qd[3];
-            tvp_u4<TY>(T, stage(zs - 1), stage(zs), x, y, zs - 1, row, 4 + 4 * lane, uprev, qd);
-        }
-        __syncthreads();
-        tvp_issue<TY>(T, stage(F + 3), F + 3, F, zhi, x0, y0);
-    }
-    for (int z = zs; z < ze; ++z) {
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-        const float* s0 = stage(z);
-        const float* s1 = stage(z + 1);
-        float u[4] = {0.f, 0.f, 0.f, 0.f};
-        float4 q[3];
-        if (helper) {
-            if (lane < TY && x0 >= 1 && y < T.ny) {   // u(x0 - 1, y): staged column 3, row lane + 1
-                const int r = lane + 1, xm = x0 - 1;
-                float t = 0.f;
-                if (xm >= 1) t += tvp_q1(T, s0, 0, r, 3, R);
-                t -= tvp_q1(T, s0, 0, r, 4, R);                                 // x0 < nx
-                if (y >= 1) t += tvp_q1(T, s0, 1, r, 3, R);
-                t -= tvp_q1(T, s0, 1, r + 1, 3, R);
-                if (z >= 1) t += tvp_q1(T, s0, 2, r, 3, R);
-                if (z + 1 < T.nz) t -= tvp_q1(T, s1, 2, r, 3, R);
-                su[r * TVP_C + 3] = fmaf(-T.w, t, s0[(6 * R + r) * TVP_C + 3]);
-            }
-        } else if (act) {
-            tvp_u4<TY>(T, s0, s1, x, y, z, row, 4 + 4 * lane, u, q);
-            *reinterpret_cast<float4*>(&su[row * TVP_C + 4 + 4 * lane]) = make_float4(u[0], u[1], u[2], u[3]);
-        }
-        __syncthreads();
-        if (out) {
-            const float uxm = su[row * TVP_C + 3 + 4 * lane];                 // u(x - 1)
-            const float4 up = *reinterpret_cast<const float4*>(&su[(row - 1) * TVP_C + 4 + 4 * lane]);
-            const float upa[4] = {up.x, up.y, up.z, up.w};
-            const float qa[3][4] = {{q[0].x, q[0].y, q[0].z, q[0].w}, {q[1].x, q[1].y, q[1].z, q[1].w},
-                                    {q[2].x, q[2].y, q[2].z, q[2].w}};
-            float po[3][4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float left = k == 0 ? uxm : u[k - 1];
-                const float gx = x + k >= 1 ? u[k] - left : 0.f;
-                const float gy = y >= 1 ? u[k] - upa[k] : 0.f;
-                const float gz = z >= 1 ? u[k] - uprev[k] : 0.f;
-                const float a0 = qa[0][k] + gx * T.s, a1 = qa[1][k] + gy * T.s, a2 = qa[2][k] + gz * T.s;
-                const float n2 = a0 * a0 + a1 * a1 + a2 * a2;
-                const float inv = n2 > 1.f ? rsqrtf(n2) : 1.f;
-                po[0][k] = a0 * inv;
-                po[1][k] = a1 * inv;
-                po[2][k] = a2 * inv;
-            }
-            const long long i = (long long)(z - T.z0) * plane + (long long)y * T.nx + x;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) st4(T.Pn + c * T.n + i, po[c][0], po[c][1], po[c][2], po[c][3]);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) uprev[k] = u[k];
-        __syncthreads();                           // stage z and the u rows are free again
-        tvp_issue<TY>(T, stage(z + 3), z + 3, F, zhi, x0, y0);
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
 // float4 form of k_tv_out (nx % 4 == 0): 4 x voxels per lane, in place (b = x is read only at
 // the lane's own voxels)
 __global__ void __launch_bounds__(256) k_tv_out4(const TvLaunch T, float* out) {
@@ -1492,23 +1334,8 @@ void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st) {
         const char* e = getenv("BSGD_TV_MINB");
         return e ? atoi(e) : 4;
     }();
-    static const int pipelined = [] {
-        const char* e = getenv("BSGD_TV_PIPE");
-        return e ? atoi(e) : 1;
-    }();
-    if (pipelined) {
-        constexpr size_t smem = sizeof(float) * (3 * TVP_F * (TY + 2) * TVP_C + (TY + 1) * TVP_C);
-        static bool attr = [] {
-            cudaFuncSetAttribute(k_tv_fgp_zp<TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            return true;
-        }();
-        (void)attr;
-        k_tv_fgp_zp<TY><<<g, (TY + 2) * 32, smem, st>>>(T);
-    } else if (minb >= 6) {
-        k_tv_fgp_z<TY, 6><<<g, (TY + 2) * 32, 0, st>>>(T);
-    } else {
-        k_tv_fgp_z<TY, 4><<<g, (TY + 2) * 32, 0, st>>>(T);
-    }
+    if (minb >= 6) k_tv_fgp_z<TY, 6><<<g, (TY + 2) * 32, 0, st>>>(T);
+    else k_tv_fgp_z<TY, 4><<<g, (TY + 2) * 32, 0, st>>>(T);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
