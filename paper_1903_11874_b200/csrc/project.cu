@@ -25,6 +25,9 @@
 #include "internal.h"
 
 namespace bsgd {
+#ifndef PROJ3_MINB
+#define PROJ3_MINB 4
+#endif
 
 namespace {
 
@@ -552,7 +555,7 @@ __device__ __forceinline__ bool walk3_setup(const ProjLaunch& L, const BlockDesc
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 4) k_project3(const ProjLaunch L) {
+__global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L) {
     const BlockDesc& B = L.blocks[blockIdx.z];
     Walk3 W;
     if (!walk3_setup<MODE>(L, B, W)) return;
