@@ -340,3 +340,51 @@ def test_balanced_z_splits(bs):
     # traversal is additive over slabs up to boundary slivers)
     for k in range(8):
         assert abs(v_bal[k] - vt[zs[k]:zs[k + 1]].sum()) <= 2e-4 * v_bal[k]
+
+
+@pytest.mark.parametrize("mode", ["im", "sgd", "stratified"])
+def test_band_exchange_schedules(bs, mode):
+    """The band exchange under the other epoch shapes: BSGD-IM (tile rows only; Algo 2),
+    Eq. 4 SGD (every block's FP fresh) and owner-stratified columns, G = 4 virtual ranks,
+    against the oracle."""
+    p, g, vol32, y = problem("cfg3", K=32, n_views=30)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = float(np.float32(0.5 / ob.power_iteration(P, 20, seed=1)))
+    E, G = 12, 4
+    xtb = P.grid.to_blocks(vol32)
+    kw = {"im": dict(im=True), "sgd": dict(sgd=True), "stratified": dict(strata=G)}[mode]
+    flags = {"im": bs.IS, "sgd": bs.SGD, "stratified": bs.STRATIFIED}[mode]
+    gN = 4 if mode != "sgd" else 8
+    prm = ob.Params(seed=3, mu=mu, rows_per_epoch=1, cols_per_epoch=gN, total_epochs=E, **kw)
+    o = ob.OracleBSGD(g, p.blocks, p.M, y.astype(np.float64), prm, row_kind="random", row_seed=11,
+                      tiles=p.tiles, x_true=xtb.astype(np.float64))
+    for _ in range(E):
+        o.epoch()
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, tiles=p.tiles, rank=r, world=G,
+                                     vgroup=group) for r in range(G)]
+    nb = p.N // G
+
+    def run(r, s):
+        yd = torch.from_numpy(y).cuda()
+        xd = torch.zeros(nb * P.grid.bsize, device="cuda")
+        xt = torch.from_numpy(xtb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+        res = ctxs[r].run(yd, xd, epochs=E, mu0=mu, seed=3, x_true=xt, rows_per_epoch=1, cols_per_epoch=gN,
+                          flags=flags, strata=G if mode == "stratified" else 0, stream=s)
+        s.synchronize()
+        return res, xd.cpu().numpy().astype(np.float64), ctxs[r].comm_stats()
+
+    out = _ranks(bs, G, run)
+    for c in ctxs:
+        c.close()
+    group.close()
+    assert all(o_[2]["mode"] == "band" for o_ in out)
+    res0 = out[0][0]
+    obj = np.array([r_["obj"] for r_ in o.log])
+    rmse = np.array([r_["rmse"] for r_ in o.log])
+    x = np.concatenate([o_[1] for o_ in out])
+    e_obj = float(np.max(np.abs(res0.obj - obj) / obj))
+    e_rmse = float(np.max(np.abs(res0.rmse - rmse) / rmse))
+    e_x = float(np.max(np.abs(x - o.x.ravel())) / np.max(np.abs(o.x)))
+    print(f"band exchange {mode}: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}")
+    assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (e_obj, e_rmse, e_x)
