@@ -39,6 +39,16 @@ def main():
         ctx.visit_table()
         ctx.solve("fista", y, x, 2, 1e-5, lam=0.1, tv_iters=2)
         ctx.close()
+    # unequal z-slabs (forward / back single operators share a padded scratch)
+    zs = [0, 3, 9, 20, 32]
+    ctx = bs.Context.from_geometry(g, (1, 1, 4), p.M, kind="random", row_seed=1, z_splits=zs)
+    x = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+    ctx.run(y, x, epochs=3, mu0=1e-5, seed=1, rows_per_epoch=1, cols_per_epoch=2, flags=bs.TV | bs.AUTO_MU,
+            lam=0.1, tv_iters=2, tv_period=2)
+    proj = torch.zeros(g.n_rays, device="cuda")
+    for j in range(4):
+        ctx.forward([0, 5], j, x[j * ctx.block_voxels:(j + 1) * ctx.block_voxels], proj)
+    ctx.close()
     torch.cuda.synchronize()
     # virtual ranks: band exchange + TV halos
     G = 2
