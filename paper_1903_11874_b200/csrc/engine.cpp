@@ -111,7 +111,8 @@ struct bsgd_ctx_s {
     // band covers it, one M-double allreduce.  BSGD_EXCHANGE=full keeps the full allreduce.
     bool band = false;
     std::vector<int2> bands;         // [world][n_views] (lo, hi)
-    std::vector<float*> rbuf;        // [world] peers' partial sums, compact like pc (overlap rows)
+    float *ex_send = nullptr, *ex_recv = nullptr;   // packed overlap chunks (sent / received)
+    long long ex_cap = 0;
     double* d_npart = nullptr;       // [M] this rank's partial ||r_I||^2
     unsigned long long comm_bytes = 0, comm_msgs = 0;   // residual exchange, sent by this rank
     float* gap_proj = nullptr;   // BSGD_LOG_TRUE_OBJ: A x (full length)
@@ -547,46 +548,85 @@ struct bsgd_ctx_s {
     int2 band_of(int h, int v) const { return bands[(size_t)h * n_views + v]; }
     static int2 isect(int2 a, int2 b) { return make_int2(std::max(a.x, b.x), std::min(a.y, b.y)); }
 
-    // Send this rank's pc on the overlap rows to every peer whose band overlaps, receive theirs
-    // into rbuf[h] (same compact offsets).  Symmetric: the overlap is the same set of rows
-    // seen from either side.
-    void band_exchange(const std::vector<int>& vsel, cudaStream_t st) {
-        const int V = (int)vsel.size();
-        struct Chunk { long long off, cnt; };
-        std::vector<std::vector<Chunk>> ch(world);
+    // The exchange plan of rank g for the selected views: per peer h (ascending) the chunks of
+    // its compact partial sums pc on the overlap rows band_g ∩ band_h (slot order), packed back to
+    // back; peer h's region starts at off[h].  Symmetric: g's chunk list for h equals h's for g.
+    struct Chunk { long long src, cnt, k, lo; };
+    struct ExPlan {
+        std::vector<std::vector<Chunk>> ch;
+        std::vector<long long> off;
+        long long total = 0;
+    };
+    ExPlan plan_for(int g, const std::vector<int>& vsel) const {
+        ExPlan P;
+        P.ch.resize(world);
+        P.off.assign(world + 1, 0);
         for (int h = 0; h < world; ++h) {
-            if (h == rank) continue;
-            for (int k = 0; k < V; ++k) {
-                const int2 o = isect(band_of(rank, vsel[k]), band_of(h, vsel[k]));
+            P.off[h] = P.total;
+            if (h == g) continue;
+            for (int k = 0; k < (int)vsel.size(); ++k) {
+                const int2 o = isect(band_of(g, vsel[k]), band_of(h, vsel[k]));
                 if (o.x >= o.y) continue;
-                ch[h].push_back({(long long)k * per + (long long)o.x * nu, (long long)(o.y - o.x) * nu});
+                P.ch[h].push_back({(long long)k * per + (long long)o.x * nu, (long long)(o.y - o.x) * nu, k, o.x});
+                P.total += (long long)(o.y - o.x) * nu;
             }
-            if (!ch[h].empty() && !rbuf[h]) rbuf[h] = dnew<float>(n_rays, false);
-            for (auto& c : ch[h]) {
+        }
+        P.off[world] = P.total;
+        return P;
+    }
+
+    // Send this rank's pc on the overlap rows to every peer whose band overlaps and receive theirs:
+    // the chunks are packed (k_copy_chunks) into one buffer, one ncclSend / ncclRecv per peer, into
+    // ex_recv (peer h's chunks at off[h]); the virtual-rank group copies each peer's region from its
+    // offered pack buffer.  Returns the plan (the residual kernel reads ex_recv through it).
+    ExPlan band_exchange(const std::vector<int>& vsel, std::vector<char>& staging, size_t& off, cudaStream_t st) {
+        ExPlan P = plan_for(rank, vsel);
+        if (P.total > ex_cap) {
+            ex_send = dnew<float>(P.total, false);
+            ex_recv = dnew<float>(P.total, false);
+            ex_cap = P.total;
+        }
+        std::vector<long long> tab;      // (src, dst, cnt) triples
+        for (int h = 0; h < world; ++h) {
+            long long d = P.off[h];
+            for (auto& c : P.ch[h]) {
+                tab.push_back(c.src);
+                tab.push_back(d);
+                tab.push_back(c.cnt);
+                d += c.cnt;
                 comm_bytes += 4ull * (unsigned long long)c.cnt;
-                ++comm_msgs;
             }
+            if (!P.ch[h].empty()) ++comm_msgs;
+        }
+        if (!tab.empty()) {   // the chunk table goes after this epoch's residual tables in d_tab
+            const size_t start = off;
+            const long long* dt = tab_put(off, tab, staging);
+            if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow (exchange plan)");
+            BSGD_CUDA(cudaMemcpyAsync(d_tab + start, staging.data() + start, off - start, cudaMemcpyHostToDevice, st));
+            launch_copy_chunks(pc, ex_send, dt, (int)(tab.size() / 3), st);
         }
         if (vg) {
-            vg_offer(pc, st);
+            vg_offer(ex_send, st);
             for (int h = 0; h < world; ++h) {
-                if (ch[h].empty()) continue;
+                const long long n = P.off[h + 1] - P.off[h];
+                if (n == 0) continue;
+                const ExPlan Q = plan_for(h, vsel);                 // where h packed its chunks for me
                 BSGD_CUDA(cudaStreamWaitEvent(st, vg->ev1[h], 0));
-                const float* src = (const float*)vg->src[h];
-                for (auto& c : ch[h])
-                    BSGD_CUDA(cudaMemcpyAsync(rbuf[h] + c.off, src + c.off, sizeof(float) * c.cnt,
-                                              cudaMemcpyDeviceToDevice, st));
+                BSGD_CUDA(cudaMemcpyAsync(ex_recv + P.off[h], (const float*)vg->src[h] + Q.off[rank],
+                                          sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
             }
             vg_release(st);
-            return;
+            return P;
         }
         BSGD_NCCL(ncclGroupStart());
-        for (int h = 0; h < world; ++h)
-            for (auto& c : ch[h]) {
-                BSGD_NCCL(ncclSend(pc + c.off, (size_t)c.cnt, ncclFloat, h, comm, st));
-                BSGD_NCCL(ncclRecv(rbuf[h] + c.off, (size_t)c.cnt, ncclFloat, h, comm, st));
-            }
+        for (int h = 0; h < world; ++h) {
+            const long long n = P.off[h + 1] - P.off[h];
+            if (n == 0) continue;
+            BSGD_NCCL(ncclSend(ex_send + P.off[h], (size_t)n, ncclFloat, h, comm, st));
+            BSGD_NCCL(ncclRecv(ex_recv + P.off[h], (size_t)n, ncclFloat, h, comm, st));
+        }
         BSGD_NCCL(ncclGroupEnd());
+        return P;
     }
 
     // line 7 with the band exchange (Rl: the k_residual launch of this epoch, pc filled):
@@ -594,14 +634,24 @@ struct bsgd_ctx_s {
     void band_residual(ResLaunch& Rl, const std::vector<int>& vsel, const std::vector<int>& sel_rows,
                        const int* drows, std::vector<char>& staging, size_t& off, cudaStream_t st) {
         const int V = (int)vsel.size();
-        band_exchange(vsel, st);
+        const ExPlan P = band_exchange(vsel, staging, off, st);
         std::vector<int2> bt((size_t)V * world), rg(V);
         for (int k = 0; k < V; ++k) {
             for (int h = 0; h < world; ++h) bt[(size_t)k * world + h] = band_of(h, vsel[k]);
             rg[k] = rank == 0 ? make_int2(0, nv) : band_of(rank, vsel[k]);
         }
+        // element (slot k, row v, column u) of peer h's partial sums sits at ex_recv[k per + v nu +
+        // u + adj[k][h]] (only rows of band_me ∩ band_h are read); own pc: adj = 0
+        std::vector<long long> adj((size_t)V * world, 0);
+        for (int h = 0; h < world; ++h) {
+            long long d = P.off[h];
+            for (auto& c : P.ch[h]) {
+                adj[(size_t)c.k * world + h] = d - c.src;
+                d += c.cnt;
+            }
+        }
         std::vector<const float*> dp(world, nullptr);
-        for (int h = 0; h < world; ++h) dp[h] = h == rank ? pc : rbuf[h];
+        for (int h = 0; h < world; ++h) dp[h] = h == rank ? pc : (P.off[h + 1] > P.off[h] ? ex_recv : nullptr);
         const size_t start = off;
         BandLaunch B;
         B.n_slots = V;
@@ -613,6 +663,7 @@ struct bsgd_ctx_s {
         B.bands = tab_put(off, bt, staging);
         B.range = tab_put(off, rg, staging);
         B.data = tab_put(off, dp, staging);
+        B.adj = tab_put(off, adj, staging);
         if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
         BSGD_CUDA(cudaMemcpyAsync(d_tab + start, staging.data() + start, off - start, cudaMemcpyHostToDevice, st));
         B.y = Rl.y;
@@ -1670,7 +1721,6 @@ bsgd_status bsgd_create_ex(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block
             c->band = !(e && std::string(e) == "full");
             if (c->band) {
                 c->compute_bands();
-                c->rbuf.assign(c->world, nullptr);
                 c->d_npart = c->dnew<double>(c->M);
             }
         }
@@ -1678,8 +1728,8 @@ bsgd_status bsgd_create_ex(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block
         c->d_rpart = c->dnew<double>((long long)c->n_views * RES_GX);
         c->d_red = c->dnew<double>(16);
         c->d_visits = c->dnew<unsigned long long>(1);
-        c->tab_bytes = 2 * (size_t)(64 + 16 * ((size_t)c->n_views * (2 + 4LL * c->s + 1 + c->world) + 64LL * c->s +
-                                              c->M + c->world) + 4096);
+        c->tab_bytes = 2 * (size_t)(64 + 16 * ((size_t)c->n_views * (2 + 4LL * c->s + 1 + 4LL * c->world) +
+                                              64LL * c->s + c->M + c->world) + 4096);
         c->d_tab = (char*)c->dalloc(c->tab_bytes);
         c->h_normsq.assign(c->M, 0.0);
         if (c->vg) {

@@ -153,13 +153,18 @@ struct BandLaunch {
     const int* views;           // [n_slots]
     const int2* bands;          // [n_slots][G] (lo, hi) detector rows of every rank's band
     const int2* range;          // [n_slots] rows this rank visits
-    const float* const* data;   // [G] compact [n_slots * per] partial sums (own pc / received)
+    const float* const* data;   // [G] partial sums: own pc (compact [n_slots * per]) / the
+                                // packed received chunks
+    const long long* adj;       // [n_slots][G] element offset of peer h's chunk of slot k
+                                // (element (k, v, u) at data[h][k per + v nu + u + adj])
     const float* y;
     float* r;
     double* part;               // [n_slots][RES_GX] per-CTA partial ||r||^2
 };
 void launch_residual_band(const BandLaunch& B, cudaStream_t st);
 void launch_copy_rows(double* dst, const double* src, const int* rows, int n, cudaStream_t st);
+// dst[t[3c+1] + i] = src[t[3c] + i], i < t[3c+2], for the n chunks c of the device table t
+void launch_copy_chunks(const float* src, float* dst, const long long* t, int n, cudaStream_t st);
 // R.normsq[i] = fixed-order sum of R.part over the slots of row block i (gx CTAs per slot)
 void launch_normsq_final(const ResLaunch& R, int gx, cudaStream_t st);
 // deterministic BP: S (power of two) from max|r| over n rays, V views and rpc (an upper bound on

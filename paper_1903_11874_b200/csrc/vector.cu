@@ -290,11 +290,12 @@ __global__ void __launch_bounds__(256) k_residual_band(const BandLaunch B) {
             mine |= h == B.me;
             const float* d = B.data[h];
             if (!d) continue;                    // a band not overlapping this rank's
+            const long long a = cbase + e + B.adj[(size_t)slot * B.G + h];
             if (v4) {
-                const float4 t = *reinterpret_cast<const float4*>(d + cbase + e);
+                const float4 t = *reinterpret_cast<const float4*>(d + a);
                 acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
             } else {
-                acc.x += d[cbase + e];
+                acc.x += d[a];
             }
         }
         if (mine) {
@@ -321,6 +322,12 @@ __global__ void __launch_bounds__(256) k_residual_band(const BandLaunch B) {
     }
     ss = block_sum(ss);
     if (threadIdx.x == 0) B.part[(size_t)slot * RES_GX + blockIdx.x] = ss;
+}
+
+__global__ void __launch_bounds__(256) k_copy_chunks(const float* src, float* dst, const long long* t) {
+    const long long s0 = t[3 * blockIdx.y], d0 = t[3 * blockIdx.y + 1], n = t[3 * blockIdx.y + 2];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[d0 + i] = src[s0 + i];
 }
 
 __global__ void k_copy_rows(double* dst, const double* src, const int* rows, int n) {
@@ -1226,6 +1233,13 @@ void launch_scale(float* v, long long n, const double* nrm, cudaStream_t st) {
 void launch_residual_band(const BandLaunch& B, cudaStream_t st) {
     if (B.n_slots == 0) return;
     k_residual_band<<<dim3(RES_GX, (unsigned)B.n_slots), 256, 0, st>>>(B);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_copy_chunks(const float* src, float* dst, const long long* t, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_copy_chunks<<<dim3(32, (unsigned)n), 256, 0, st>>>(src, dst, t);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
 }
