@@ -258,11 +258,6 @@ struct bsgd_ctx_s {
     float* pN(float* base, long long b) const { return base + b * padN + orgN; }
     float* pT(float* base, long long b) const { return base + b * padT + orgT; }
     void release() {
-        for (auto& sl : pin) {
-            if (sl.ev) cudaEventDestroy(sl.ev);
-            if (sl.p) cudaFreeHost(sl.p);
-        }
-        pin.clear();
         if (order_ev) cudaEventDestroy(order_ev);
         order_ev = nullptr;
         for (auto& e : up_ev) cudaEventDestroy(e);
@@ -389,39 +384,7 @@ struct bsgd_ctx_s {
     }
     void tab_upload(const std::vector<char>& staging, size_t used, cudaStream_t st) {
         if (used > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
-        h2d_tab(0, used, staging, st);
-    }
-    // Launch tables go up through a ring of pinned host slots, so the copy is truly
-    // asynchronous (a pageable cudaMemcpyAsync blocks the host until the DMA is done, which
-    // made the per-epoch host work of the small configurations wait on the GPU); a slot is
-    // reused only after the event recorded behind its previous copy has completed.
-    struct PinSlot { char* p = nullptr; cudaEvent_t ev = nullptr; bool used = false; };
-    std::vector<PinSlot> pin;
-    int pin_next = 0;
-    void h2d_tab(size_t start, size_t end, const std::vector<char>& staging, cudaStream_t st) {
-        if (end <= start) return;
-        const size_t n = end - start;
-        if (pin.empty()) {
-            pin.resize(8);
-            for (auto& sl : pin) {
-                if (cudaMallocHost((void**)&sl.p, tab_bytes) != cudaSuccess ||
-                    cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming) != cudaSuccess) {
-                    cudaGetLastError();
-                    sl.p = nullptr;
-                }
-            }
-        }
-        PinSlot& sl = pin[pin_next];
-        pin_next = (pin_next + 1) % (int)pin.size();
-        if (!sl.p) {   // no pinned memory: the (host-synchronous) pageable copy
-            BSGD_CUDA(cudaMemcpyAsync(d_tab + start, staging.data() + start, n, cudaMemcpyHostToDevice, st));
-            return;
-        }
-        if (sl.used) BSGD_CUDA(cudaEventSynchronize(sl.ev));
-        memcpy(sl.p + start, staging.data() + start, n);
-        BSGD_CUDA(cudaMemcpyAsync(d_tab + start, sl.p + start, n, cudaMemcpyHostToDevice, st));
-        BSGD_CUDA(cudaEventRecord(sl.ev, st));
-        sl.used = true;
+        BSGD_CUDA(cudaMemcpyAsync(d_tab, staging.data(), used, cudaMemcpyHostToDevice, st));
     }
 
     // ------------------------------------------------------------ operators
@@ -494,7 +457,8 @@ struct bsgd_ctx_s {
         L.visits = (mode == PROJ_COUNT) ? count_target : nullptr;
         L.det_scale = d_det_scale;
         if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
-        h2d_tab(tab_off, off, staging, st);
+        BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_off, staging.data() + tab_off, off - tab_off,
+                                  cudaMemcpyHostToDevice, st));
         launch_project(mode, L, st);
     }
 
@@ -638,7 +602,7 @@ struct bsgd_ctx_s {
             const size_t start = off;
             const long long* dt = tab_put(off, tab, staging);
             if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow (exchange plan)");
-            h2d_tab(start, off, staging, st);
+            BSGD_CUDA(cudaMemcpyAsync(d_tab + start, staging.data() + start, off - start, cudaMemcpyHostToDevice, st));
             launch_copy_chunks(pc, ex_send, dt, (int)(tab.size() / 3), st);
         }
         if (vg) {
@@ -701,7 +665,7 @@ struct bsgd_ctx_s {
         B.data = tab_put(off, dp, staging);
         B.adj = tab_put(off, adj, staging);
         if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
-        h2d_tab(start, off, staging, st);
+        BSGD_CUDA(cudaMemcpyAsync(d_tab + start, staging.data() + start, off - start, cudaMemcpyHostToDevice, st));
         B.y = Rl.y;
         B.r = Rl.r;
         B.part = d_rpart;
@@ -808,7 +772,8 @@ struct bsgd_ctx_s {
             Rl.views = tab_put(off, vsel, staging);
             Rl.slot_row = tab_put(off, slot_row, staging);
             int* drows = tab_put(off, sel_rows, staging);
-            h2d_tab(tab_bytes / 2, off, staging, st);
+            BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_bytes / 2, staging.data() + tab_bytes / 2,
+                                      off - tab_bytes / 2, cudaMemcpyHostToDevice, st));
             Rl.per = (int)per;
             Rl.z = z;
             Rl.zr = d_zr;
@@ -1081,7 +1046,8 @@ struct bsgd_ctx_s {
             Rl.slot_row = tab_put(off, slot_row, staging);
             int* drows = tab_put(off, rsel, staging);
             if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
-            h2d_tab(tab_bytes / 2, off, staging, st);
+            BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_bytes / 2, staging.data() + tab_bytes / 2,
+                                      off - tab_bytes / 2, cudaMemcpyHostToDevice, st));
             Rl.per = (int)per;
             Rl.z = z;
             Rl.zr = d_zr;
@@ -1875,7 +1841,8 @@ bsgd_status bsgd_forward(bsgd_ctx c, int32_t n, const int32_t* views, const int3
             staging.resize(off);
             const int* dv = c->tab_put(off, vv, staging);
             const int4* dr = c->tab_put(off, rc, staging);
-            c->h2d_tab(c->tab_bytes / 2, off, staging, st);
+            BSGD_CUDA(cudaMemcpyAsync(c->d_tab + c->tab_bytes / 2, staging.data() + c->tab_bytes / 2,
+                                      off - c->tab_bytes / 2, cudaMemcpyHostToDevice, st));
             launch_zero_rects(proj, dv, dr, n, c->nu, c->nv, st);
         }
         c->project(PROJ_FP, vv, {b}, rc, {c->fp_scratchN}, {c->fp_scratchT}, {}, {}, {proj}, nullptr, 0.f,
