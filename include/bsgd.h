@@ -328,6 +328,14 @@ bsgd_status bsgd_allreduce_time(bsgd_ctx ctx, int64_t count, int32_t iters, void
  * rows no band covers keep r = y).  Errors: BSGD_E_CONTRACT for NULL outputs.            */
 bsgd_status bsgd_comm_stats(bsgd_ctx ctx, uint64_t* bytes_sent, uint64_t* messages, int32_t* band_mode);
 
+/* Pure host function (no GPU): the detector band of rank `rank` of `world` -- per view v the
+ * rows [bands_out[2v], bands_out[2v+1]) that its owned blocks [rank N/world, (rank+1) N/world)
+ * project into (the union of the blocks' footprint rows, the same fp64 computation the band
+ * exchange uses; [0, 0) when no row does).  bands_out: host [n_views][2].  Errors:
+ * BSGD_E_CONTRACT, BSGD_E_GEOMETRY, BSGD_E_PARTITION as bsgd_create.                       */
+bsgd_status bsgd_rank_bands_host(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks, int32_t world,
+                                 int32_t rank, int32_t* bands_out);
+
 /* Host-only plan of the residual exchange for a hypothetical ownership of this ctx's block
  * grid by `world` ranks (rank g owns blocks [g N/world, (g+1) N/world)), for one epoch whose
  * selected row blocks hold the n_sel views `views` (host int32): *band_bytes = bytes all

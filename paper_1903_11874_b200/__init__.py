@@ -129,6 +129,7 @@ SIGS = {
     "bsgd_create": ([P(Geometry), Dims, BlockGrid, RowGrid, P(Dist), P(Alloc), P(_ctx)], C.c_int),
     "bsgd_create_ex": ([P(Geometry), Dims, BlockGrid, RowGrid, P(Dist), P(Alloc), P(CreateOpts), P(_ctx)], C.c_int),
     "bsgd_block_box": ([_ctx, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+    "bsgd_rank_bands_host": ([P(Geometry), Dims, BlockGrid, C.c_int32, C.c_int32, P(C.c_int32)], C.c_int),
     "bsgd_balanced_z_splits": ([_ctx, C.c_int32, P(C.c_int32), C.c_void_p], C.c_int),
     "bsgd_destroy": ([_ctx], None),
     "bsgd_vgroup_create": ([C.c_int32, P(C.c_void_p)], C.c_int),
@@ -208,6 +209,16 @@ def geometry_circular(beam, n_views, arc_deg, OP, OD, det_u, det_v, pitch_u, pit
     b = {"parallel": PARALLEL, "fan": FAN, "cone": CONE}.get(beam, beam)
     _check(_lib.bsgd_geometry_circular(int(b), n_views, arc_deg, OP, OD, det_u, det_v, pitch_u, pitch_v,
                                        out.ctypes.data_as(P(C.c_double))))
+    return out
+
+
+def rank_bands(geom, blocks, world, rank) -> np.ndarray:
+    """[n_views][2] detector row band of rank `rank` (bsgd_rank_bands_host; pure host)."""
+    vecs = np.ascontiguousarray(geom.vecs, dtype=np.float64)
+    g = Geometry(int(geom.beam), vecs.shape[0], int(geom.det_u), int(geom.det_v), vecs.ctypes.data_as(P(C.c_double)))
+    out = np.zeros((vecs.shape[0], 2), dtype=np.int32)
+    _check(_lib.bsgd_rank_bands_host(C.byref(g), Dims(*geom.dims), BlockGrid(*blocks), int(world), int(rank),
+                                     out.ctypes.data_as(P(C.c_int32))))
     return out
 
 

@@ -2405,6 +2405,40 @@ bsgd_status bsgd_exchange_plan(bsgd_ctx c, int32_t world, int32_t n_sel, const i
     });
 }
 
+bsgd_status bsgd_rank_bands_host(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block_grid blocks, int32_t world,
+                                 int32_t rank, int32_t* bands_out) {
+    return guard(nullptr, [&] {
+        if (!geom || !geom->vecs || !bands_out || world < 1 || rank < 0 || rank >= world)
+            fail(BSGD_E_CONTRACT, "bad arguments");
+        if (geom->n_views < 1 || geom->det_u < 1 || geom->det_v < 1 || geom->beam < 0 || geom->beam > 2)
+            fail(BSGD_E_GEOMETRY, "bad geometry");
+        if (blocks.bx < 1 || blocks.by < 1 || blocks.bz < 1 || dims.nx % blocks.bx || dims.ny % blocks.by ||
+            dims.nz % blocks.bz)
+            fail(BSGD_E_PARTITION, "volume dims must be divisible by the block grid");
+        const int N = blocks.bx * blocks.by * blocks.bz;
+        if (N % world) fail(BSGD_E_PARTITION, "N must be divisible by world");
+        // the host fields the footprint needs (no device state)
+        bsgd_ctx_s h;
+        h.beam = geom->beam;
+        h.n_views = geom->n_views;
+        h.nu = geom->det_u;
+        h.nv = geom->det_v;
+        h.vecs.assign(geom->vecs, geom->vecs + 12LL * geom->n_views);
+        h.dims[0] = dims.nx; h.dims[1] = dims.ny; h.dims[2] = dims.nz;
+        h.bgrid[0] = blocks.bx; h.bgrid[1] = blocks.by; h.bgrid[2] = blocks.bz;
+        for (int k = 0; k < 3; ++k) h.bd[k] = h.dims[k] / h.bgrid[k];
+        h.N = N;
+        h.world = world;
+        h.s = N / world;
+        const std::vector<int2> bd = h.rank_bands(world, h.s);
+        for (int v = 0; v < h.n_views; ++v) {
+            const int2 b = bd[(size_t)rank * h.n_views + v];
+            bands_out[2 * v] = b.x;
+            bands_out[2 * v + 1] = b.y;
+        }
+    });
+}
+
 bsgd_status bsgd_block_box(bsgd_ctx c, int32_t j, int32_t* lo, int32_t* hi) {
     return guard(c, [&] {
         if (!c || !lo || !hi || j < 0 || j >= c->N) fail(BSGD_E_CONTRACT, "bad arguments");
