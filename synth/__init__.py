@@ -218,6 +218,35 @@ def rasterise(ells: np.ndarray, dims) -> np.ndarray:
     return img
 
 
+def rasterise_torch(ells: np.ndarray, dims, device: str = "cuda"):
+    """rasterise() evaluated with torch on `device`: the same fp64 element-wise operations in
+    the same order (each torch op is one correctly rounded IEEE operation, as in numpy), so
+    the voxel values are identical; returns a float32 torch tensor (nz, ny, nx) on `device`.
+    (The 1024^3 phantom takes ~40 min single-threaded in numpy.)"""
+    import torch
+    nx, ny, nz = dims
+    f64 = dict(dtype=torch.float64, device=device)
+    xs = torch.arange(nx, **f64) + 0.5 - nx / 2.0
+    ys = torch.arange(ny, **f64) + 0.5 - ny / 2.0
+    zs = torch.arange(nz, **f64) + 0.5 - nz / 2.0 if nz > 1 else torch.zeros(1, **f64)
+    out = torch.empty((len(zs), ny, nx), dtype=torch.float32, device=device)
+    step = max(1, (1 << 24) // max(1, nx * ny))
+    for z_lo in range(0, len(zs), step):
+        z_hi = min(len(zs), z_lo + step)
+        Z, Y, X = torch.meshgrid(zs[z_lo:z_hi], ys, xs, indexing="ij")
+        sub = torch.zeros(Z.shape, **f64)
+        for rho, a, b, c, x0, y0, z0, phi in ells:
+            cp, sp = math.cos(math.radians(phi)), math.sin(math.radians(phi))
+            dx, dy, dz = X - float(x0), Y - float(y0), Z - float(z0)
+            xr = cp * dx + sp * dy
+            yr = -sp * dx + cp * dy
+            inside = (xr / float(a)) * (xr / float(a)) + (yr / float(b)) * (yr / float(b)) \
+                + (dz / float(c)) * (dz / float(c)) <= 1.0
+            sub[inside] += float(rho)
+        out[z_lo:z_hi] = sub.to(torch.float32)
+    return out
+
+
 def ray_endpoints(geom: Geometry, views: np.ndarray):
     """World-coordinate ray parametrisation p(alpha) = A + alpha*B, alpha in [0,1].
 

@@ -27,7 +27,10 @@ def inputs(spec, device="cpu"):
     p = synth.PRESETS[spec["name"]]
     g = p.geometry()
     ells = synth.ellipsoids_world(p.phantom, g.dims)
-    vol32 = synth.rasterise(ells, g.dims).astype(np.float32)
+    if device == "cpu":
+        vol32 = synth.rasterise(ells, g.dims).astype(np.float32)
+    else:   # the same values (identical fp64 operations), minutes faster at 1024^3
+        vol32 = synth.rasterise_torch(ells, g.dims, device=device).cpu().numpy()
     y = synth.analytic_projection(g, ells, device=device).ravel()
     if p.noise is not None:
         kind, a, seed = p.noise
