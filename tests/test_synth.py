@@ -9,7 +9,7 @@ import synth
 
 
 def test_rasterise_torch_equals_numpy():
-    for dims, kind in [((48, 40, 36), "random"), ((600, 600, 60), "shepp3d"), ((64, 64, 1), "shepp2d")]:
+    for dims, kind in [((48, 40, 36), "random"), ((1100, 1100, 16), "shepp3d"), ((64, 64, 1), "shepp2d")]:
         e = synth.ellipsoids_world(kind, dims)
         a = synth.rasterise(e, dims).astype(np.float32)
         b = synth.rasterise_torch(e, dims, device="cpu").numpy()
@@ -17,8 +17,8 @@ def test_rasterise_torch_equals_numpy():
 
 
 def test_rasterise_chunking_is_exact():
-    dims = (600, 600, 70)            # 46 planes per chunk -> 2 chunks
-    e = synth.ellipsoids_world("random", dims)
+    dims = (1100, 1100, 16)          # 13 planes per chunk -> 2 chunks
+    e = synth.ellipsoids_world("shepp3d", dims)
     nx, ny, nz = dims
     xs = np.arange(nx) + 0.5 - nx / 2
     ys = np.arange(ny) + 0.5 - ny / 2
