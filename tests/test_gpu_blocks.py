@@ -388,3 +388,68 @@ def test_band_exchange_schedules(bs, mode):
     e_x = float(np.max(np.abs(x - o.x.ravel())) / np.max(np.abs(o.x)))
     print(f"band exchange {mode}: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}")
     assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (e_obj, e_rmse, e_x)
+
+
+def test_unequal_slabs_other_paths(bs):
+    """Unequal z-slabs through the remaining entry points: a host-buffer run equals the device
+    run (per-block uploads / downloads of the thinner slabs' rows); deterministic BP runs are
+    bit-identical; LOG_TRUE_OBJ's fresh A x and the seen-voxel RMSE match the oracle; and a
+    full-gradient solver (FISTA-TV) gives the same iterates as on equal slabs (the partition
+    does not change a full-gradient method)."""
+    p, g, vol32, y = _zs_problem(K=32, n_views=30)
+    zs = [0, 3, 7, 12, 16, 19, 24, 27, 32]
+    grid = BlockGrid(g.dims, (1, 1, 8), zs)
+    P = Projector(g, grid)
+    mu = float(np.float32(1.0 / ob.power_iteration(P, 20, seed=1)))
+    xtb = grid.to_blocks(vol32)
+    # host buffers vs device buffers
+    outs = []
+    for host in (False, True):
+        ctx = bs.Context.from_geometry(g, (1, 1, 8), p.M, kind="random", row_seed=2, z_splits=zs)
+        if host:
+            yh, xh = torch.from_numpy(y.copy()).pin_memory(), torch.zeros(8 * grid.bsize).pin_memory()
+            res = ctx.run(yh, xh, epochs=10, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=3, flags=bs.AUTO_MU)
+            xr = xh.numpy().copy()
+        else:
+            yd, xd = torch.from_numpy(y).cuda(), torch.zeros(8 * grid.bsize, device="cuda")
+            res = ctx.run(yd, xd, epochs=10, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=3, flags=bs.AUTO_MU)
+            xr = xd.cpu().numpy()
+        outs.append((res.obj.copy(), res.mu.copy(), xr))
+        ctx.close()
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.allclose(outs[0][0], outs[1][0], rtol=1e-5)
+    assert np.max(np.abs(outs[0][2] - outs[1][2])) <= 1e-4 * np.max(np.abs(outs[0][2]))
+    assert np.all(outs[1][2].reshape(8, -1) * (1 - grid.mask()) == 0)
+    # deterministic BP: two runs bit-identical
+    xs = []
+    for _ in range(2):
+        ctx = bs.Context.from_geometry(g, (1, 1, 8), p.M, kind="random", row_seed=2, z_splits=zs)
+        xd = torch.zeros(8 * grid.bsize, device="cuda")
+        ctx.run(torch.from_numpy(y).cuda(), xd, epochs=6, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=3,
+                flags=bs.DETERMINISTIC)
+        xs.append(xd.cpu().numpy())
+        ctx.close()
+    assert np.array_equal(xs[0], xs[1])
+    # LOG_TRUE_OBJ: 1/2 |y - A x_k|^2 after each epoch vs the oracle
+    prm = ob.Params(seed=4, mu=mu, rows_per_epoch=1, cols_per_epoch=3)
+    o = ob.OracleBSGD(g, (1, 1, 8), p.M, y.astype(np.float64), prm, row_kind="random", row_seed=2, z_splits=zs)
+    want = []
+    for _ in range(4):
+        o.epoch()
+        want.append(o.true_objective())
+    ctx = bs.Context.from_geometry(g, (1, 1, 8), p.M, kind="random", row_seed=2, z_splits=zs)
+    xd = torch.zeros(8 * grid.bsize, device="cuda")
+    res = ctx.run(torch.from_numpy(y).cuda(), xd, epochs=4, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=3,
+                  flags=bs.LOG_TRUE_OBJ, x_true=torch.from_numpy(xtb.ravel().copy()).cuda())
+    ctx.close()
+    assert np.max(np.abs(res.obj_true - want) / np.array(want)) < 1e-5, (res.obj_true, want)
+    # FISTA-TV: the same iterates over unequal slabs as over equal ones
+    xs = []
+    for split in (zs, None):
+        ctx = bs.Context.from_geometry(g, (1, 1, 8), p.M, z_splits=split)
+        gb = BlockGrid(g.dims, (1, 1, 8), split)
+        xd = torch.zeros(8 * gb.bsize, device="cuda")
+        obj, _ = ctx.solve("fista", torch.from_numpy(y).cuda(), xd, 8, mu, lam=0.05, tv_iters=10)
+        xs.append((obj, gb.from_blocks(xd.cpu().numpy().reshape(8, -1))))
+        ctx.close()
+    assert np.allclose(xs[0][0], xs[1][0], rtol=1e-5)
+    assert np.max(np.abs(xs[0][1] - xs[1][1])) <= 1e-4 * np.max(np.abs(xs[1][1]))
