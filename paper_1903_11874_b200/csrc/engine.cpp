@@ -581,10 +581,12 @@ struct bsgd_ctx_s {
     // offered pack buffer.  Returns the plan (the residual kernel reads ex_recv through it).
     ExPlan band_exchange(const std::vector<int>& vsel, std::vector<char>& staging, size_t& off, cudaStream_t st) {
         ExPlan P = plan_for(rank, vsel);
-        if (P.total > ex_cap) {
-            ex_send = dnew<float>(P.total, false);
-            ex_recv = dnew<float>(P.total, false);
-            ex_cap = P.total;
+        if (P.total > ex_cap) {   // sized once for the largest plan (every view selected)
+            std::vector<int> all(n_views);
+            for (int v = 0; v < n_views; ++v) all[v] = v;
+            ex_cap = std::max(P.total, plan_for(rank, all).total);
+            ex_send = dnew<float>(ex_cap, false);
+            ex_recv = dnew<float>(ex_cap, false);
         }
         std::vector<long long> tab;      // (src, dst, cnt) triples
         for (int h = 0; h < world; ++h) {
