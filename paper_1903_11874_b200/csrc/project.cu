@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
     const int sxo = W.sxo, pstep = W.pstep, k0 = W.k0, nk = W.nk, rowstep = W.rowstep;
     const int view = W.view, iu = W.iu, iv = W.iv;
     const int slot = (int)((blockIdx.x / (unsigned)L.n_chunks) % (unsigned)L.n_slots);
-    const unsigned nsxo = (unsigned)(-sxo), npstep = (unsigned)(-pstep);
+
     const float wbp = W.wbp;
     double acc = 0.0;
     float acc32 = 0.f;
@@ -623,10 +623,11 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
                 l1 = m2 - m1;
                 l2 = 1.f - m2;
             }
-            // bx, bz are 0 or ~0u (= -1): the steps as multiply-adds (FMA pipe)
-            const unsigned dox = bx * nsxo, doz = bz * npstep;
+            // bx, bz are 0 or ~0u: the steps as masks (ALU pipe; the FMA pipe carries the IMADs
+            // of the address arithmetic: FP 97.0 -> 96.5 ms)
+            const unsigned dox = bx & (unsigned)sxo, doz = bz & (unsigned)pstep;
             const unsigned o1 = o + (ux <= uz ? dox : doz);
-            const unsigned o2 = bz * npstep + (bx * nsxo + o);
+            const unsigned o2 = o + dox + doz;
             const unsigned mor = bx | bz, mand = bx & bz;
             if (MODE == PROJ_FP) {
                 // software pipeline: this slice's gathers are issued before the previous
