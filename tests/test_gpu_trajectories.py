@@ -163,3 +163,65 @@ def test_is_off_last_global_epochs(bs):
     for splits in ([K], [12, 8], [16, 4]):
         cat, x = _gpu_split(bs, p, g, vol32, y, P, splits, mu, 11, bs.IS, total=K, is_off_last=L)
         print("is_off_last", splits, _cmp(o, cat, x))
+
+
+@pytest.mark.parametrize("G", [4])
+def test_full_size_cfg4_fixture_on_virtual_ranks(bs, G):
+    """The cfg4 fixture (512^3, BSGD-TV + Algo 3, 40 epochs) reproduced by G virtual ranks on
+    one GPU: the band exchange of the residual, the z-plane TV halos and the rank-summed Algo 3
+    dots at full size give the single-rank oracle trajectory."""
+    import threading
+    spec = ts.CFG4
+    with open(os.path.join(GOLDEN, "trajectory_cfg4.json")) as f:
+        fx = json.load(f)
+    g, y, vol32 = ts.inputs(spec, device="cuda")
+    _check_inputs(fx, y)
+    grid = BlockGrid(g.dims, spec["blocks"])
+    xtb = grid.to_blocks(vol32)
+    del vol32
+    group = bs.VirtualGroup(G)
+    ctxs = [bs.Context.from_geometry(g, spec["blocks"], spec["M"], kind="random", row_seed=spec["row_seed"],
+                                     rank=r, world=G, vgroup=group) for r in range(G)]
+    nb = grid.N // G
+    out, errs = [None] * G, []
+
+    def main(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                yd = torch.from_numpy(y).cuda()
+                xd = torch.zeros(nb * grid.bsize, device="cuda")
+                xt = torch.from_numpy(xtb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
+                res = ctxs[r].run(yd, xd, epochs=spec["epochs"], mu0=float(np.float32(spec["mu0"])), seed=spec["seed"],
+                                  x_true=xt, rows_per_epoch=spec["rows"], cols_per_epoch=spec["cols"],
+                                  flags=bs.TV | bs.AUTO_MU, lam=spec["lam"], tv_iters=20, stream=s)
+                s.synchronize()
+                out[r] = (res, xd.cpu().numpy().astype(np.float64), ctxs[r].comm_stats())
+        except Exception as e:          # noqa: BLE001 -- surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=main, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    for c in ctxs:
+        c.close()
+    group.close()
+    assert not errs, errs
+    res0 = out[0][0]
+    log = fx["log"]
+    assert [r["rows"] for r in log] == res0.sel_rows.tolist()
+    assert [r["cols"] for r in log] == res0.sel_cols.tolist()
+    assert np.allclose(res0.mu, [r["mu"] for r in log], rtol=1e-12)
+    obj = np.array([r["obj"] for r in log])
+    rmse = np.array([r["rmse"] for r in log])
+    e_obj = float(np.max(np.abs(res0.obj - obj) / obj))
+    e_rmse = float(np.max(np.abs(res0.rmse - rmse) / rmse))
+    x = np.concatenate([o[1] for o in out])
+    idx = np.asarray(fx["x_sample_idx"], dtype=np.int64)
+    e_x = float(np.max(np.abs(x[idx] - np.asarray(fx["x_sample"]))) / fx["x_absmax"])
+    sent = sum(o[2]["bytes_sent"] for o in out)
+    print(f"cfg4 fixture on {G} virtual ranks: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}; "
+          f"band exchange {sent / 1e9:.3f} GB over 40 epochs")
+    assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (e_obj, e_rmse, e_x)
