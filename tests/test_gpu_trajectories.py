@@ -165,14 +165,16 @@ def test_is_off_last_global_epochs(bs):
         print("is_off_last", splits, _cmp(o, cat, x))
 
 
-@pytest.mark.parametrize("G", [4])
-def test_full_size_cfg4_fixture_on_virtual_ranks(bs, G):
-    """The cfg4 fixture (512^3, BSGD-TV + Algo 3, 40 epochs) reproduced by G virtual ranks on
-    one GPU: the band exchange of the residual, the z-plane TV halos and the rank-summed Algo 3
-    dots at full size give the single-rank oracle trajectory."""
+@pytest.mark.parametrize("name,G", [("cfg4", 4), ("cfg5", 2)])
+def test_full_size_fixture_on_virtual_ranks(bs, name, G):
+    """The full-size fixtures reproduced by G virtual ranks on one GPU (cfg4: 512^3, BSGD-TV +
+    Algo 3, 40 epochs, G = 4; cfg5: 1024^3, 20 epochs, G = 2): the band exchange of the
+    residual, the z-plane TV halos and the rank-summed Algo 3 dots at full size give the
+    single-rank oracle trajectory."""
     import threading
-    spec = ts.CFG4
-    with open(os.path.join(GOLDEN, "trajectory_cfg4.json")) as f:
+    spec = ts.CFG4 if name == "cfg4" else ts.CFG5
+    flags = bs.TV | bs.AUTO_MU if name == "cfg4" else 0
+    with open(os.path.join(GOLDEN, f"trajectory_{name}.json")) as f:
         fx = json.load(f)
     g, y, vol32 = ts.inputs(spec, device="cuda")
     _check_inputs(fx, y)
@@ -194,7 +196,7 @@ def test_full_size_cfg4_fixture_on_virtual_ranks(bs, G):
                 xt = torch.from_numpy(xtb[r * nb:(r + 1) * nb].ravel().copy()).cuda()
                 res = ctxs[r].run(yd, xd, epochs=spec["epochs"], mu0=float(np.float32(spec["mu0"])), seed=spec["seed"],
                                   x_true=xt, rows_per_epoch=spec["rows"], cols_per_epoch=spec["cols"],
-                                  flags=bs.TV | bs.AUTO_MU, lam=spec["lam"], tv_iters=20, stream=s)
+                                  flags=flags, lam=spec.get("lam", 0.1), tv_iters=20, stream=s)
                 s.synchronize()
                 out[r] = (res, xd.cpu().numpy().astype(np.float64), ctxs[r].comm_stats())
         except Exception as e:          # noqa: BLE001 -- surfaced below
@@ -222,6 +224,6 @@ def test_full_size_cfg4_fixture_on_virtual_ranks(bs, G):
     idx = np.asarray(fx["x_sample_idx"], dtype=np.int64)
     e_x = float(np.max(np.abs(x[idx] - np.asarray(fx["x_sample"]))) / fx["x_absmax"])
     sent = sum(o[2]["bytes_sent"] for o in out)
-    print(f"cfg4 fixture on {G} virtual ranks: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}; "
-          f"band exchange {sent / 1e9:.3f} GB over 40 epochs")
+    print(f"{name} fixture on {G} virtual ranks: obj {e_obj:.3g} rmse {e_rmse:.3g} x {e_x:.3g}; "
+          f"band exchange {sent / 1e9:.3f} GB over {spec['epochs']} epochs")
     assert e_obj < 1e-3 and e_rmse < 1e-3 and e_x < 1e-2, (e_obj, e_rmse, e_x)
