@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define BSGD_ABI_VERSION 3
+#define BSGD_ABI_VERSION 4   /* 4: bsgd_create_ex (unequal z-slabs), band exchange queries */
 
 typedef struct bsgd_ctx_s* bsgd_ctx;
 

@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(bs):
     want = set(declared_symbols())
     assert want, "header parse failed"
     assert want <= exported, want - exported
-    assert bs.abi_version() == 3
+    assert bs.abi_version() == 4
 
 
 def test_geometry_bit_exact(bs):
