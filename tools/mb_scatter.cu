@@ -1,0 +1,151 @@
+// Micro-benchmark behind the BP accumulator choice ("shared-memory
+// accumulation"): the throughput of one scatter-add per lane per iteration with the BP
+// walk's address pattern (32 lanes -> 32 consecutive floats of one image row, the row
+// advancing every iteration; 35 % of the lanes add a second element in the neighbouring cell o ^ 1), into
+//   red_g   : global memory, red.global.add.f32 (the current k_project3<BP>, L2-resident target)
+//   atoms_i : shared memory, int32 fixed point, red.shared.add.u32 (native ATOMS.ADD) + F2I
+//   atoms_f : shared memory, fp32 atomicAdd (ptxas: LDS + FADD + ATOMS.CAST.SPIN loop)
+//   rmw     : shared memory, plain LDS + FADD + STS (no atomics: the bound an exclusive-owner
+//             scheme could reach)
+// and the gather side: ld.global.nc (L2-resident source) vs ld.shared, same pattern.
+// Each kernel runs ITER iterations per thread on a persistent grid (148 x 4 CTAs x 256).
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o mb_scatter tools/mb_scatter.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define ITER 4096
+#define SROWS 48            // shared tile rows of 128 floats (24 KB) per CTA
+constexpr int ROWF = 128;   // floats per tile row
+
+__device__ __forceinline__ unsigned pat(unsigned it, unsigned lane, unsigned wid) {
+    // row advances every iteration; warps of a CTA start on different rows
+    return ((it * 7u + wid * 5u) % SROWS) * ROWF + 32u * (wid & 3u) + lane;
+}
+__device__ __forceinline__ bool extra(unsigned it, unsigned lane) {
+    return ((it * 2654435761u + lane * 40503u) >> 16) % 100u < 35u;
+}
+
+__global__ void __launch_bounds__(256) red_g(float* dst, size_t span, float w) {
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float* base = dst + ((size_t)blockIdx.x * SROWS * ROWF) % span;
+    for (unsigned it = 0; it < ITER; ++it) {
+        const unsigned o = pat(it, lane, wid);
+        asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + o), "f"(w));
+        if (extra(it, lane)) asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + (o ^ 1u)), "f"(w));
+        w += 1e-7f;
+    }
+}
+
+__global__ void __launch_bounds__(256) atoms_i(float* dst, float w) {
+    __shared__ int s[SROWS * ROWF];
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) s[i] = 0;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(s);
+    for (unsigned it = 0; it < ITER; ++it) {
+        const unsigned o = pat(it, lane, wid);
+        const int q = __float2int_rn(w * 1048576.f);
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sb + 4 * o), "r"(q));
+        if (extra(it, lane)) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sb + 4 * (o ^ 1u)), "r"(q));
+        w += 1e-7f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) dst[(size_t)blockIdx.x * SROWS * ROWF + i] = (float)s[i];
+}
+
+__global__ void __launch_bounds__(256) atoms_f(float* dst, float w) {
+    __shared__ float s[SROWS * ROWF];
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) s[i] = 0.f;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (unsigned it = 0; it < ITER; ++it) {
+        const unsigned o = pat(it, lane, wid);
+        atomicAdd(&s[o], w);
+        if (extra(it, lane)) atomicAdd(&s[o ^ 1u], w);
+        w += 1e-7f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) dst[(size_t)blockIdx.x * SROWS * ROWF + i] = s[i];
+}
+
+// plain read-modify-write (racy by design: only the LDS + FADD + STS throughput is measured,
+// the rate an exclusive-owner accumulator could reach)
+__global__ void __launch_bounds__(256) rmw(float* dst, float w) {
+    __shared__ float s[SROWS * ROWF];
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) s[i] = 0.f;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    volatile float* vs = s;
+    for (unsigned it = 0; it < ITER; ++it) {
+        const unsigned o = pat(it, lane, wid);
+        vs[o] = vs[o] + w;
+        if (extra(it, lane)) vs[o ^ 1u] = vs[o ^ 1u] + w;
+        w += 1e-7f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) dst[(size_t)blockIdx.x * SROWS * ROWF + i] = s[i];
+}
+
+__global__ void __launch_bounds__(256) gather_g(const float* __restrict__ src, size_t span, float* out) {
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const float* base = src + ((size_t)blockIdx.x * SROWS * ROWF) % span;
+    float acc = 0.f;
+#pragma unroll 4
+    for (unsigned it = 0; it < ITER; ++it) {
+        const unsigned o = pat(it, lane, wid);
+        acc = fmaf(__ldg(base + o), 0.5f, acc);
+        acc = fmaf(__ldg(base + (o ^ (extra(it, lane) ? 1u : 0u))), 0.25f, acc);
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+
+__global__ void __launch_bounds__(256) gather_s(const float* __restrict__ src, float* out) {
+    __shared__ float s[SROWS * ROWF];
+    for (int i = threadIdx.x; i < SROWS * ROWF; i += blockDim.x) s[i] = src[i];
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float acc = 0.f;
+#pragma unroll 4
+    for (unsigned it = 0; it < ITER; ++it) {
+        const unsigned o = pat(it, lane, wid);
+        acc = fmaf(s[o], 0.5f, acc);
+        acc = fmaf(s[o ^ (extra(it, lane) ? 1u : 0u)], 0.25f, acc);
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = sms * 4;
+    const size_t span = (size_t)64 << 20;   // 256 MB of floats: the L2-resident window is per CTA
+    float* buf;
+    cudaMalloc(&buf, span * sizeof(float) + (size_t)grid * SROWS * ROWF * sizeof(float));
+    cudaMemset(buf, 0, span * sizeof(float));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double ops = (double)grid * 256 * ITER * 1.35;   // element updates (1 + 0.35 extra)
+    auto run = [&](const char* name, auto launch) {
+        for (int r = 0; r < 3; ++r) launch();
+        cudaEventRecord(e0);
+        for (int r = 0; r < 10; ++r) launch();
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 10;
+        printf("{\"kernel\": \"%s\", \"ms\": %.4f, \"elem_per_s\": %.4e, \"elem_per_sm_cycle_at_1.9GHz\": %.3f}\n", name,
+               ms, ops / (ms * 1e-3), ops / (ms * 1e-3) / (sms * 1.9e9));
+    };
+    float* out = buf + span;
+    run("red_global_f32", [&] { red_g<<<grid, 256>>>(buf, span - SROWS * ROWF, 1.f); });
+    run("atoms_int32_fixed", [&] { atoms_i<<<grid, 256>>>(out, 1.f); });
+    run("atoms_f32_cas", [&] { atoms_f<<<grid, 256>>>(out, 1.f); });
+    run("smem_rmw_no_atomic", [&] { rmw<<<grid, 256>>>(out, 1.f); });
+    run("gather_global_nc", [&] { gather_g<<<grid, 256>>>(buf, span - SROWS * ROWF, out); });
+    run("gather_shared", [&] { gather_s<<<grid, 256>>>(buf, out); });
+    cudaError_t err = cudaDeviceSynchronize();
+    printf("{\"status\": \"%s\", \"sms\": %d}\n", cudaGetErrorString(err), sms);
+    return err != cudaSuccess;
+}
