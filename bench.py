@@ -538,9 +538,12 @@ def run_ours(args, rank, world, local_rank):
 def time_tv(bs, ctx, x, w, p, aM, gN, world, stream, epoch_ms, peak, iters=20, calls=3):
     """The TV proximal call of Algo 4 line 16 on this rank's owned volume,
     timed on its own (CUDA events on the launch stream, max over ranks): 20 FGP iterations.
-    Algorithmic HBM bytes per call: per iteration read q (3), p (3), b and write q, p
-    (13 floats = 52 B per voxel; the first iteration reads neither q nor p: -24 B), plus the
-    final x = b - w grad^T p in place (read b, 3 p, write x: 20 B); no set-up pass."""
+    Algorithmic HBM bytes per call of the path that runs (TV):
+      one rank (k_tv_fgp_z2, two iterations per pass): read p_{k-1}, p_{k-2} (24 B) + b (4 B),
+        write p_k, p_{k+1} (24 B) = 52 B per voxel per pair; the first pair reads only b (28 B);
+      several ranks (k_tv_fgp_z, one iteration per launch): read p_{k-1}, p_{k-2}, b, write p_k
+        = 40 B per voxel; k = 1 reads only b (16 B), k = 2 reads p_1 and b (28 B);
+    plus the final x = b - w grad^T p in place (read b, 3 p, write x: 20 B)."""
     import torch
     import torch.distributed as dist
     xt = x.clone()
@@ -561,14 +564,21 @@ def time_tv(bs, ctx, x, w, p, aM, gN, world, stream, epoch_ms, peak, iters=20, c
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     n = x.numel()
-    nbytes = n * (52.0 * iters - 24.0 + 20.0)
+    pairs = world == 1 and p.blocks[:2] == (1, 1) and p.dims[0] % 4 == 0 and os.environ.get("BSGD_TV_Z2", "1") != "0"
+    if pairs:
+        per_voxel = 28.0 + 52.0 * (iters // 2 - 1) + (40.0 if iters % 2 else 0.0) + 20.0
+        kernel = "k_tv_fgp_z2 (two FGP iterations per pass) x iters/2 + k_tv_out"
+        what = "52 B per voxel per two FGP iterations (28 B in the first pair) + 20 B final"
+    else:
+        per_voxel = 16.0 + 28.0 + 40.0 * (iters - 2) + 20.0
+        kernel = ("k_tv_fgp_z (one FGP iteration per launch) x iters + k_tv_out" if p.blocks[:2] == (1, 1)
+                  else "k_tv_u + k_tv_pq per iteration + k_tv_u")
+        what = "40 B per voxel per FGP iteration (16 B at k = 1, 28 B at k = 2) + 20 B final"
+    nbytes = n * per_voxel
     period = max(1, round(p.M * p.N / (aM * gN)))
     del xt
     return {"ms_per_call": ms, "iters": iters, "w": w, "voxels_per_rank": n, "launches_per_call": int(launches),
-            "kernel": "k_tv_fgp4 (fused FGP iteration, float4) x iters + k_tv_out" if p.blocks[:2] == (1, 1)
-            else "k_tv_u + k_tv_pq per iteration + k_tv_u",
-            "algorithmic_bytes": f"{nbytes:.4g} B per call (52 B per voxel per FGP iteration, 28 B in the first, "
-                                 f"+ 20 B final)",
+            "kernel": kernel, "algorithmic_bytes": f"{nbytes:.4g} B per call ({what})",
             "achieved_gbs": nbytes / (ms / 1e3) / 1e9, "frac": nbytes / (ms / 1e3) / 1e9 / peak,
             "period_epochs": period,
             "epochs_per_s_tv_amortised": 1e3 / (epoch_ms + ms / period)}

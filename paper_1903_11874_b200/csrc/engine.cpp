@@ -147,7 +147,7 @@ struct bsgd_ctx_s {
     float *eud_cur = nullptr, *eud_prev = nullptr;
     float *tv_u = nullptr, *tv_p = nullptr, *tv_q = nullptr, *tv_hq = nullptr, *tv_hu = nullptr,
           *tv_q2 = nullptr, *tv_hp = nullptr, *tv_pk = nullptr, *tvz_hp = nullptr, *tvz_hn = nullptr,
-          *tv_xc = nullptr;
+          *tv_xc = nullptr, *tv_q3 = nullptr;
     float *fp_scratchT = nullptr, *fp_scratchN = nullptr, *pw_v = nullptr, *pw_proj = nullptr, *pw_vT = nullptr,
           *pw_vN = nullptr;
     float* xN = nullptr;   // slack-padded copy of x_owned (FP source for main-Y views)
@@ -1276,6 +1276,19 @@ struct bsgd_ctx_s {
                 tvz_hn = dnew<float>(2 * plane);
             }
             float* buf[3] = {tv_q, tv_q2, tv_p};
+            // one rank owning the whole volume: two iterations per pass (k_tv_fgp_z2, temporal
+            // blocking), p_k in buf4[k % 4]; an odd last iteration takes k_tv_fgp_z
+            const bool z2 = world == 1 && iters >= 2 && Tl.z0 == 0 && Tl.z1 == dims[2] &&
+                            !(getenv("BSGD_TV_Z2") && atoi(getenv("BSGD_TV_Z2")) == 0);
+            float* buf4[4] = {tv_q, tv_q2, tv_p, nullptr};
+            if (z2) {
+                if (!tv_q3) tv_q3 = dnew<float>(3 * n, false);
+                buf4[3] = tv_q3;
+            }
+            auto b4 = [&](int j) { return buf4[((j % 4) + 4) % 4]; };
+            std::vector<double> sk_(iters + 3, 1.0);   // s_1 = 1, s_{j+1} = (1 + sqrt(1 + 4 s_j^2)) / 2
+            for (int j = 1; j + 1 < (int)sk_.size(); ++j) sk_[j + 1] = (1.0 + sqrt(1.0 + 4.0 * sk_[j] * sk_[j])) / 2.0;
+            auto beta_of = [&](int j) { return j >= 1 ? (sk_[j] - 1.0) / sk_[j + 1] : 0.0; };   // beta_j
             TvzLaunch Z{};
             Z.nx = dims[0];
             Z.ny = dims[1];
@@ -1293,6 +1306,45 @@ struct bsgd_ctx_s {
             Z.pf = 2;
             if (const char* e = getenv("BSGD_TV_PF")) Z.pf = std::max(0, atoi(e));
             if (world > 1) halo_exchange(x_owned + n - plane, tvz_hp + 6 * plane, plane, false, st);   // b of z0-1
+            if (z2) {
+                Tvz2Launch Y{};
+                Y.nx = dims[0];
+                Y.ny = dims[1];
+                Y.nz = dims[2];
+                Y.n = n;
+                Y.b = x_owned;
+                Y.w = (float)wgt;
+                Y.s = (float)(1.0 / (Tl.L * wgt));
+                Y.zc = std::max(1, std::min(32, dims[2] / 8));
+                if (const char* e = getenv("BSGD_TV_Z2C")) Y.zc = std::max(1, atoi(e));   // A/B hooks
+                Y.pf = 1;
+                if (const char* e = getenv("BSGD_TV_PF")) Y.pf = std::max(0, atoi(e));
+                int k = 1;
+                for (; k + 1 <= iters; k += 2) {
+                    Y.P1 = b4(k - 1);
+                    Y.P2 = b4(k - 2);
+                    Y.Pa = b4(k);
+                    Y.Pb = b4(k + 1);
+                    Y.stage = k == 1 ? 1 : (k == 2 ? 2 : 0);
+                    Y.beta0 = (float)beta_of(k - 1);
+                    Y.beta1 = (float)beta_of(k);
+                    launch_tv_fgp_z2(Y, st);
+                }
+                if (k == iters) {                            // odd count: the last iteration alone
+                    Z.P1 = b4(k - 1);
+                    Z.P2 = b4(k - 2);
+                    Z.Pn = b4(k);
+                    Z.stage = k == 1 ? 1 : (k == 2 ? 2 : 0);
+                    Z.beta = (float)beta_of(k - 1);
+                    launch_tv_fgp_z(Z, st);
+                }
+                float* pf = b4(iters);                       // p_K
+                Tl.first = 0;
+                Tl.q = pf;
+                Tl.wf = (float)wgt;
+                launch_tv_out(Tl, x_owned, st);
+                return;
+            }
             double s_prev = 1.0;                             // s_{k-1}
             for (int k = 1; k <= iters; ++k) {
                 double beta = 0.0;                           // beta_{k-1} = (s_{k-1} - 1) / s_k

@@ -257,5 +257,26 @@ struct TvzLaunch {
     int pf;                    // L2 prefetch distance in planes (0 = none)
 };
 void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st);
+// Two FGP iterations k, k+1 per pass (temporal blocking; one rank owning the whole volume as
+// one [z][y][x] array): reads p_{k-1}, p_{k-2}, b, writes p_k and p_{k+1} -- 52 B per voxel
+// per two iterations instead of 2 x 40.  Each CTA marches up a column of zc planes of a
+// 56 x 12 x-y tile (nx % 4 == 0); the loaded region carries a 2-voxel halo (the two stencils' reach),
+// iteration k runs one plane ahead of iteration k+1; q_k, u_k, q_{k+1}, u_{k+1} live in
+// shared-memory rings, p_{k-1} and b (read only at the loading thread's own voxels) in registers.
+struct Tvz2Launch {
+    int nx, ny, nz;
+    long long n;               // voxels (component stride of the P buffers)
+    const float* b;            // prox input
+    const float* P1;           // p_{k-1}
+    const float* P2;           // p_{k-2}
+    float* Pa;                 // p_k (output)
+    float* Pb;                 // p_{k+1} (output)
+    float w, s;                // w = mu lambda, s = 1/(L w)
+    float beta0, beta1;        // beta_{k-1} (q_k) and beta_k (q_{k+1})
+    int stage;                 // of iteration k: 1 (q_k = 0, p_{k-1} = 0), 2 (q_k = p_{k-1}), 0
+    int zc;                    // planes per CTA
+    int pf;                    // L2 prefetch distance in planes (0 = none)
+};
+void launch_tv_fgp_z2(const Tvz2Launch& T, cudaStream_t st);
 
 }  // namespace bsgd

@@ -1065,6 +1065,202 @@ __global__ void __launch_bounds__((TY + 2) * 32, MINB) k_tv_fgp_z(const TvzLaunc
     }
 }
 
+// ---- two FGP iterations per pass (k_tv_fgp_z2, Tvz2Launch; nx % 4 == 0) ---------------
+// Region coordinates (rx, ry) in [0, 64) x [0, 16) <-> voxel (x0 - 4 + rx, y0 - 2 + ry) of a
+// 56 x 12 output tile (x0, y0): a thread owns the 4 x-consecutive voxels of one region row
+// (float4 in global and shared memory; x0 - 4 keeps the quads 16-byte aligned).  Iteration k
+// needs u_k on [-2, W] (the backward gradient of p_k's 1-voxel halo), hence q_k on
+// [-2, W + 1]; p_k / q_{k+1} live on [-1, W], u_{k+1} on [-1, W - 1], p_{k+1} on the tile
+// (the same in y, where the halo is exactly 2).  Values beyond these ranges are computed from
+// whatever the region holds and never read.
+// Step z of the march: L loads plane z + 1 (q_k = p_{k-1} + beta_{k-1} (p_{k-1} - p_{k-2}) to
+// shared memory; p_{k-1} and b, which only the loading thread reads, in registers), U1 evaluates u_k(z) = b - w grad^T q_k, P1 projects p_k(z) and forms
+// q_{k+1}(z) = p_k + beta_k (p_k - p_{k-1}), U2 evaluates u_{k+1}(z - 1), P2 projects
+// p_{k+1}(z - 1).  Four barriers per plane (two per iteration, as k_tv_fgp_z).
+constexpr int Z2_W = 56, Z2_RW = 64;
+constexpr int Z2_FIELDS = 16;   // sq 2x3, su 2, sq1 2x3, su1 2 (p_{k-1} and b stay in registers)
+template <int RH> constexpr int z2_threads() { return Z2_RW / 4 * RH; }
+template <int RH> constexpr size_t z2_smem() { return sizeof(float) * Z2_FIELDS * Z2_RW * RH; }
+
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void sts4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void f4a(float4 v, float a[4]) {
+    a[0] = v.x;
+    a[1] = v.y;
+    a[2] = v.z;
+    a[3] = v.w;
+}
+
+// u = b - w grad^T q on the quad at offset o of row gy, plane zq (q: 3 component fields of
+// plane zq, qzn: z component of plane zq + 1; zero differences at index 0 and beyond the
+// last index, Eq. 6 adjoint)
+__device__ __forceinline__ float4 z2_u(const float* qx, const float* qy, const float* qz, const float* qzn,
+                                       float4 bb, int o, int gx0, int gy, int zq, int nx, int ny, int nz, float w) {
+    float ax[5], ay[4], ayn[4], az[4], azn[4], b[4];
+    f4a(lds4(qx + o), ax);
+    ax[4] = qx[o + 4];
+    f4a(lds4(qy + o), ay);
+    f4a(lds4(qy + o + Z2_RW), ayn);
+    f4a(lds4(qz + o), az);
+    f4a(lds4(qzn + o), azn);
+    f4a(bb, b);
+    const float cy = gy >= 1 ? 1.f : 0.f, cyn = gy + 1 < ny ? 1.f : 0.f;
+    const float cz = zq >= 1 ? 1.f : 0.f, czn = zq + 1 < nz ? 1.f : 0.f;
+    float u[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        float t = (gx0 + e >= 1 ? ax[e] : 0.f) - (gx0 + e + 1 < nx ? ax[e + 1] : 0.f);
+        t += cy * ay[e] - cyn * ayn[e] + cz * az[e] - czn * azn[e];
+        u[e] = fmaf(-w, t, b[e]);
+    }
+    return make_float4(u[0], u[1], u[2], u[3]);
+}
+
+// p = P_{|p| <= 1}(q + s grad u) on the quad at offset o (uu: u of the plane, uprev: u of the
+// plane below; backward differences, zero at index 0)
+__device__ __forceinline__ void z2_p(const float* uu, const float* uprev, const float* qx, const float* qy,
+                                     const float* qz, int o, int gx0, int gy, int zq, float s, float p[3][4]) {
+    float u[4], uup[4], upr[4], q[3][4];
+    f4a(lds4(uu + o), u);
+    const float ul = uu[o - 1];
+    f4a(lds4(uu + o - Z2_RW), uup);
+    f4a(lds4(uprev + o), upr);
+    f4a(lds4(qx + o), q[0]);
+    f4a(lds4(qy + o), q[1]);
+    f4a(lds4(qz + o), q[2]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float left = e == 0 ? ul : u[e - 1];
+        const float gx = gx0 + e >= 1 ? u[e] - left : 0.f;
+        const float gy_ = gy >= 1 ? u[e] - uup[e] : 0.f;
+        const float gz = zq >= 1 ? u[e] - upr[e] : 0.f;
+        const float a0 = q[0][e] + gx * s, a1 = q[1][e] + gy_ * s, a2 = q[2][e] + gz * s;
+        const float n2 = a0 * a0 + a1 * a1 + a2 * a2;
+        const float iv = n2 > 1.f ? rsqrtf(n2) : 1.f;
+        p[0][e] = a0 * iv;
+        p[1][e] = a1 * iv;
+        p[2][e] = a2 * iv;
+    }
+}
+
+template <int Z2_RH>
+__global__ void __launch_bounds__(Z2_RW / 4 * Z2_RH, Z2_RH <= 16 ? 3 : 2) k_tv_fgp_z2(const Tvz2Launch T) {
+    constexpr int Z2_H = Z2_RH - 4, Z2_F = Z2_RW * Z2_RH;
+    extern __shared__ __align__(16) float sm[];
+    float* const sq = sm;                       // [2][3][F]  q_k of planes z, z + 1
+    float* const su = sq + 6 * Z2_F;            // [2][F]     u_k of planes z - 1, z
+    float* const sq1 = su + 2 * Z2_F;           // [2][3][F]  q_{k+1} of planes z - 1, z
+    float* const su1 = sq1 + 6 * Z2_F;          // [2][F]     u_{k+1} of planes z - 2, z - 1
+    const int nx = T.nx, ny = T.ny, nz = T.nz;
+    const long long plane = (long long)nx * ny;
+    const int tq = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int rx0 = 4 * tq, o = ty * Z2_RW + rx0;
+    const int gx0 = blockIdx.x * Z2_W - 4 + rx0, gy = blockIdx.y * Z2_H - 2 + ty;
+    const int zs = blockIdx.z * T.zc, ze = min(zs + T.zc, nz);
+    const bool qin = gy >= 0 && gy < ny && gx0 >= 0 && gx0 < nx;   // nx % 4 == 0: whole quads
+    const bool tile_x = tq >= 1 && tq < 15, tile = tile_x && ty >= 2 && ty < Z2_RH - 2 && qin;
+    const long long gi = (long long)gy * nx + gx0;
+    const float w = T.w, s = T.s, be0 = T.beta0, be1 = T.beta1;
+    const int stage = T.stage;
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    // a thread always owns the same quad, so what only its own quad reads stays in registers:
+    // p_{k-1} of plane z (P1's momentum) and b of planes z - 1, z (U2, U1), loaded one step ahead
+    float4 p1n[3] = {zero4, zero4, zero4}, bn = zero4, bz = zero4, bzm = zero4;
+
+    for (int z = max(zs - 3, -1); z <= ze; ++z) {
+        const float4 p1z[3] = {p1n[0], p1n[1], p1n[2]};   // p_{k-1}(z)
+        bzm = bz;                                         // b(z - 1)
+        bz = bn;                                          // b(z)
+        // ---- L: plane z + 1 -> sq (+ p_{k-1}, b in registers)
+        {
+            const int zl = z + 1, a = zl & 1;
+            const int zp = zl + T.pf;
+            if (T.pf > 0 && qin && zp >= 0 && zp < nz && (tq == 0 || (gx0 & 31) == 0)) {   // once per line
+                const long long ip = (long long)zp * plane + gi;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (stage != 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(T.P1 + c * T.n + ip));
+                    if (stage == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(T.P2 + c * T.n + ip));
+                }
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(T.b + ip));
+            }
+            float4 p1[3] = {zero4, zero4, zero4}, p2[3] = {zero4, zero4, zero4}, bb = zero4;
+            if (qin && zl >= 0 && zl < nz) {
+                const long long i = (long long)zl * plane + gi;
+                if (stage != 1) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p1[c] = __ldg(reinterpret_cast<const float4*>(T.P1 + c * T.n + i));
+                }
+                if (stage == 0) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) p2[c] = __ldg(reinterpret_cast<const float4*>(T.P2 + c * T.n + i));
+                }
+                bb = __ldg(reinterpret_cast<const float4*>(T.b + i));
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                // q_k as k_tv_fgp_z forms it (stage 1: 0; stage 2: p_1)
+                float4 q = p1[c];
+                if (stage == 0)
+                    q = make_float4(p1[c].x + be0 * (p1[c].x - p2[c].x), p1[c].y + be0 * (p1[c].y - p2[c].y),
+                                    p1[c].z + be0 * (p1[c].z - p2[c].z), p1[c].w + be0 * (p1[c].w - p2[c].w));
+                sts4(sq + (a * 3 + c) * Z2_F + o, q);
+                p1n[c] = p1[c];
+            }
+            bn = bb;
+        }
+        __syncthreads();
+        // ---- U1: u_k(z) on region rows [0, 15)
+        if (z >= 0 && z < nz && ty < Z2_RH - 1) {
+            const int a = z & 1, an = (z + 1) & 1;
+            sts4(su + a * Z2_F + o, z2_u(sq + (a * 3 + 0) * Z2_F, sq + (a * 3 + 1) * Z2_F, sq + (a * 3 + 2) * Z2_F,
+                                         sq + (an * 3 + 2) * Z2_F, bz, o, gx0, gy, z, nx, ny, nz, w));
+        }
+        __syncthreads();
+        // ---- P1: p_k(z) on rows [1, 15); q_{k+1}(z); p_k written on the output tile
+        if (z >= 0 && z < nz && ty >= 1 && ty < Z2_RH - 1) {
+            const int a = z & 1, ap = (z + 1) & 1;   // ap = (z - 1) & 1
+            float pk[3][4];
+            z2_p(su + a * Z2_F, su + ap * Z2_F, sq + (a * 3 + 0) * Z2_F, sq + (a * 3 + 1) * Z2_F,
+                 sq + (a * 3 + 2) * Z2_F, o, gx0, gy, z, s, pk);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float pm[4];
+                f4a(p1z[c], pm);
+                float4 qn = zero4;
+                if (qin)
+                    qn = make_float4(pk[c][0] + be1 * (pk[c][0] - pm[0]), pk[c][1] + be1 * (pk[c][1] - pm[1]),
+                                     pk[c][2] + be1 * (pk[c][2] - pm[2]), pk[c][3] + be1 * (pk[c][3] - pm[3]));
+                sts4(sq1 + (a * 3 + c) * Z2_F + o, qn);
+            }
+            if (tile && z >= zs && z < ze) {
+                const long long i = (long long)z * plane + gi;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) st4(T.Pa + c * T.n + i, pk[c][0], pk[c][1], pk[c][2], pk[c][3]);
+            }
+        }
+        __syncthreads();
+        // ---- U2: u_{k+1}(z - 1) on rows [1, 14)
+        const int zz = z - 1;
+        if (zz >= 0 && zz < nz && ty >= 1 && ty < Z2_RH - 2) {
+            const int a = zz & 1, an = z & 1;
+            sts4(su1 + a * Z2_F + o, z2_u(sq1 + (a * 3 + 0) * Z2_F, sq1 + (a * 3 + 1) * Z2_F, sq1 + (a * 3 + 2) * Z2_F,
+                                          sq1 + (an * 3 + 2) * Z2_F, bzm, o, gx0, gy, zz, nx, ny, nz, w));
+        }
+        __syncthreads();
+        // ---- P2: p_{k+1}(z - 1) on the output tile
+        if (tile && zz >= zs && zz < ze) {
+            const int a = zz & 1, ap = (zz + 1) & 1;   // ap = (zz - 1) & 1
+            float pk[3][4];
+            z2_p(su1 + a * Z2_F, su1 + ap * Z2_F, sq1 + (a * 3 + 0) * Z2_F, sq1 + (a * 3 + 1) * Z2_F,
+                 sq1 + (a * 3 + 2) * Z2_F, o, gx0, gy, zz, s, pk);
+            const long long i = (long long)zz * plane + gi;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) st4(T.Pb + c * T.n + i, pk[c][0], pk[c][1], pk[c][2], pk[c][3]);
+        }
+    }
+}
+
 // float4 form of k_tv_out (nx % 4 == 0): 4 x voxels per lane, in place (b = x is read only at
 // the lane's own voxels)
 __global__ void __launch_bounds__(256) k_tv_out4(const TvLaunch T, float* out) {
@@ -1352,6 +1548,30 @@ void launch_tv_fgp_z(const TvzLaunch& T, cudaStream_t st) {
     else k_tv_fgp_z<TY, 4><<<g, (TY + 2) * 32, 0, st>>>(T);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
+}
+
+template <int RH>
+static void launch_z2(const Tvz2Launch& T, cudaStream_t st) {
+    static const bool attr = [] {
+        BSGD_CUDA(cudaFuncSetAttribute(k_tv_fgp_z2<RH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)z2_smem<RH>()));
+        return true;
+    }();
+    (void)attr;
+    const dim3 g((unsigned)((T.nx + Z2_W - 1) / Z2_W), (unsigned)((T.ny + RH - 5) / (RH - 4)),
+                 (unsigned)((T.nz + T.zc - 1) / T.zc));
+    k_tv_fgp_z2<RH><<<g, z2_threads<RH>(), z2_smem<RH>(), st>>>(T);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
+}
+
+void launch_tv_fgp_z2(const Tvz2Launch& T, cudaStream_t st) {
+    // region height (output rows + 4 halo rows); A/B hook BSGD_TV_Z2H
+    static const int rh = [] {
+        const char* e = getenv("BSGD_TV_Z2H");
+        return e ? atoi(e) : 16;
+    }();
+    if (rh >= 24) launch_z2<24>(T, st);
+    else launch_z2<16>(T, st);
 }
 
 void launch_tv_out(const TvLaunch& T, float* out, cudaStream_t st) {

@@ -568,6 +568,8 @@ def test_trajectory_fuzz(bs, seed):
     ((128, 40, 70), (1, 1, 2), 0.3, 3),     # ... k = 3 (first momentum step); 35-plane slabs
     ((136, 20, 24), (1, 1, 3), 0.3, 20),    # fused float4 path: ragged x / y tiles, 3 slabs
     ((64, 48, 1), (1, 1, 1), 0.5, 50),      # fused 2D (nz = 1, L = 8)
+    ((184, 30, 50), (1, 1, 2), 0.3, 4),     # two-iteration passes: ragged 60 x 12 tiles, 9 z-chunks
+    ((64, 64, 64), (1, 1, 2), 0.2, 5),      # ... two passes and a trailing single iteration
     ((24, 16, 20), (2, 2, 2), 0.3, 20),     # octants: the generic two-kernel path
 ])
 @pytest.mark.parametrize("method", ["fgp", "chambolle"])

@@ -1,8 +1,8 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): every kernel family of the library on a scaled cone problem -- the FP / BP
 traversals (v3 + steep v2 companions, COUNT, deterministic BP), the residual, the block
-update, Algo 3's reductions, the IM weights, the fused FGP TV prox (float4 and scalar
-layouts), the generic TV path of non-slab grids, TV(x), the solvers, and the virtual-rank
+update, Algo 3's reductions, the IM weights, the fused FGP TV prox (two-iteration passes,
+float4 and scalar layouts), the generic TV path of non-slab grids, TV(x), the solvers, and the virtual-rank
 collectives (band exchange, halos).
 
     compute-sanitizer --tool racecheck python tools/sanitize.py
@@ -48,6 +48,13 @@ def main():
     proj = torch.zeros(g.n_rays, device="cuda")
     for j in range(4):
         ctx.forward([0, 5], j, x[j * ctx.block_voxels:(j + 1) * ctx.block_voxels], proj)
+    ctx.close()
+    torch.cuda.synchronize()
+    # two-iteration TV passes (k_tv_fgp_z2) over several 60 x 12 tiles and z-chunks, odd count
+    gt = synth.Geometry(2, synth.circular("cone", 4, 360.0, 800.0, 500.0, 8, 8, 1.0, 1.0), 8, 8, (136, 30, 40))
+    ctx = bs.Context.from_geometry(gt, (1, 1, 2), 1)
+    xt = torch.rand(136 * 30 * 40, device="cuda")
+    ctx.tv_prox(xt, 0.2, 5)
     ctx.close()
     torch.cuda.synchronize()
     # virtual ranks: band exchange + TV halos
