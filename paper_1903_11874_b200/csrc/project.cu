@@ -68,6 +68,15 @@ __device__ __forceinline__ bool lane_steep(const double b[3]) {
     const double lim = fabs(b[1]) * (1.0 - 1.0 / 1073741824.0);
     return b[1] == 0.0 || !(fabs(b[0]) < lim) || !(fabs(b[2]) < lim);
 }
+// FP: a non-zero minor slope |b_c / b_1| < 2^-16.  The v3 FP takes the crossing point from
+// the high word of its 64-bit plane distance (u = D_hi 2^32 / K), which moves a crossing by
+// < 2^32 / K = 2^-32 / |k| of a slice: fine for |k| >= 2^-16 (< 5e-7 of a ray sum), so warps
+// with a smaller non-zero slope go to the v2 companion like steep ones (rare: a ray within
+// 2^-16 rad of a grid axis)
+__device__ __forceinline__ bool lane_fine(const double b[3]) {
+    const double f = fabs(b[1]) * (1.0 / 65536.0);
+    return (b[0] != 0.0 && fabs(b[0]) < f) || (b[2] != 0.0 && fabs(b[2]) < f);
+}
 // v3 main axis, chosen per WARP (majority of its rays; the lanes must share one layout for
 // coalescing): fewer steep lanes than a per-view choice where the fan/cone spans 45 deg.
 __device__ __forceinline__ bool warp_main_x(const double b[3], bool inrect) {
@@ -75,10 +84,12 @@ __device__ __forceinline__ bool warp_main_x(const double b[3], bool inrect) {
     const unsigned n = __ballot_sync(0xffffffffu, inrect);
     return 2 * __popc(vx) > __popc(n);
 }
-// lane_steep evaluated in the v3 frame of a world-frame direction b
-__device__ __forceinline__ bool lane_steep_v3(const double b[3], bool mainX) {
+// the v3 kernel's companion predicate (steep, or FP with a fine slope) evaluated in the v3
+// frame of a world-frame direction b
+template <int MODE>
+__device__ __forceinline__ bool lane_v2_v3(const double b[3], bool mainX) {
     const double f[3] = {mainX ? b[1] : b[0], mainX ? b[0] : b[1], b[2]};
-    return lane_steep(f);
+    return lane_steep(f) || (MODE == PROJ_FP && lane_fine(f));
 }
 
 // FP output address of ray (view, iu, iv): the full-length vector, or the block's packed
@@ -162,7 +173,7 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     make_ray(L.g, vec, iu, iv, a, b);
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     bool steep3 = false;   // STEEP_ONLY: the v3 kernel's predicate, in the v3 kernel's frame
-    if (STEEP_ONLY) steep3 = lane_steep_v3(b, warp_main_x(b, inrect));
+    if (STEEP_ONLY) steep3 = lane_v2_v3<MODE>(b, warp_main_x(b, inrect));
     int lo[3] = {B.lo[0], B.lo[1], B.lo[2]}, hi[3] = {B.hi[0], B.hi[1], B.hi[2]};
     if (mainX) {
         double t = a[0]; a[0] = a[1]; a[1] = t;
@@ -473,7 +484,9 @@ __device__ __forceinline__ bool walk3_setup(const ProjLaunch& L, const BlockDesc
     // the v2 kernel takes this warp if a lane's ray is steep or starts / ends inside the box
     // (source or detector within the block: no face to exit through, the zero border would
     // not absorb the rest of the slice)
-    if (__any_sync(0xffffffffu, hit && (lane_steep(b) || amin == 0.0 || amax == 1.0))) return false;
+    if (__any_sync(0xffffffffu, hit && (lane_steep(b) || (MODE == PROJ_FP && lane_fine(b)) || amin == 0.0 ||
+                                        amax == 1.0)))
+        return false;
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     float rs = 0.f;
     W.S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
@@ -566,6 +579,7 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
     unsigned long long DX = W.DX, DZ = W.DZ;
     const unsigned long long KX = W.KX, KZ = W.KZ;
     const float ikx = W.ikx, ikz = W.ikz, slo = W.slo, shi_last = W.shi_last, Ls = W.Ls, S = W.S;
+    const float ikxh = ikx * 4294967296.f, ikzh = ikz * 4294967296.f;   // FP: 2^32 / K
     unsigned o = W.o;
     const int sxo = W.sxo, pstep = W.pstep, k0 = W.k0, nk = W.nk, rowstep = W.rowstep;
     const int view = W.view, iu = W.iu, iv = W.iv;
@@ -591,9 +605,12 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
             const bool in = (unsigned)rel <= (unsigned)nk;
             // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
             // plane distance borrows
-            const float fx = __ull2float_rn(DX) * ikx;
+            // (FP: from the high word, D_hi 2^32 / K -- I2FP.U32 on the ALU pipe instead of
+            // I2F.U64 on the XU pipe; |k| >= 2^-16 here, see lane_fine.  Without a crossing u
+            // only has to saturate: the three segments then share voxel o.)
+            const float fx = MODE == PROJ_FP ? __uint2float_rn((unsigned)(DX >> 32)) * ikxh : __ull2float_rn(DX) * ikx;
             const unsigned bx = sub_borrow(DX, KX);                 // ~0u on a plane crossing
-            const float fz = __ull2float_rn(DZ) * ikz;
+            const float fz = MODE == PROJ_FP ? __uint2float_rn((unsigned)(DZ >> 32)) * ikzh : __ull2float_rn(DZ) * ikz;
             const unsigned bz = sub_borrow(DZ, KZ);
             float l0, l1, l2, ux, uz;
             if (MODE == PROJ_COUNT) {

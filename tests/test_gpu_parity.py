@@ -136,6 +136,32 @@ def test_operator_parity_rects_and_ragged(bs):
     _fp_bp_check(bs, g2, (2, 1, 2), 1, np.arange(6), range(4))
 
 
+def test_operator_parity_small_slopes(bs):
+    """Rays within a hair of a grid axis: minor slopes |k| = 0, 3e-6, 1.4e-5 (below 2^-16:
+    the FP warp goes to the v2 companion, lane_fine) and 1.6e-5 .. 3e-4 (the v3 FP takes the
+    crossing point from the high word of its fixed-point plane distance, < 2^-32/|k| of a
+    slice) over 1024-slice walks, detector offsets on and next to voxel planes, random x
+    (large neighbour differences): FP and BP per ray / voxel against the oracle."""
+    ks = [0.0, 3e-6, 1.4e-5, 1.6e-5, 2.5e-5, 6e-5, 3e-4, -2e-5, -4e-6]
+    nu = 91
+    vecs = np.zeros((len(ks), 12))
+    for i, k in enumerate(ks):
+        d = np.array([-k, -1.0, 0.0]) / np.hypot(k, 1.0)      # parallel rays along -y, x slope k
+        vecs[i, 0:3] = d
+        vecs[i, 3:6] = (0.013 if i % 2 else 0.0, 0.0, 0.0)    # on-plane and off-plane offsets
+        vecs[i, 6:9] = 0.7 * np.array([-d[1], d[0], 0.0])
+        vecs[i, 9:12] = (0.0, 0.0, 1.0)
+    g = synth.Geometry(synth.PARALLEL, vecs, nu, 1, (64, 1024, 1))
+    wf, wb = _fp_bp_check(bs, g, (1, 2, 1), 1, np.arange(len(ks)), range(2))
+    print(f"small slopes: worst FP |d|/tol {wf:.3g}, worst BP |d|/tol {wb:.3g}")
+    # cone beam: z slopes of about -1e-4 that cross the slab boundary plane z = 128 inside
+    # the volume (source 0.3 above it, detector centre 0.1 below), rows 0.004 apart
+    vc = synth.circular("cone", 4, 360.0, 3000.0, 1000.0, 24, 9, 1.0, 0.004)
+    vc[:, 2], vc[:, 5] = 0.3, -0.1
+    g3 = synth.Geometry(synth.CONE, vc, 24, 9, (16, 16, 256))
+    _fp_bp_check(bs, g3, (1, 1, 2), 1, np.arange(4), range(2), seed=3)
+
+
 @pytest.mark.parametrize("tilt", [20.0, 40.0])
 def test_operator_parity_laminography_octants(bs, tilt):
     """N4: an arbitrary trajectory through the per-view vectors — cone-beam
