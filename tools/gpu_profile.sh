@@ -21,9 +21,9 @@ timeout 900 ncu --section SpeedOfLight --section MemoryWorkloadAnalysis --sectio
   --metrics lts__t_sectors_op_red.sum,lts__t_requests_op_red.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum \
   --clock-control none -k regex:k_project3 -s 7 -c 1 -o gpurun_out/prof_bp_${TAG} -f \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-tv --cheap-data > gpurun_out/prof_bp_${TAG}.log 2>&1
-# one block update (a slab) and one z-marching TV iteration
-timeout 600 ncu --set full --clock-control none -k regex:k_block_update -s 40 -c 1 -o gpurun_out/prof_upd_${TAG} -f \
+# one block update (a slab) and one two-iteration TV pass (k_tv_fgp_z2, the one-rank default)
+timeout 600 ncu --set full --clock-control none -k regex:k_block_update -s 8 -c 1 -o gpurun_out/prof_upd_${TAG} -f \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-tv --cheap-data > gpurun_out/prof_upd_${TAG}.log 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:k_tv_fgp_z -s 25 -c 1 -o gpurun_out/prof_tv_${TAG} -f \
+timeout 600 ncu --set full --clock-control none -k regex:k_tv_fgp_z2 -s 14 -c 1 -o gpurun_out/prof_tv_${TAG} -f \
   python tools/tv_profile.py 1024 1024 1024 8 > gpurun_out/prof_tv_${TAG}.log 2>&1
 ls -la gpurun_out
