@@ -322,8 +322,11 @@ bsgd_status bsgd_allreduce_time(bsgd_ctx ctx, int64_t count, int32_t iters, void
  * bsgd_create, host-side counters of what this rank SENT for line 7 of the epochs it ran:
  * band mode (world > 1, default): the partial projection sums on the detector rows where this
  * rank's band (the rows its blocks project into) overlaps a peer's, one message per (peer,
- * view); full mode (environment BSGD_EXCHANGE=full): the ring allreduce's 2 (G-1)/G of the
- * selected rows' buffer per epoch.  *band_mode (nullable) = 1 in band mode.  In band mode the
+ * view); LSA mode (environment BSGD_EXCHANGE=lsa): the same overlap rows, read by this rank's
+ * residual kernel directly from each peer's partial-sum buffer (an NCCL symmetric window;
+ * counted as the bytes this rank READ, one "message" per peer); full mode (BSGD_EXCHANGE=full):
+ * the ring allreduce's 2 (G-1)/G of the selected rows' buffer per epoch.  *band_mode
+ * (nullable) = 1 in band mode, 2 in LSA mode, 0 in full mode.  In band and LSA mode the
  * residual r is formed on this rank's band rows only (bsgd_get_state's r is valid there;
  * rows no band covers keep r = y).  Errors: BSGD_E_CONTRACT for NULL outputs.            */
 bsgd_status bsgd_comm_stats(bsgd_ctx ctx, uint64_t* bytes_sent, uint64_t* messages, int32_t* band_mode);

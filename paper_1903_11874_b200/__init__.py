@@ -539,7 +539,8 @@ class Context:
         (bsgd_comm_stats)."""
         b, m, band = C.c_uint64(), C.c_uint64(), C.c_int32()
         self._c(_lib.bsgd_comm_stats(self.h, C.byref(b), C.byref(m), C.byref(band)))
-        return {"bytes_sent": int(b.value), "messages": int(m.value), "mode": "band" if band.value else "full"}
+        return {"bytes_sent": int(b.value), "messages": int(m.value),
+                "mode": {0: "full", 1: "band", 2: "lsa"}[int(band.value)]}
 
     def exchange_plan(self, world, views) -> dict:
         """Bytes one epoch's residual exchange would send over `world` ranks for the given

@@ -110,6 +110,18 @@ struct bsgd_ctx_s {
     // rows no band covers stay r = y).  ||r_I||^2: each row counted by the lowest rank whose
     // band covers it, one M-double allreduce.  BSGD_EXCHANGE=full keeps the full allreduce.
     bool band = false;
+    // LSA mode (BSGD_EXCHANGE=lsa, band mode over NCCL): the band residual kernel reads the
+    // peers' partial sums straight from their memory over NVLink -- pc is an NCCL symmetric
+    // window (ncclMemAlloc + ncclCommWindowRegister), each peer's copy addressed through
+    // ncclGetPeerPointer -- so there is no pack kernel, no send / receive buffers and no
+    // ncclSend / ncclRecv; a one-float allreduce orders "every rank wrote pc" before the reads,
+    // the ||r_I||^2 allreduce that follows orders the reads before the next epoch's writes.
+    // Virtual ranks emulate it with each other's pc pointers (same device).
+    bool lsa = false;
+    void* pc_win = nullptr;                // ncclWindow_t of pc (NCCL ranks)
+    bool pc_ncclmem = false;               // pc from ncclMemAlloc
+    std::vector<const float*> lsa_pc;      // per rank: its pc as this device addresses it
+    float* d_bar = nullptr;                // the one-float "partials written" allreduce
     std::vector<int2> bands;         // [world][n_views] (lo, hi)
     float *ex_send = nullptr, *ex_recv = nullptr;   // packed overlap chunks (sent / received)
     long long ex_cap = 0;
@@ -257,6 +269,15 @@ struct bsgd_ctx_s {
     }
     float* pN(float* base, long long b) const { return base + b * padN + orgN; }
     float* pT(float* base, long long b) const { return base + b * padT + orgT; }
+    // the LSA window and its memory go before the communicator
+    void release_comm() {
+        if (pc_win && comm) ncclCommWindowDeregister(comm, (ncclWindow_t)pc_win);
+        pc_win = nullptr;
+        if (pc_ncclmem) ncclMemFree(pc);
+        pc_ncclmem = false;
+        if (comm) ncclCommDestroy(comm);
+        comm = nullptr;
+    }
     void release() {
         if (order_ev) cudaEventDestroy(order_ev);
         order_ev = nullptr;
@@ -636,7 +657,25 @@ struct bsgd_ctx_s {
     void band_residual(ResLaunch& Rl, const std::vector<int>& vsel, const std::vector<int>& sel_rows,
                        const int* drows, std::vector<char>& staging, size_t& off, cudaStream_t st) {
         const int V = (int)vsel.size();
-        const ExPlan P = band_exchange(vsel, staging, off, st);
+        const ExPlan P = lsa ? plan_for(rank, vsel) : band_exchange(vsel, staging, off, st);
+        std::vector<const float*> peer(world, nullptr);
+        if (lsa) {   // every rank's pc written, then read in place from its memory
+            if (vg) {
+                vg_offer(pc, st);
+                for (int h = 0; h < world; ++h) {
+                    BSGD_CUDA(cudaStreamWaitEvent(st, vg->ev1[h], 0));
+                    peer[h] = (const float*)vg->src[h];
+                }
+            } else {
+                BSGD_NCCL(ncclAllReduce(d_bar, d_bar, 1, ncclFloat, ncclSum, comm, st));
+                peer = lsa_pc;
+            }
+            for (int h = 0; h < world; ++h)   // bytes this rank reads from peer h's memory
+                if (P.off[h + 1] > P.off[h]) {
+                    comm_bytes += 4ull * (unsigned long long)(P.off[h + 1] - P.off[h]);
+                    ++comm_msgs;
+                }
+        }
         std::vector<int2> bt((size_t)V * world), rg(V);
         for (int k = 0; k < V; ++k) {
             for (int h = 0; h < world; ++h) bt[(size_t)k * world + h] = band_of(h, vsel[k]);
@@ -644,8 +683,9 @@ struct bsgd_ctx_s {
         }
         // element (slot k, row v, column u) of peer h's partial sums sits at ex_recv[k per + v nu +
         // u + adj[k][h]] (only rows of band_me ∩ band_h are read); own pc: adj = 0
+        // (LSA: peer h's own pc, adj = 0)
         std::vector<long long> adj((size_t)V * world, 0);
-        for (int h = 0; h < world; ++h) {
+        for (int h = 0; h < world && !lsa; ++h) {
             long long d = P.off[h];
             for (auto& c : P.ch[h]) {
                 adj[(size_t)c.k * world + h] = d - c.src;
@@ -653,7 +693,8 @@ struct bsgd_ctx_s {
             }
         }
         std::vector<const float*> dp(world, nullptr);
-        for (int h = 0; h < world; ++h) dp[h] = h == rank ? pc : (P.off[h + 1] > P.off[h] ? ex_recv : nullptr);
+        for (int h = 0; h < world; ++h)
+            dp[h] = h == rank ? pc : (P.off[h + 1] > P.off[h] ? (lsa ? peer[h] : ex_recv) : nullptr);
         const size_t start = off;
         BandLaunch B;
         B.n_slots = V;
@@ -672,6 +713,7 @@ struct bsgd_ctx_s {
         B.r = Rl.r;
         B.part = d_rpart;
         launch_residual_band(B, st);
+        if (lsa && vg) vg_release(st);
         ResLaunch Rn = Rl;
         Rn.normsq = d_npart;
         launch_zero_rows(d_npart, drows, (int)sel_rows.size(), st);
@@ -1769,9 +1811,12 @@ bsgd_status bsgd_create_ex(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block
         c->accT = c->dnew_pad(c->s, true);
         if (const char* e = getenv("BSGD_FORCE_NCCL")) c->coll = atoi(e) != 0;   // test hook
         if (c->world > 1) c->coll = true;
-        c->pc = c->coll ? c->dnew<float>(c->n_rays) : nullptr;
+        const char* exch = getenv("BSGD_EXCHANGE");
+        c->lsa = c->coll && exch && std::string(exch) == "lsa";
+        // LSA over NCCL: pc comes from ncclMemAlloc once the communicator exists (below)
+        c->pc = c->coll && !(c->lsa && !c->vg) ? c->dnew<float>(c->n_rays) : nullptr;
         if (c->world > 1) {
-            const char* e = getenv("BSGD_EXCHANGE");
+            const char* e = exch;
             c->band = !(e && std::string(e) == "full");
             if (c->band) {
                 c->compute_bands();
@@ -1799,10 +1844,33 @@ bsgd_status bsgd_create_ex(const bsgd_geometry* geom, bsgd_dims dims, bsgd_block
             BSGD_NCCL(ncclGetUniqueId(&id));
             BSGD_NCCL(ncclCommInitRank(&c->comm, 1, id, 0));
         }
+        if (c->lsa && !c->vg) {   // pc as an NCCL symmetric window, every rank's copy addressable
+            const size_t bytes = sizeof(float) * (size_t)c->n_rays;
+            BSGD_NCCL(ncclMemAlloc((void**)&c->pc, bytes));
+            c->pc_ncclmem = true;
+            BSGD_CUDA(cudaMemset(c->pc, 0, bytes));
+            ncclWindow_t w = nullptr;
+            BSGD_NCCL(ncclCommWindowRegister(c->comm, c->pc, bytes, &w, NCCL_WIN_COLL_SYMMETRIC));
+            c->pc_win = w;
+            void** dptr = (void**)c->dalloc(sizeof(void*) * (size_t)c->world);
+            launch_lsa_ptrs(w, c->world, dptr, 0);
+            std::vector<void*> hp((size_t)c->world);
+            BSGD_CUDA(cudaMemcpy(hp.data(), dptr, sizeof(void*) * hp.size(), cudaMemcpyDeviceToHost));
+            for (void* q : hp) c->lsa_pc.push_back((const float*)q);
+            // the window's own-rank address is a second mapping of pc: a value written through
+            // it must read back through pc
+            const float probe = 1234.5f;
+            float back = 0.f;
+            BSGD_CUDA(cudaMemcpy((void*)c->lsa_pc[c->rank], &probe, sizeof probe, cudaMemcpyHostToDevice));
+            BSGD_CUDA(cudaMemcpy(&back, c->pc, sizeof back, cudaMemcpyDeviceToHost));
+            if (back != probe) fail(BSGD_E_NCCL, "LSA exchange: the window's own-rank address does not alias pc");
+            BSGD_CUDA(cudaMemset(c->pc, 0, sizeof(float)));
+            c->d_bar = c->dnew<float>(1);
+        }
         BSGD_CUDA(cudaDeviceSynchronize());
     });
     if (st != BSGD_OK) {
-        if (c->comm) ncclCommDestroy(c->comm);
+        c->release_comm();
         c->release();
         return st;
     }
@@ -1833,7 +1901,7 @@ void bsgd_vgroup_destroy(bsgd_vgroup g) {
 void bsgd_destroy(bsgd_ctx ctx) {
     if (!ctx) return;
     cudaDeviceSynchronize();
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    ctx->release_comm();
     ctx->release();
     delete ctx;
 }
@@ -2545,7 +2613,7 @@ bsgd_status bsgd_comm_stats(bsgd_ctx c, uint64_t* bytes_sent, uint64_t* messages
         if (!c || !bytes_sent || !messages) fail(BSGD_E_CONTRACT, "bad arguments");
         *bytes_sent = c->comm_bytes;
         *messages = c->comm_msgs;
-        if (band_mode) *band_mode = c->band ? 1 : 0;
+        if (band_mode) *band_mode = c->band ? (c->lsa ? 2 : 1) : 0;
     });
 }
 

@@ -278,5 +278,8 @@ struct Tvz2Launch {
     int pf;                    // L2 prefetch distance in planes (0 = none)
 };
 void launch_tv_fgp_z2(const Tvz2Launch& T, cudaStream_t st);
+// out[h] = this device's address of rank h's copy of an NCCL symmetric window (LSA exchange;
+// w: the ncclWindow_t, n: world size)
+void launch_lsa_ptrs(void* w, int n, void** out, cudaStream_t st);
 
 }  // namespace bsgd

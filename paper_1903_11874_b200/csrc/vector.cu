@@ -9,6 +9,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <nccl.h>
+#include <nccl_device.h>
+
 #include "internal.h"
 
 namespace bsgd {
@@ -1572,6 +1575,17 @@ void launch_tv_fgp_z2(const Tvz2Launch& T, cudaStream_t st) {
     }();
     if (rh >= 24) launch_z2<24>(T, st);
     else launch_z2<16>(T, st);
+}
+
+__global__ void k_lsa_ptrs(ncclWindow_t w, int n, void** out) {
+    const int h = threadIdx.x;
+    if (h < n) out[h] = ncclGetPeerPointer(w, 0, h);
+}
+
+void launch_lsa_ptrs(void* w, int n, void** out, cudaStream_t st) {
+    k_lsa_ptrs<<<1, 32, 0, st>>>((ncclWindow_t)w, n, out);
+    BSGD_CUDA(cudaGetLastError());
+    note_launch();
 }
 
 void launch_tv_out(const TvLaunch& T, float* out, cudaStream_t st) {

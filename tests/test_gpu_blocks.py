@@ -162,7 +162,9 @@ def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
     """N2: the residual formed from the peers' partial sums on overlapping
     detector bands only (default for world > 1) reproduces the oracle's Algo 1 + Algo 3
     trajectory, and the full-allreduce mode (BSGD_EXCHANGE=full), on G virtual ranks of a
-    scaled cfg5-shaped cone problem (8 z-slabs); it sends >= 4x fewer bytes."""
+    scaled cfg5-shaped cone problem (8 z-slabs); it sends >= 4x fewer bytes.  LSA mode
+    (BSGD_EXCHANGE=lsa): the residual kernel reads the same overlap rows straight from the
+    peers' partial-sum buffers (here the other virtual ranks' buffers on the same device)."""
     p, g, vol32, y = problem("cfg5", K=64, n_views=36)
     P = Projector(g, BlockGrid(g.dims, p.blocks))
     mu = float(np.float32(1.5 / ob.power_iteration(P, 20, seed=1)))
@@ -175,7 +177,7 @@ def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
         o.epoch()
     nb = p.N // G
     runs = {}
-    for mode in ("band", "full"):
+    for mode in ("band", "full", "lsa"):
         monkeypatch.setenv("BSGD_EXCHANGE", mode)
         group = bs.VirtualGroup(G)
         ctxs = [bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=11, rank=r, world=G,
@@ -196,7 +198,7 @@ def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
         for e in range(E):
             views = [v for i in out[0][0].sel_rows[e] for v in ctxs[0].row_block_views(int(i))]
             pl = ctxs[0].exchange_plan(G, views)
-            plan += pl["band_bytes"] if mode == "band" else pl["full_bytes"]
+            plan += pl["full_bytes"] if mode == "full" else pl["band_bytes"]   # lsa reads what band sends
         for c in ctxs:
             c.close()
         group.close()
@@ -222,6 +224,7 @@ def test_band_exchange_matches_oracle_and_full_allreduce(bs, G, monkeypatch):
     band = sum(o_[2]["bytes_sent"] for o_ in runs["band"])
     full = sum(o_[2]["bytes_sent"] for o_ in runs["full"])
     assert 0 < band and 4 * band <= full, (band, full)
+    assert sum(o_[2]["bytes_sent"] for o_ in runs["lsa"]) == band      # the same overlap rows, read in place
 
 
 # ----------------------------------------------------------------- unequal z-slabs (N3)

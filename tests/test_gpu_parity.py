@@ -497,6 +497,29 @@ def test_collective_path_one_rank(bs, monkeypatch):
         assert np.allclose(out[0][k], out[1][k], rtol=1e-5, atol=0)
 
 
+def test_lsa_window_one_rank(bs, monkeypatch):
+    """The LSA exchange set-up on real NCCL (N2): with a one-rank communicator
+    (BSGD_FORCE_NCCL=1) and BSGD_EXCHANGE=lsa the partial-sum buffer comes from ncclMemAlloc,
+    is registered as a symmetric window and a value written through its own-rank
+    ncclGetPeerPointer address must read back through the buffer (the create fails
+    otherwise); the run through that buffer reproduces the plain run."""
+    p, g, vol32, y = problem("cfg3", K=32, n_views=30)
+    P = Projector(g, BlockGrid(g.dims, p.blocks))
+    mu = 1.5 / ob.power_iteration(P, 20, seed=1)
+    out = []
+    for env in ({"BSGD_FORCE_NCCL": "0"}, {"BSGD_FORCE_NCCL": "1", "BSGD_EXCHANGE": "lsa"}):
+        monkeypatch.delenv("BSGD_EXCHANGE", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ctx = bs.Context.from_geometry(g, p.blocks, p.M, kind="random", row_seed=2)
+        xd = torch.zeros(ctx.owned_count * ctx.block_voxels, device="cuda")
+        res = ctx.run(torch.from_numpy(y).cuda(), xd, epochs=8, mu0=mu, seed=4, rows_per_epoch=1, cols_per_epoch=4)
+        out.append((xd.cpu().numpy(), res.obj.copy()))
+        ctx.close()
+    assert np.allclose(out[0][1], out[1][1], rtol=1e-5, atol=0)
+    assert np.max(np.abs(out[0][0] - out[1][0])) <= 1e-5 * np.max(np.abs(out[0][0]))
+
+
 @pytest.mark.parametrize("pinned", [True, False])
 def test_host_buffer_run_matches_device_run(bs, pinned):
     """bsgd_run with y / x in host memory (uploads overlapped with the first epoch on a
