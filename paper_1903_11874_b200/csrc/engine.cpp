@@ -177,10 +177,11 @@ struct bsgd_ctx_s {
     void ensure_copy_stream() {
         if (copy_st) return;
         BSGD_CUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
-        up_ev.resize(s + 2);
+        up_ev.resize(s + 3);   // x blocks, y of the first epoch's rows, misc, the rest of y
         for (auto& e : up_ev) BSGD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         d_normsq0 = dnew<double>(M);
     }
+    int* d_rows_tmp = nullptr;         // M ints: a row-block list for one launch
     double* d_red = nullptr;           // 8 doubles scratch
     double* d_log = nullptr;           // per-epoch [obj, rmse] scratch
     long long d_log_cap = 0;
@@ -731,7 +732,7 @@ struct bsgd_ctx_s {
     // (its ||y_I||^2 are kept in d_normsq0 for Algo 3's ||r||^0).
     struct Upload {
         const std::vector<cudaEvent_t>* xev = nullptr;
-        cudaEvent_t yev = nullptr;
+        cudaEvent_t yev = nullptr;       // host y: the views of this (first) epoch's selected rows
         bool y_reset = false;
         // last epoch of a host-x run: each block's x goes to the host as soon as its final
         // update is done (the BP of the final row block then runs block by block), so the
@@ -799,8 +800,8 @@ struct bsgd_ctx_s {
         }
         if (up && up->yev) {
             BSGD_CUDA(cudaStreamWaitEvent(st, up->yev, 0));
-            if (up->y_reset) {
-                reset_r(y, st);
+            if (up->y_reset) {   // the selected rows now; the others after this epoch (bsgd_run)
+                reset_r(y, st, &sel_rows);
                 BSGD_CUDA(cudaMemcpyAsync(d_normsq0, d_normsq, sizeof(double) * M, cudaMemcpyDeviceToDevice, st));
             }
         }
@@ -957,20 +958,24 @@ struct bsgd_ctx_s {
         rnorm_hist.clear();
     }
     // ... and r = y on every row block with ||r_I||^2 (needs y on the device)
-    void reset_r(const float* y, cudaStream_t st) {
-        BSGD_CUDA(cudaMemsetAsync(d_normsq, 0, sizeof(double) * M, st));
+    // only: the row blocks to reset (nullptr: all; d_normsq of the others is left untouched)
+    void reset_r(const float* y, cudaStream_t st, const std::vector<int>* only = nullptr) {
+        if (!only) BSGD_CUDA(cudaMemsetAsync(d_normsq, 0, sizeof(double) * M, st));
         // r = y - sum z = y on every row block, with ||r_I||^2 (Algo 1 line 1)
-        std::vector<int> all(n_views), srow(n_views);
-        int pos = 0;
-        for (int i = 0; i < M; ++i)
+        std::vector<int> all, srow;
+        std::vector<int> blocks_;
+        if (only) blocks_ = *only;
+        else for (int i = 0; i < M; ++i) blocks_.push_back(i);
+        for (int i : blocks_)
             for (int v : rows[i]) {
-                all[pos] = v;
-                srow[pos++] = i;
+                all.push_back(v);
+                srow.push_back(i);
             }
+        if (all.empty()) return;
         std::vector<char> staging;
         size_t off = 0;
         ResLaunch Rl;
-        Rl.n_slots = n_views;
+        Rl.n_slots = (int)all.size();
         Rl.views = tab_put(off, all, staging);
         Rl.slot_row = tab_put(off, srow, staging);
         tab_upload(staging, off, st);
@@ -2134,11 +2139,31 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             c->x_events.assign(c->up_ev.begin(), c->up_ev.begin() + c->s);
             up.xev = &c->x_events;
         }
+        // y in the order of use: the views of the first epoch's selected row blocks (the first
+        // residual waits only for them), then the rest (waited for after the first epoch)
+        std::vector<int> rows_first(aM), rows_rest;
         if (y_host) {
             if (!c->y_dev) c->y_dev = c->dnew<float>(c->n_rays, false);
-            BSGD_CUDA(cudaMemcpyAsync(c->y_dev, y_in, sizeof(float) * c->n_rays, cudaMemcpyHostToDevice,
-                                      c->copy_st));
-            BSGD_CUDA(cudaEventRecord(c->up_ev[c->s], c->copy_st));
+            const int eg0 = (P->flags & BSGD_RESUME) ? c->epoch : 0;
+            host::select(P->seed, 1, eg0, c->M, aM, rows_first.data());
+            std::vector<char> first((size_t)c->n_views, 0);
+            for (int i : rows_first)
+                for (int v : c->rows[i]) first[(size_t)v] = 1;
+            for (int i = 0; i < c->M; ++i)
+                if (std::find(rows_first.begin(), rows_first.end(), i) == rows_first.end()) rows_rest.push_back(i);
+            const size_t per = (size_t)c->per;
+            for (int pass = 1; pass >= 0; --pass) {   // runs of consecutive views of each group
+                for (int v = 0; v < c->n_views;) {
+                    if (first[(size_t)v] != pass) { ++v; continue; }
+                    int w = v;
+                    while (w < c->n_views && first[(size_t)w] == pass) ++w;
+                    BSGD_CUDA(cudaMemcpyAsync(c->y_dev + (size_t)v * per, y_in + (size_t)v * per,
+                                              sizeof(float) * per * (size_t)(w - v), cudaMemcpyHostToDevice,
+                                              c->copy_st));
+                    v = w;
+                }
+                BSGD_CUDA(cudaEventRecord(c->up_ev[pass ? c->s : c->s + 2], c->copy_st));
+            }
             y = c->y_dev;
             up.yev = c->up_ev[c->s];
         }
@@ -2158,7 +2183,10 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
                 up.y_reset = true;
                 defer_r0 = true;
             } else {
-                if (y_host) BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
+                if (y_host) {
+                    BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
+                    BSGD_CUDA(cudaStreamWaitEvent(st, c->up_ev[c->s + 2], 0));
+                }
                 c->reset(y, st);
             }
             c->mu = P->mu0;
@@ -2174,7 +2202,10 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             c->rnorm_hist.push_back(sqrt(s2));
         };
         if (c->rnorm_hist.empty() && !defer_r0) {
-            if (y_host && up.yev) BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
+            if (y_host && up.yev) {
+                BSGD_CUDA(cudaStreamWaitEvent(st, up.yev, 0));
+                BSGD_CUDA(cudaStreamWaitEvent(st, c->up_ev[c->s + 2], 0));
+            }
             push_r0(c->d_normsq);
         }
         if (im && !uni) c->ensure_im_table(st, (P->flags & BSGD_IS_AREA) ? 1 : 0);
@@ -2260,6 +2291,16 @@ bsgd_status bsgd_run(bsgd_ctx c, const float* y_in, float* x_in, const float* xt
             }
             c->epoch_step(y, x, rows, sgd ? std::vector<int>() : cols, tiles, (float)c->mu, sgd, st, evp, false,
                           hook);
+            if (e == 0 && y_host) {   // the rest of y: r = y and ||y_I||^2 on the row blocks not selected
+                BSGD_CUDA(cudaStreamWaitEvent(st, c->up_ev[c->s + 2], 0));
+                if (defer_r0 && !rows_rest.empty()) {
+                    c->reset_r(y, st, &rows_rest);
+                    if (!c->d_rows_tmp) c->d_rows_tmp = c->dnew<int>(c->M, false);
+                    BSGD_CUDA(cudaMemcpyAsync(c->d_rows_tmp, rows_rest.data(), sizeof(int) * rows_rest.size(),
+                                              cudaMemcpyHostToDevice, st));
+                    launch_copy_rows(c->d_normsq0, c->d_normsq, c->d_rows_tmp, (int)rows_rest.size(), st);
+                }
+            }
             if (e == 0 && defer_r0) push_r0(c->d_normsq0);
             if (want_visits) {   // FP visits of this epoch on this rank (BP visits are the same segments)
                 unsigned long long nvt = 0;
