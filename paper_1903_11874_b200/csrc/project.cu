@@ -25,6 +25,14 @@
 #include "internal.h"
 
 namespace bsgd {
+#ifndef PROJ3_FP32STEP
+#define PROJ3_FP32STEP 1   // FP: 32-bit plane distances (0: the 64-bit stepping, for A/B)
+#endif
+#if PROJ3_FP32STEP
+#define PROJ3_FINE 4096.0
+#else
+#define PROJ3_FINE 65536.0
+#endif
 #ifndef PROJ3_MINB
 #define PROJ3_MINB 4
 #endif
@@ -74,7 +82,7 @@ __device__ __forceinline__ bool lane_steep(const double b[3]) {
 // with a smaller non-zero slope go to the v2 companion like steep ones (rare: a ray within
 // 2^-16 rad of a grid axis)
 __device__ __forceinline__ bool lane_fine(const double b[3]) {
-    const double f = fabs(b[1]) * (1.0 / 65536.0);
+    const double f = fabs(b[1]) * (1.0 / PROJ3_FINE);
     return (b[0] != 0.0 && fabs(b[0]) < f) || (b[2] != 0.0 && fabs(b[2]) < f);
 }
 // v3 main axis, chosen per WARP (majority of its rays; the lanes must share one layout for
@@ -404,6 +412,14 @@ __device__ __forceinline__ unsigned sub_borrow(unsigned long long& D, unsigned l
     return m;
 }
 
+// 32-bit form: D -= K, ~0u on a borrow
+__device__ __forceinline__ unsigned sub_borrow32(unsigned& D, unsigned K) {
+    unsigned m, Dn;
+    asm("sub.cc.u32 %0, %2, %3;\n\tsubc.u32 %1, 0, 0;" : "=r"(Dn), "=r"(m) : "r"(D), "r"(K));
+    D = Dn;
+    return m;
+}
+
 // Distance from coordinate c (mirrored so that it increases along the ray) to the next
 // plane in 2^-64 voxel units, and the cell the walk starts in.  A point exactly on a plane
 // with a non-zero slope starts in the cell below with distance 0 (a zero-length segment,
@@ -561,6 +577,33 @@ __device__ __forceinline__ bool walk3_setup(const ProjLaunch& L, const BlockDesc
         W.shi_last = (float)fmin(fmax((amax - (yin1 - a[1]) * inv[1]) * fabs(b[1]), 0.0), 1.0);
         if (j1 == j0) W.shi_last = fmaxf(W.shi_last, W.slo);
         W.Ls = (float)(blen * ainv1);
+#if PROJ3_FP32STEP
+        if (MODE == PROJ_FP) {
+            // The 32-bit walk (2^-32 voxel distances, K rounded) starts exact at the lane's OWN
+            // first slice j0 and is rewound to jstart in modular arithmetic -- D32 + k0 K32, the
+            // wraps of that sum are the crossings the k0 steps will count, o backed off by them
+            // -- so its drift (< 2^-33 voxel per step) accumulates over the lane's own slices
+            // only: a crossing moves by < N 2^-33 / |k| slices on an N-slice segment.
+            const double ap0 = (yin0 - a[1]) * inv[1];
+            const double xr0 = a[0] + ap0 * b[0] - lo[0], zr0 = a[2] + ap0 * b[2] - lo[2];
+            int cx0, cz0;
+            unsigned long long DX0 = plane_dist(mx ? -xr0 : xr0, W.KX, cx0);
+            unsigned long long DZ0 = plane_dist(mz ? -zr0 : zr0, W.KZ, cz0);
+            if (!W.KX) DX0 = ~0ull;
+            if (!W.KZ) DZ0 = ~0ull;
+            const int ix0 = mx ? -cx0 - 1 : cx0, iz0 = mz ? -cz0 - 1 : cz0;
+            const unsigned kx32 = (unsigned)((W.KX >> 32) + ((W.KX >> 31) & 1ull));
+            const unsigned kz32 = (unsigned)((W.KZ >> 32) + ((W.KZ >> 31) & 1ull));
+            const unsigned long long tx = (DX0 >> 32) + (unsigned long long)(unsigned)W.k0 * kx32;
+            const unsigned long long tz = (DZ0 >> 32) + (unsigned long long)(unsigned)W.k0 * kz32;
+            W.DX = tx << 32;                                        // the kernel takes the high words
+            W.DZ = tz << 32;
+            const unsigned o_lane = (unsigned)iz0 * (unsigned)plane + (unsigned)(j0 - lo[1]) * (unsigned)bdx +
+                                    (unsigned)ix0;
+            W.o = o_lane - (unsigned)W.k0 * (unsigned)(sy * bdx) - (unsigned)(tx >> 32) * (unsigned)W.sxo -
+                  (unsigned)(tz >> 32) * (unsigned)W.pstep;
+        }
+#endif
     }
     W.rowstep = sy * bdx;
     W.wbp = W.Ls * rs;   // BP weight per unit of main-axis travel
@@ -578,8 +621,16 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
     const int jlo_p = W.jlo_p, jhi_p = W.jhi_p, jlo_n = W.jlo_n, jhi_n = W.jhi_n;
     unsigned long long DX = W.DX, DZ = W.DZ;
     const unsigned long long KX = W.KX, KZ = W.KZ;
+    // FP (PROJ3_FP32STEP): the plane distances in 2^-32 voxel, D truncated, K rounded; the
+    // stepping then drifts < N 2^-33 voxel over N slices, a crossing moves by that / |k| --
+    // below 2^-32 / |k| slices for |k| >= 2^-12 (lane_fine routes smaller slopes to v2)
+    unsigned DX32 = (unsigned)(DX >> 32), DZ32 = (unsigned)(DZ >> 32);
+    const unsigned KX32 = (unsigned)((KX >> 32) + ((KX >> 31) & 1ull));
+    const unsigned KZ32 = (unsigned)((KZ >> 32) + ((KZ >> 31) & 1ull));
     const float ikx = W.ikx, ikz = W.ikz, slo = W.slo, shi_last = W.shi_last, Ls = W.Ls, S = W.S;
     const float ikxh = ikx * 4294967296.f, ikzh = ikz * 4294967296.f;   // FP: 2^32 / K
+    const float ikx32 = KX32 ? (float)(1.0 / (double)KX32) : 4.656613e-10f;   // 1 / K32 (K = 0: 2^-31)
+    const float ikz32 = KZ32 ? (float)(1.0 / (double)KZ32) : 4.656613e-10f;
     unsigned o = W.o;
     const int sxo = W.sxo, pstep = W.pstep, k0 = W.k0, nk = W.nk, rowstep = W.rowstep;
     const int view = W.view, iu = W.iu, iv = W.iv;
@@ -608,10 +659,26 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
             // (FP: from the high word, D_hi 2^32 / K -- I2FP.U32 on the ALU pipe instead of
             // I2F.U64 on the XU pipe; |k| >= 2^-16 here, see lane_fine.  Without a crossing u
             // only has to saturate: the three segments then share voxel o.)
+#if PROJ3_FP32STEP
+            float fx, fz;
+            unsigned bx, bz;
+            if (MODE == PROJ_FP) {
+                fx = __uint2float_rn(DX32) * ikx32;
+                bx = sub_borrow32(DX32, KX32);                      // ~0u on a plane crossing
+                fz = __uint2float_rn(DZ32) * ikz32;
+                bz = sub_borrow32(DZ32, KZ32);
+            } else {
+                fx = __ull2float_rn(DX) * ikx;
+                bx = sub_borrow(DX, KX);
+                fz = __ull2float_rn(DZ) * ikz;
+                bz = sub_borrow(DZ, KZ);
+            }
+#else
             const float fx = MODE == PROJ_FP ? __uint2float_rn((unsigned)(DX >> 32)) * ikxh : __ull2float_rn(DX) * ikx;
             const unsigned bx = sub_borrow(DX, KX);                 // ~0u on a plane crossing
             const float fz = MODE == PROJ_FP ? __uint2float_rn((unsigned)(DZ >> 32)) * ikzh : __ull2float_rn(DZ) * ikz;
             const unsigned bz = sub_borrow(DZ, KZ);
+#endif
             float l0, l1, l2, ux, uz;
             if (MODE == PROJ_COUNT) {
                 // exact in-block segments: the slice clamped to [s_lo, s_hi] at the lane's
