@@ -655,10 +655,10 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
             const int rel = k - kb;
             const bool in = (unsigned)rel <= (unsigned)nk;
             // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
-            // plane distance borrows
-            // (FP: from the high word, D_hi 2^32 / K -- I2FP.U32 on the ALU pipe instead of
-            // I2F.U64 on the XU pipe; |k| >= 2^-16 here, see lane_fine.  Without a crossing u
-            // only has to saturate: the three segments then share voxel o.)
+            // plane distance borrows.  FP: the 32-bit walk (I2FP.U32 on the ALU pipe, no 64-bit
+            // carries; |k| >= 2^-12 here, see lane_fine and walk3_setup); without a crossing u
+            // only has to saturate: the three segments then share voxel o.  (PROJ3_FP32STEP=0:
+            // the 64-bit walk with the high-word conversion, for A/B.)
 #if PROJ3_FP32STEP
             float fx, fz;
             unsigned bx, bz;
