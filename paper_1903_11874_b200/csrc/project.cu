@@ -29,7 +29,7 @@ namespace bsgd {
 #define PROJ3_FP32STEP 1   // FP: 32-bit plane distances (0: the 64-bit stepping, for A/B)
 #endif
 #if PROJ3_FP32STEP
-#define PROJ3_FINE 4096.0
+#define PROJ3_FINE 8192.0
 #else
 #define PROJ3_FINE 65536.0
 #endif
@@ -76,11 +76,12 @@ __device__ __forceinline__ bool lane_steep(const double b[3]) {
     const double lim = fabs(b[1]) * (1.0 - 1.0 / 1073741824.0);
     return b[1] == 0.0 || !(fabs(b[0]) < lim) || !(fabs(b[2]) < lim);
 }
-// FP: a non-zero minor slope |b_c / b_1| < 2^-16.  The v3 FP takes the crossing point from
-// the high word of its 64-bit plane distance (u = D_hi 2^32 / K), which moves a crossing by
-// < 2^32 / K = 2^-32 / |k| of a slice: fine for |k| >= 2^-16 (< 5e-7 of a ray sum), so warps
-// with a smaller non-zero slope go to the v2 companion like steep ones (rare: a ray within
-// 2^-16 rad of a grid axis)
+// FP: a non-zero minor slope |b_c / b_1| below 1 / PROJ3_FINE (2^-13).  The v3 FP walks
+// 32-bit plane distances (2^-32 voxel, see walk3_setup), which move a crossing by < N 2^-33 /
+// |k| slices on an N-slice segment: < 2^-31 / |k| of the ray sum per crossing, fine for
+// |k| >= 2^-13; warps with a smaller non-zero slope go to the v2 companion like steep ones
+// (rare: a ray within 2^-13 rad of a grid axis).  (PROJ3_FP32STEP=0: the 64-bit walk with the
+// high-word conversion, whose error 2^-32 / |k| needs only 2^-16.)
 __device__ __forceinline__ bool lane_fine(const double b[3]) {
     const double f = fabs(b[1]) * (1.0 / PROJ3_FINE);
     return (b[0] != 0.0 && fabs(b[0]) < f) || (b[2] != 0.0 && fabs(b[2]) < f);
@@ -623,7 +624,7 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
     const unsigned long long KX = W.KX, KZ = W.KZ;
     // FP (PROJ3_FP32STEP): the plane distances in 2^-32 voxel, D truncated, K rounded; the
     // stepping then drifts < N 2^-33 voxel over N slices, a crossing moves by that / |k| --
-    // below 2^-32 / |k| slices for |k| >= 2^-12 (lane_fine routes smaller slopes to v2)
+    // below 2^-32 / |k| slices for |k| >= 2^-13 (lane_fine routes smaller slopes to v2)
     unsigned DX32 = (unsigned)(DX >> 32), DZ32 = (unsigned)(DZ >> 32);
     const unsigned KX32 = (unsigned)((KX >> 32) + ((KX >> 31) & 1ull));
     const unsigned KZ32 = (unsigned)((KZ >> 32) + ((KZ >> 31) & 1ull));
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(256, PROJ3_MINB) k_project3(const ProjLaunch L
             const bool in = (unsigned)rel <= (unsigned)nk;
             // crossing point u = D / K of each axis (round-to-nearest, <= 1.5 ulp) when its
             // plane distance borrows.  FP: the 32-bit walk (I2FP.U32 on the ALU pipe, no 64-bit
-            // carries; |k| >= 2^-12 here, see lane_fine and walk3_setup); without a crossing u
+            // carries; |k| >= 2^-13 here, see lane_fine and walk3_setup); without a crossing u
             // only has to saturate: the three segments then share voxel o.  (PROJ3_FP32STEP=0:
             // the 64-bit walk with the high-word conversion, for A/B.)
 #if PROJ3_FP32STEP

@@ -137,12 +137,12 @@ def test_operator_parity_rects_and_ragged(bs):
 
 
 def test_operator_parity_small_slopes(bs):
-    """Rays within a hair of a grid axis: minor slopes |k| = 0 and 3e-6 .. 2.3e-4 (below the
-    v3 FP's limit 2^-12: the FP warp goes to the v2 companion, lane_fine) and 2.5e-4 .. 1e-3
-    (the v3 FP steps 32-bit plane distances, a crossing moves by < 2^-32/|k| of a slice) over
-    1024-slice walks, detector offsets on and next to voxel planes, random x (large neighbour
-    differences): FP and BP per ray / voxel against the oracle."""
-    ks = [0.0, 3e-6, 1.4e-5, 6e-5, 2.3e-4, 2.5e-4, 3e-4, 6e-4, 1e-3, -2.6e-4, -4e-6]
+    """Rays within a hair of a grid axis: minor slopes |k| = 0 and 3e-6 .. 1.2e-4 (below the
+    v3 FP's limit 2^-13: the FP warp goes to the v2 companion, lane_fine) and 1.3e-4 .. 1e-3
+    (the v3 FP steps 32-bit plane distances, a crossing moves by < N 2^-33/|k| of a slice on
+    an N-slice segment) over 1024-slice walks, detector offsets on and next to voxel planes,
+    random x (large neighbour differences): FP and BP per ray / voxel against the oracle."""
+    ks = [0.0, 3e-6, 1.4e-5, 6e-5, 1.2e-4, 1.3e-4, 2.5e-4, 3e-4, 6e-4, 1e-3, -1.3e-4, -4e-6]
     nu = 91
     vecs = np.zeros((len(ks), 12))
     for i, k in enumerate(ks):
