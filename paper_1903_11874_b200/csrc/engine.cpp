@@ -182,6 +182,9 @@ struct bsgd_ctx_s {
         d_normsq0 = dnew<double>(M);
     }
     int* d_rows_tmp = nullptr;         // M ints: a row-block list for one launch
+    uint2* v2_list = nullptr;          // ProjLaunch::v2_list (the v2 companion's warps)
+    unsigned* v2_count = nullptr;
+    long long v2_cap = 0;
     double* d_red = nullptr;           // 8 doubles scratch
     double* d_log = nullptr;           // per-epoch [obj, rmse] scratch
     long long d_log_cap = 0;
@@ -478,6 +481,21 @@ struct bsgd_ctx_s {
         L.accumulate = accumulate;
         L.visits = (mode == PROJ_COUNT) ? count_target : nullptr;
         L.det_scale = d_det_scale;
+        // the warps k_project3 hands to the v2 companion are listed (capacity: every warp of
+        // the launch); BSGD_V2_LIST=0 keeps the grid companion (A/B)
+        static const bool v2l = !(getenv("BSGD_V2_LIST") && atoi(getenv("BSGD_V2_LIST")) == 0);
+        L.v2_list = nullptr;
+        L.v2_count = nullptr;
+        if (v2l) {
+            const long long warps = (long long)nbands * ns * L.n_chunks * nb * 8;
+            if (warps > v2_cap) {
+                v2_list = dnew<uint2>(warps, false);
+                v2_cap = warps;
+            }
+            if (!v2_count) v2_count = dnew<unsigned>(1);
+            L.v2_list = v2_list;
+            L.v2_count = v2_count;
+        }
         if (off > tab_bytes) fail(BSGD_E_CONTRACT, "launch table overflow");
         BSGD_CUDA(cudaMemcpyAsync(d_tab + tab_off, staging.data() + tab_off, off - tab_off,
                                   cudaMemcpyHostToDevice, st));

@@ -93,6 +93,9 @@ struct ProjLaunch {
     unsigned long long* visits;  // nullable counter
     const float* det_scale;    // PROJ_BPD: device scalar S (a power of two); the BP targets
                                // are then int64 fixed-point accumulators (value * S)
+    uint2* v2_list;            // the warps k_project3 leaves to the v2 companion: (blockIdx.x,
+    unsigned* v2_count;        //   blockIdx.z << 3 | warp), appended by k_project3; capacity =
+                               //   the launch's warps (grid.x grid.z 8); nullptr: grid companion
 };
 
 // PROJ_BPD: the BP with order-independent (deterministic) 64-bit fixed-point reductions

@@ -150,25 +150,27 @@ __device__ __forceinline__ bool clip(const double a[3], const double b[3], const
 // common case (at most one x and one z plane crossing inside the slice: up to three
 // segments, their loads issued together), a rare general loop for further crossings,
 // 32-bit voxel offsets and fp32 slice sums flushed into an fp64 accumulator.
-template <int MODE, bool STEEP_ONLY = false>
-__global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
+// (one warp's work: the warp of CTA (bidx, bidz) whose thread index is tidx; warp-independent)
+template <int MODE, bool STEEP_ONLY>
+__device__ __forceinline__ void project2_body(const ProjLaunch& L, const unsigned bidx, const unsigned bidz,
+                                              const int tidx) {
     // band-major CTA order: blockIdx.x = (band * n_slots + slot) * n_chunks + chunk, so the
     // CTAs resident at any time cover the same detector-row band of consecutive views
     // (rays of one band cross the same z-range of the volume -> L2 reuse across views).
-    const BlockDesc& B = L.blocks[blockIdx.z];
-    unsigned bid = blockIdx.x;
+    const BlockDesc& B = L.blocks[bidz];
+    unsigned bid = bidx;
     const int chunk = (int)(bid % (unsigned)L.n_chunks);
     bid /= (unsigned)L.n_chunks;
     const int slot = (int)(bid % (unsigned)L.n_slots);
     const int band = B.band_lo + (int)(bid / (unsigned)L.n_slots);
-    const int4 rc = L.rects[(size_t)blockIdx.z * L.n_slots + slot];
+    const int4 rc = L.rects[(size_t)bidz * L.n_slots + slot];
     const int r0 = max(rc.z, band * L.rows_per_band), r1 = min(rc.w, band * L.rows_per_band + L.rows_per_band);
     const int w = rc.y - rc.x;
     if (r0 >= r1 || w <= 0) return;
     const int nrect = (r1 - r0) * w;
-    const int base = chunk * (int)blockDim.x;
+    const int base = chunk * 256;
     if (base >= nrect) return;                       // uniform over the CTA
-    const int tid = base + (int)threadIdx.x;
+    const int tid = base + tidx;
     const bool inrect = tid < nrect;
     const int iu = rc.x + (inrect ? tid % w : 0);
     const int iv = r0 + (inrect ? tid / w : 0);
@@ -346,7 +348,25 @@ __global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
     }
     if (MODE == PROJ_COUNT && L.visits) {   // per (block, slot) counters
         unsigned int s = __reduce_add_sync(0xffffffffu, nvis);
-        if ((threadIdx.x & 31) == 0 && s) atomicAdd(L.visits + (size_t)blockIdx.z * L.n_slots + slot, (unsigned long long)s);
+        if ((tidx & 31) == 0 && s) atomicAdd(L.visits + (size_t)bidz * L.n_slots + slot, (unsigned long long)s);
+    }
+}
+
+template <int MODE, bool STEEP_ONLY = false>
+__global__ void __launch_bounds__(256, 4) k_project2(const ProjLaunch L) {
+    project2_body<MODE, STEEP_ONLY>(L, blockIdx.x, blockIdx.z, (int)threadIdx.x);
+}
+
+// The v2 companion over the warps k_project3 listed (persistent warps striding the list):
+// only those warps pay the v2 set-up, instead of every warp of the launch grid.
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) k_project2_list(const ProjLaunch L) {
+    const unsigned n = *L.v2_count;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += nw) {   // warp-uniform
+        const uint2 q = L.v2_list[e];
+        project2_body<MODE, true>(L, q.x, q.y >> 3, (int)((q.y & 7u) * 32u + lane));
     }
 }
 
@@ -502,8 +522,11 @@ __device__ __forceinline__ bool walk3_setup(const ProjLaunch& L, const BlockDesc
     // (source or detector within the block: no face to exit through, the zero border would
     // not absorb the rest of the slice)
     if (__any_sync(0xffffffffu, hit && (lane_steep(b) || (MODE == PROJ_FP && lane_fine(b)) || amin == 0.0 ||
-                                        amax == 1.0)))
+                                        amax == 1.0))) {
+        if (L.v2_list && (threadIdx.x & 31) == 0)   // hand the warp to the list companion
+            L.v2_list[atomicAdd(L.v2_count, 1u)] = make_uint2(blockIdx.x, (blockIdx.z << 3) | (threadIdx.x >> 5));
         return false;
+    }
     const double blen = sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]);
     float rs = 0.f;
     W.S = MODE == PROJ_BPD ? *L.det_scale : 0.f;
@@ -812,15 +835,22 @@ void launch_project(int mode, const ProjLaunch& L, cudaStream_t st) {
         note_launch();
         return;
     }
-    // v3 (default), then the v2 traversal for the warps v3 skipped (same launch geometry,
-    // same predicate)
+    // v3 (default), then the v2 traversal for the warps v3 skipped (listed by v3, or the same
+    // launch geometry and predicate when no list is given)
+    if (L.v2_list) BSGD_CUDA(cudaMemsetAsync(L.v2_count, 0, sizeof(unsigned), st));
     if (mode == PROJ_FP) k_project3<PROJ_FP><<<grid, 256, 0, st>>>(L);
     else if (mode == PROJ_BP) k_project3<PROJ_BP><<<grid, 256, 0, st>>>(L);
     else if (mode == PROJ_BPD) k_project3<PROJ_BPD><<<grid, 256, 0, st>>>(L);
     else k_project3<PROJ_COUNT><<<grid, 256, 0, st>>>(L);
     BSGD_CUDA(cudaGetLastError());
     note_launch();
-    if (mode == PROJ_FP) k_project2<PROJ_FP, true><<<grid, 256, 0, st>>>(L);
+    if (L.v2_list) {   // only the listed warps
+        const dim3 pg(148 * 4);
+        if (mode == PROJ_FP) k_project2_list<PROJ_FP><<<pg, 256, 0, st>>>(L);
+        else if (mode == PROJ_BP) k_project2_list<PROJ_BP><<<pg, 256, 0, st>>>(L);
+        else if (mode == PROJ_BPD) k_project2_list<PROJ_BPD><<<pg, 256, 0, st>>>(L);
+        else k_project2_list<PROJ_COUNT><<<pg, 256, 0, st>>>(L);
+    } else if (mode == PROJ_FP) k_project2<PROJ_FP, true><<<grid, 256, 0, st>>>(L);
     else if (mode == PROJ_BP) k_project2<PROJ_BP, true><<<grid, 256, 0, st>>>(L);
     else if (mode == PROJ_BPD) k_project2<PROJ_BPD, true><<<grid, 256, 0, st>>>(L);
     else k_project2<PROJ_COUNT, true><<<grid, 256, 0, st>>>(L);
